@@ -1,0 +1,142 @@
+"""CPU oracle for the Turbo MCKP scheduler hot path -- TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+legs may import this package. The product package paper_2207_00172_b200 never
+imports it and shares no code with it (see oracle/turbo_oracle.c header).
+
+Functions follow /root/reference/PAPER.md §5 (lines 491-545) and §6.4 (line 858);
+see turbo_oracle.c for the per-function citations and DESIGN.md for readings.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from typing import Optional
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "turbo_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with plain gcc -O2 (no intrinsics)."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-std=c99", "-shared", "-fPIC", "-pthread",
+                               "-o", _LIB, _SRC])
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        _lib = ctypes.CDLL(_LIB)
+    return _lib
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _i32(a):
+    return np.ascontiguousarray(a, dtype=np.int32)
+
+
+def _i64(a):
+    return np.ascontiguousarray(a, dtype=np.int64)
+
+
+def profiles_flat(wl):
+    """Concatenate profile tables: (gain, cost, offset[P], C[P], K[P])."""
+    gain = np.concatenate([_i32(g) for g in wl.profiles_gain]) if wl.profiles_gain else np.zeros(0, np.int32)
+    cost = np.concatenate([_i32(c) for c in wl.profiles_cost]) if wl.profiles_cost else np.zeros(0, np.int32)
+    sizes = np.array([len(g) for g in wl.profiles_gain], dtype=np.int64)
+    off = np.zeros(len(sizes), dtype=np.int64)
+    if len(sizes) > 1:
+        off[1:] = np.cumsum(sizes[:-1])
+    C = np.array([s[0] for s in wl.profiles_shape], dtype=np.int32)
+    K = np.array([s[1] for s in wl.profiles_shape], dtype=np.int32)
+    return _i32(gain), _i32(cost), off, C, K
+
+
+def option_offsets(num_frames, K):
+    """first_option[w] = sum_{w' < w} N_w' K_w' (layout bookkeeping only)."""
+    n = np.asarray(num_frames, dtype=np.int64) * np.asarray(K, dtype=np.int64)
+    off = np.zeros(len(n), dtype=np.int64)
+    if len(n) > 1:
+        off[1:] = np.cumsum(n[:-1])
+    return off, int(n.sum())
+
+
+def budget(capacity, num_frames, base_cost) -> np.ndarray:
+    lib = _load()
+    cap, nf = _i32(capacity), _i32(num_frames)
+    out = np.zeros(len(nf), dtype=np.int32)
+    lib.oracle_budget(ctypes.c_int32(len(nf)), _p(cap), _p(nf), ctypes.c_int32(int(base_cost)), _p(out))
+    return out
+
+
+def lookup(wl):
+    """a2: per-frame option tables. Returns (opt_gain, opt_cost, first_option, bad_frame)."""
+    lib = _load()
+    gain, cost, off, C, K = profiles_flat(wl)
+    Kw = K[wl.profile]
+    first_option, total = option_offsets(wl.num_frames, Kw)
+    og = np.zeros(max(total, 1), dtype=np.int32)
+    oc = np.zeros(max(total, 1), dtype=np.int32)
+    cls = np.ascontiguousarray(wl.class_id, dtype=np.uint8)
+    lib.oracle_lookup.restype = ctypes.c_int64
+    bad = lib.oracle_lookup(ctypes.c_int32(wl.num_windows), _p(_i32(wl.num_frames)), _p(_i32(wl.profile)),
+                            _p(cls), _p(gain), _p(cost), _p(off), _p(C), _p(K), _p(og), _p(oc))
+    return og[:total], oc[:total], first_option, int(bad)
+
+
+def plan(num_frames, budget_, K, opt_gain, opt_cost, mode: str = "table",
+         threads: Optional[int] = None):
+    """a3-a5 per window. mode: 'table' | 'brute' | 'value' (no exits)."""
+    lib = _load()
+    nf, bud, Kw = _i32(num_frames), _i32(budget_), _i32(K)
+    W = len(nf)
+    ff = np.zeros(W, dtype=np.int64)
+    if W > 1:
+        ff[1:] = np.cumsum(nf[:-1].astype(np.int64))
+    fo, total = option_offsets(nf, Kw)
+    F = int(nf.astype(np.int64).sum())
+    exits = np.zeros(max(F, 1), dtype=np.uint8)
+    bg = np.zeros(max(W, 1), dtype=np.int64)
+    bc = np.zeros(max(W, 1), dtype=np.int64)
+    fe = np.zeros(max(W, 1), dtype=np.uint8)
+    og = _i32(opt_gain) if total else np.zeros(1, np.int32)
+    oc = _i32(opt_cost) if total else np.zeros(1, np.int32)
+    m = {"table": 0, "brute": 1, "value": 2}[mode]
+    nt = threads or min(os.cpu_count() or 1, 64)
+    err = lib.oracle_plan_batch(ctypes.c_int32(W), _p(nf), _p(bud), _p(Kw), _p(ff), _p(fo), _p(og), _p(oc),
+                                _p(exits), _p(bg), _p(bc), _p(fe), ctypes.c_int32(m), ctypes.c_int32(nt))
+    if err:
+        raise RuntimeError(f"oracle_plan_batch failed: {err}")
+    return exits[:F], bg[:W], bc[:W], fe[:W]
+
+
+def stats(num_frames, class_id, exits, best_gain, best_cost, feasible) -> np.ndarray:
+    lib = _load()
+    out = np.zeros(181, dtype=np.int64)
+    nf = _i32(num_frames)
+    lib.oracle_stats(ctypes.c_int32(len(nf)), _p(nf), _p(np.ascontiguousarray(class_id, dtype=np.uint8)),
+                     _p(np.ascontiguousarray(exits, dtype=np.uint8)), _p(_i64(best_gain)), _p(_i64(best_cost)),
+                     _p(np.ascontiguousarray(feasible, dtype=np.uint8)), _p(out))
+    return out
+
+
+def run(wl, mode: str = "table", threads: Optional[int] = None) -> dict:
+    """The whole path a1..a6 on one workload."""
+    bud = budget(wl.capacity, wl.num_frames, wl.base_cost)
+    og, oc, fo, bad = lookup(wl)
+    K = wl.num_exits
+    exits, bg, bc, fe = plan(wl.num_frames, bud, K, og, oc, mode, threads)
+    st = stats(wl.num_frames, wl.class_id, exits, bg, bc, fe) if mode != "value" else None
+    return dict(budget=bud, opt_gain=og, opt_cost=oc, first_option=fo, bad_frame=bad,
+                exits=exits, best_gain=bg, best_cost=bc, feasible=fe, stats=st)

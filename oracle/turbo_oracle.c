@@ -1,0 +1,318 @@
+/*
+ * turbo_oracle.c -- CPU ORACLE for the Turbo enhancement-scheduler hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library. The product path
+ * (paper_2207_00172_b200/) never links, imports or calls it, and shares no code,
+ * header, table or constant with it. Inputs come from synth/ (seeded generators).
+ *
+ * Plain, slow, obviously correct: int64 arithmetic, no blocking, no SIMD, one
+ * thread per window (pthreads only ACROSS windows). Each function cites the
+ * passage of /root/reference/PAPER.md (main paper, lines 164-997) it follows;
+ * readings R1..R14 are listed in DESIGN.md.
+ *
+ * Parity pins (tests/test_oracle.py, -m "not gpu"): brute-force enumeration on
+ * tiny windows (an independent pure-Python enumeration too), the worked instance
+ * derived in SPEC.md:269 (tests/golden/), closed forms (unconstrained budget,
+ * B = 0, K = 2 uniform-cost sort, K = 2 textbook 0/1 knapsack), invariants
+ * (C* <= B, budget monotonicity PAPER.md:640, permutation invariance of G*).
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <pthread.h>
+
+#define ORACLE_NEG_INF INT64_MIN  /* "no plan of cost <= b exists" */
+
+/* ------------------------------------------------------------------ a1: budget
+ * PAPER.md:374 (§3) and :22 (draft A): the budget is set by "quantifying the
+ * number of frames reaching the object detector". Reading R3:
+ *   B_w = max(0, floor(T_w/q) - m_w * u0),  u0 = ceil(I_0/q),  I_0 = mu_D + nu_0
+ * i.e. the idle GPU time left after the mandatory detection of the m_w frames. */
+void oracle_budget(int32_t num_windows, const int32_t *capacity, const int32_t *num_frames,
+                   int32_t base_cost, int32_t *budget_out)
+{
+    for (int32_t w = 0; w < num_windows; ++w) {
+        int64_t b = (int64_t)capacity[w] - (int64_t)num_frames[w] * (int64_t)base_cost;
+        budget_out[w] = (int32_t)(b < 0 ? 0 : b);
+    }
+}
+
+/* ------------------------------------------------------------------ a2: lookup
+ * PAPER.md:519-525 (§5.2): frame x with estimated difficulty theta'_x takes, for
+ * level kappa, accuracy gain P_kappa^{theta'_x} (§5.1: profile per
+ * bucket of width 0.1) and latency I_kappa. The per-frame
+ * option table is therefore the profile row of the frame's class:
+ *   opt_gain[x][k] = gain[class_x][k],  opt_cost[x][k] = cost[class_x][k].
+ * Profiles are concatenated: profile p has C_p rows of K_p entries at prof_off[p].
+ * Returns -1, or the smallest frame index whose class is out of range (its row is
+ * then left zero). */
+int64_t oracle_lookup(int32_t num_windows, const int32_t *num_frames, const int32_t *profile,
+                      const uint8_t *class_id, const int32_t *prof_gain, const int32_t *prof_cost,
+                      const int64_t *prof_off, const int32_t *prof_C, const int32_t *prof_K,
+                      int32_t *opt_gain, int32_t *opt_cost)
+{
+    int64_t frame = 0, opt = 0, bad = -1;
+    for (int32_t w = 0; w < num_windows; ++w) {
+        int32_t p = profile[w], K = prof_K[p], C = prof_C[p];
+        for (int32_t i = 0; i < num_frames[w]; ++i, ++frame) {
+            int32_t cls = class_id[frame];
+            for (int32_t k = 0; k < K; ++k, ++opt) {
+                if (cls < C) {
+                    opt_gain[opt] = prof_gain[prof_off[p] + (int64_t)cls * K + k];
+                    opt_cost[opt] = prof_cost[prof_off[p] + (int64_t)cls * K + k];
+                } else {
+                    opt_gain[opt] = 0;
+                    opt_cost[opt] = 0;
+                    if (bad < 0) bad = frame;
+                }
+            }
+        }
+    }
+    return bad;
+}
+
+/* ------------------------------------------------------------------ a3-a5: exact plan
+ * The optimisation of PAPER.md:519-525 (§5.2, Eq. max / s.t.):
+ *     max sum_x P_{kappa_x}^{theta'_x}   s.t.  f(sum I_kappa) <= T
+ * with f = plain sum of per-frame incremental costs (reading R1: a multiple-choice
+ * knapsack), computed EXACTLY, i.e. the paper's brute-force "upper" (PAPER.md:858,
+ * §6.4). The result is the unique maximum of the total order (reading R7):
+ *   (1) larger total gain, (2) then smaller total cost, (3) then the
+ *   lexicographically smaller exit vector (frame 0 most significant).
+ * No feasible plan (reading R8): all exits 0, gain = sum g_i0, cost = sum c_i0,
+ * feasible = 0. Empty window: gain 0, cost 0, feasible. */
+
+/* Brute force: enumerate all K^N plans in lexicographic order (frame N-1 fastest);
+ * keep a plan only if strictly better in (gain, -cost), so the first one met among
+ * equals -- the lexicographically smallest -- survives. */
+int oracle_plan_brute(int32_t N, int32_t K, const int32_t *g, const int32_t *c, int32_t B,
+                      uint8_t *exits, int64_t *best_gain, int64_t *best_cost, uint8_t *feasible)
+{
+    int32_t p[64];
+    if (N > 64) return -1;
+    int found = 0;
+    int64_t bg = 0, bc = 0;
+    for (int32_t i = 0; i < N; ++i) p[i] = 0;
+    for (;;) {
+        int64_t gain = 0, cost = 0;
+        for (int32_t i = 0; i < N; ++i) {
+            gain += g[(int64_t)i * K + p[i]];
+            cost += c[(int64_t)i * K + p[i]];
+        }
+        if (cost <= B && (!found || gain > bg || (gain == bg && cost < bc))) {
+            found = 1;
+            bg = gain;
+            bc = cost;
+            for (int32_t i = 0; i < N; ++i) exits[i] = (uint8_t)p[i];
+        }
+        int32_t i = N - 1;                 /* odometer: last frame fastest */
+        while (i >= 0 && ++p[i] == K) p[i--] = 0;
+        if (i < 0) break;
+    }
+    if (!found) {
+        bg = 0;
+        bc = 0;
+        for (int32_t i = 0; i < N; ++i) {
+            exits[i] = 0;
+            bg += g[(int64_t)i * K];
+            bc += c[(int64_t)i * K];
+        }
+    }
+    *best_gain = bg;
+    *best_cost = bc;
+    *feasible = (uint8_t)found;
+    return 0;
+}
+
+/* Suffix table: T[i][b] = best gain of frames i..N-1 using total cost <= b
+ * (-inf if none), T[N][b] = 0. G* = T[0][B]; C* = min{b : T[0][b] = G*};
+ * forward reconstruction by value matching: at frame i with remaining budget r
+ * and target value V take the smallest k with c_ik <= r and
+ * g_ik + T[i+1][r - c_ik] = V. Table memory: (N+1)(B+1) int64. */
+int oracle_plan_table(int32_t N, int32_t K, const int32_t *g, const int32_t *c, int32_t B,
+                      uint8_t *exits, int64_t *best_gain, int64_t *best_cost, uint8_t *feasible)
+{
+    int64_t W = (int64_t)B + 1;
+    int64_t *T = (int64_t *)malloc(sizeof(int64_t) * (size_t)(N + 1) * (size_t)W);
+    if (!T) return -1;
+    for (int64_t b = 0; b < W; ++b) T[(int64_t)N * W + b] = 0;
+    for (int32_t i = N - 1; i >= 0; --i) {
+        for (int64_t b = 0; b < W; ++b) {
+            int64_t best = ORACLE_NEG_INF;
+            for (int32_t k = 0; k < K; ++k) {
+                int64_t ck = c[(int64_t)i * K + k];
+                if (ck > b) continue;
+                int64_t nxt = T[(int64_t)(i + 1) * W + (b - ck)];
+                if (nxt == ORACLE_NEG_INF) continue;
+                int64_t v = g[(int64_t)i * K + k] + nxt;
+                if (v > best) best = v;
+            }
+            T[(int64_t)i * W + b] = best;
+        }
+    }
+    int64_t G = T[B];
+    if (G == ORACLE_NEG_INF) {
+        int64_t bg = 0, bc = 0;
+        for (int32_t i = 0; i < N; ++i) {
+            exits[i] = 0;
+            bg += g[(int64_t)i * K];
+            bc += c[(int64_t)i * K];
+        }
+        *best_gain = bg;
+        *best_cost = bc;
+        *feasible = 0;
+        free(T);
+        return 0;
+    }
+    int64_t Cs = 0;
+    while (T[Cs] != G) ++Cs;
+    int64_t r = Cs, V = G;
+    for (int32_t i = 0; i < N; ++i) {
+        int32_t pick = -1;
+        for (int32_t k = 0; k < K && pick < 0; ++k) {
+            int64_t ck = c[(int64_t)i * K + k];
+            if (ck > r) continue;
+            int64_t nxt = T[(int64_t)(i + 1) * W + (r - ck)];
+            if (nxt == ORACLE_NEG_INF) continue;
+            if (g[(int64_t)i * K + k] + nxt == V) pick = k;
+        }
+        if (pick < 0) { free(T); return -2; }   /* cannot happen: table inconsistent */
+        exits[i] = (uint8_t)pick;
+        V -= g[(int64_t)i * K + pick];
+        r -= c[(int64_t)i * K + pick];
+    }
+    *best_gain = G;
+    *best_cost = Cs;
+    *feasible = 1;
+    free(T);
+    return 0;
+}
+
+/* Value-only optimum for windows whose full table would not fit in memory:
+ * the same recurrence over two rolling rows; returns G*, C*, feasibility. */
+int oracle_optimum_rolling(int32_t N, int32_t K, const int32_t *g, const int32_t *c, int32_t B,
+                           int64_t *best_gain, int64_t *best_cost, uint8_t *feasible)
+{
+    int64_t W = (int64_t)B + 1;
+    int64_t *nxt = (int64_t *)malloc(sizeof(int64_t) * (size_t)W);
+    int64_t *cur = (int64_t *)malloc(sizeof(int64_t) * (size_t)W);
+    if (!nxt || !cur) { free(nxt); free(cur); return -1; }
+    for (int64_t b = 0; b < W; ++b) nxt[b] = 0;
+    for (int32_t i = N - 1; i >= 0; --i) {
+        for (int64_t b = 0; b < W; ++b) {
+            int64_t best = ORACLE_NEG_INF;
+            for (int32_t k = 0; k < K; ++k) {
+                int64_t ck = c[(int64_t)i * K + k];
+                if (ck > b || nxt[b - ck] == ORACLE_NEG_INF) continue;
+                int64_t v = g[(int64_t)i * K + k] + nxt[b - ck];
+                if (v > best) best = v;
+            }
+            cur[b] = best;
+        }
+        int64_t *t = nxt; nxt = cur; cur = t;
+    }
+    int64_t G = nxt[B];
+    if (G == ORACLE_NEG_INF) {
+        int64_t bg = 0, bc = 0;
+        for (int32_t i = 0; i < N; ++i) { bg += g[(int64_t)i * K]; bc += c[(int64_t)i * K]; }
+        *best_gain = bg; *best_cost = bc; *feasible = 0;
+    } else {
+        int64_t Cs = 0;
+        while (nxt[Cs] != G) ++Cs;
+        *best_gain = G; *best_cost = Cs; *feasible = 1;
+    }
+    free(nxt); free(cur);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ batch driver
+ * Windows are independent (one plan per window of m frames); the
+ * driver only splits the window list across threads. mode: 0 = table, 1 = brute,
+ * 2 = value-only (exits left untouched). */
+typedef struct {
+    int32_t num_windows, mode, nthreads, tid;
+    const int32_t *num_frames, *budget, *K;
+    const int64_t *first_frame, *first_option;
+    const int32_t *opt_gain, *opt_cost;
+    uint8_t *exits, *feasible;
+    int64_t *best_gain, *best_cost;
+    int err;
+} oracle_job_t;
+
+static void *oracle_worker(void *arg)
+{
+    oracle_job_t *j = (oracle_job_t *)arg;
+    for (int32_t w = j->tid; w < j->num_windows; w += j->nthreads) {
+        const int32_t *g = j->opt_gain + j->first_option[w];
+        const int32_t *c = j->opt_cost + j->first_option[w];
+        uint8_t *ex = j->exits ? j->exits + j->first_frame[w] : NULL;
+        int r;
+        if (j->mode == 1)
+            r = oracle_plan_brute(j->num_frames[w], j->K[w], g, c, j->budget[w], ex,
+                                  &j->best_gain[w], &j->best_cost[w], &j->feasible[w]);
+        else if (j->mode == 2)
+            r = oracle_optimum_rolling(j->num_frames[w], j->K[w], g, c, j->budget[w],
+                                       &j->best_gain[w], &j->best_cost[w], &j->feasible[w]);
+        else
+            r = oracle_plan_table(j->num_frames[w], j->K[w], g, c, j->budget[w], ex,
+                                  &j->best_gain[w], &j->best_cost[w], &j->feasible[w]);
+        if (r) j->err = r;
+    }
+    return NULL;
+}
+
+int oracle_plan_batch(int32_t num_windows, const int32_t *num_frames, const int32_t *budget,
+                      const int32_t *K, const int64_t *first_frame, const int64_t *first_option,
+                      const int32_t *opt_gain, const int32_t *opt_cost, uint8_t *exits,
+                      int64_t *best_gain, int64_t *best_cost, uint8_t *feasible,
+                      int32_t mode, int32_t nthreads)
+{
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    oracle_job_t jobs[256];
+    pthread_t th[256];
+    for (int32_t t = 0; t < nthreads; ++t) {
+        oracle_job_t j = {num_windows, mode, nthreads, t, num_frames, budget, K, first_frame,
+                          first_option, opt_gain, opt_cost, exits, feasible, best_gain, best_cost, 0};
+        jobs[t] = j;
+    }
+    if (nthreads == 1) {
+        oracle_worker(&jobs[0]);
+        return jobs[0].err;
+    }
+    for (int32_t t = 0; t < nthreads; ++t) pthread_create(&th[t], NULL, oracle_worker, &jobs[t]);
+    int err = 0;
+    for (int32_t t = 0; t < nthreads; ++t) {
+        pthread_join(th[t], NULL);
+        if (jobs[t].err) err = jobs[t].err;
+    }
+    return err;
+}
+
+/* ------------------------------------------------------------------ a6: statistics
+ * Totals and histograms of the plans (the quantities PAPER.md §6 reports per run:
+ * accuracy gain and enhancement usage), layout int64[181]:
+ *   [0,16)    exits histogram (frames per chosen level kappa)
+ *   [16,176)  class x exit histogram, classes 0..9 (PAPER.md:511 buckets), row-major
+ *   176 sum of best_gain, 177 sum of best_cost, 178 #windows, 179 #frames,
+ *   180 #infeasible windows. */
+void oracle_stats(int32_t num_windows, const int32_t *num_frames, const uint8_t *class_id,
+                  const uint8_t *exits, const int64_t *best_gain, const int64_t *best_cost,
+                  const uint8_t *feasible, int64_t *stats)
+{
+    memset(stats, 0, sizeof(int64_t) * 181);
+    int64_t f = 0;
+    for (int32_t w = 0; w < num_windows; ++w) {
+        for (int32_t i = 0; i < num_frames[w]; ++i, ++f) {
+            int k = exits[f] & 15;
+            stats[k] += 1;
+            if (class_id[f] < 10) stats[16 + class_id[f] * 16 + k] += 1;
+        }
+        stats[176] += best_gain[w];
+        stats[177] += best_cost[w];
+        stats[178] += 1;
+        stats[179] += num_frames[w];
+        stats[180] += feasible[w] ? 0 : 1;
+    }
+}

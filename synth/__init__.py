@@ -1,0 +1,36 @@
+"""Seeded synthetic workloads for the Turbo MCKP scheduler hot path.
+
+This module is the ONLY code shared between the CPU oracle (``oracle/``) and the
+CUDA path (``paper_2207_00172_b200/``). It produces *inputs* only -- difficulty
+class ids, offline profile tables (gain, cost), and window metadata -- and holds
+none of the scheduler's arithmetic (no budget derivation, no lookup, no DP).
+
+Generator: a counter-based splitmix64 (Steele et al.) keyed by
+(seed, stream, counter), vectorised with numpy uint64 wrap-around arithmetic,
+so any window's inputs can be regenerated independently of the others (this is
+what lets each GPU rank build its own shard with no scatter).
+
+Workload recipe:
+  * classes: C = 10 difficulty buckets of width 0.1 (§5.1),
+    class 9 hardest; P(c) ∝ exp(-0.35 c) ("a small portion of frames" are hard,
+    PAPER.md:203, :293).
+  * gains (units of 0.01 mAP point): g[c][0] = 0 (P_0 = 0);
+    g[c][k] = round(1400 * 0.604**(9-c) * (0.561 + 0.439 (k-1)/(K-2))),
+    calibrated on Appendix B (kappa5-kappa1 = 6.15 pts,
+    bucket 9 - bucket 8 = 5.54 pts).
+  * costs (incremental GPU-time units, class independent):
+    c_k = ceil(c_max k / (K-1)), c_max = ceil(3 B / N).
+  * tie-heavy parity profiles: gains U{-2..8}, costs U{0..4}, 30% of profiles
+    with c_0 > 0 (exercise infeasibility), non-monotone rows.
+"""
+from .rng import mix64, rand_u64, rand_uniform, rand_int  # noqa: F401
+from .workloads import (  # noqa: F401
+    Workload,
+    CONFIGS,
+    make_config,
+    make_tie_heavy,
+    make_adversarial,
+    paper_gain_table,
+    regular_costs,
+    concat_workloads,
+)
