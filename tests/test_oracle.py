@@ -341,7 +341,7 @@ def test_adversarial_cases(oracle_lib):
     K = wl.num_exits
     for w in range(wl.num_windows):
         N = int(wl.num_frames[w])
-        if K[w] ** N > 200000:
+        if int(K[w]) ** N > 200000:
             continue
         g = og[fo[w]: fo[w] + N * K[w]].reshape(N, K[w])
         c = oc[fo[w]: fo[w] + N * K[w]].reshape(N, K[w])
