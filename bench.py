@@ -1,0 +1,372 @@
+#!/usr/bin/env python
+"""Benchmark of the Turbo MCKP scheduler hot path on B200 (one process per GPU).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl turbo|reference]
+    torchrun --nproc-per-node N ... bench.py --gpus N      (N > 1, NCCL allreduce of the stats)
+
+A step is one pass of the whole path over the rank's windows:
+turbo_profile_lookup (a1+a2) -> turbo_mckp_solve (a3+a4+a5, fused) -> turbo_stats (a6)
+[-> allreduce of the int64[181] stats over NCCL when N > 1]. Inputs are generated on the
+host from the seeded generator (synth/) and copied to HBM before timing. Weak scaling: each
+rank plans its own windows (window ids offset by rank), per-GPU work fixed.
+The metric is BASELINE.json's: DP cell-updates/s (sum over windows of N_w (B_w + 1) per
+step, whole job) -- windows/s is reported beside it.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MCKP DP cell-updates/s and windows/s at 1/2/4/8 B200 (% of roofline)"
+UNIT = "cell-updates/s"
+
+# per-GPU window shares (weak scaling); c3's share is its 8-GPU shard
+WORKLOADS = {
+    "c1": dict(config=1, per_gpu=1, desc="1 window x 30 frames, K=4, B=120"),
+    "c2": dict(config=2, per_gpu=1024, desc="1024 streams x 1 s windows at 30 fps (N=30), K=5, B=1000 per GPU"),
+    "c3": dict(config=3, per_gpu=8192, desc="8192 windows x 300 frames, K=8, B=4096 per GPU (c3 = 65536 over 8 GPUs)"),
+    "c5": dict(config=5, per_gpu=2048, desc="mixed sweep: K 2-16, B 64-16384, N 30-300, skewed classes; 2048 windows per GPU"),
+}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_workload(name: str, rank: int):
+    import synth
+    spec = WORKLOADS[name]
+    return synth.make_config(spec["config"], window_offset=rank * spec["per_gpu"], num_windows=spec["per_gpu"])
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.12)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.thread.join(timeout=2)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle legs
+def oracle_rate(wl, budget_s: float, threads: int):
+    """Oracle (as it stands) on repetitions of the workload's windows until budget_s elapsed."""
+    import oracle
+    og, oc, _, _ = oracle.lookup(wl)
+    bud = oracle.budget(wl.capacity, wl.num_frames, wl.base_cost)
+    K = wl.num_exits
+    cells = wl.total_cells
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        oracle.plan(wl.num_frames, bud, K, og, oc, "table", threads)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    return cells * reps / el, reps, el
+
+
+def sample_for_oracle(wl, max_cells: float):
+    """A bounded prefix of the workload's windows (whole windows) with <= max_cells cells."""
+    cells = (wl.num_frames.astype(np.int64) * (wl.budget.astype(np.int64) + 1))
+    cum = np.cumsum(cells)
+    n = int(np.searchsorted(cum, max_cells, side="right"))
+    n = max(1, min(n, wl.num_windows))
+    return wl.subset(0, n)
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    name = args.workload
+    wl = make_workload(name, 0)
+    threads = os.cpu_count() or 1
+    # each step: a bounded sample (whole windows) of ~0.15 s of oracle work on all cores
+    sub = sample_for_oracle(wl, 2.0e8 * threads * 0.15)
+    import oracle
+    og, oc, _, _ = oracle.lookup(sub)
+    bud = oracle.budget(sub.capacity, sub.num_frames, sub.base_cost)
+    K = sub.num_exits
+    for _ in range(args.warmup):
+        oracle.plan(sub.num_frames, bud, K, og, oc, "table", threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.plan(sub.num_frames, bud, K, og, oc, "table", threads)
+    el = time.perf_counter() - t0
+    value = sub.total_cells * args.steps / el
+    sample = (f"{sub.num_windows} of {wl.num_windows} windows of {name} per step "
+              f"({sub.total_cells} cells), table DP + reconstruction, gcc -O2, {threads} threads")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (seeded splitmix64, synth/)",
+            "config": {"workload": f"{name}: {WORKLOADS[name]['desc']}", "oracle_sample_windows": sub.num_windows},
+            "windows_per_s": sub.num_windows * args.steps / el,
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def run_turbo(args):
+    import torch
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2207_00172_b200 import build as tbuild, turbo
+    if not os.path.exists(turbo.LIB_PATH):
+        tbuild.build()
+    turbo.load()
+
+    name = args.workload
+    wl = make_workload(name, rank)
+    b = turbo.batch_from_workload(wl, device=dev, with_plan_workspace=not args.fused)
+    stream = torch.cuda.current_stream(dev)
+    fused = args.fused
+    cells = wl.total_cells
+    W = wl.num_windows
+
+    def step(ev_dp=None):
+        b.status.fill_(-1)
+        b.stats.zero_()
+        turbo.profile_lookup(b.shape, b.profiles_dev, b.windows_dev, b.class_id, b.capacity, b.base_cost,
+                             b.opt_gain, b.opt_cost, b.status, stream)
+        if ev_dp is not None:
+            ev_dp[0].record(stream)
+        if fused:
+            turbo.mckp_solve(b.shape, b.windows_dev, b.opt_gain, b.opt_cost, b.solve_ws, b.best_gain, b.best_cost,
+                             b.feasible, b.exit_out, b.status, stream)
+        else:
+            turbo.mckp_plan(b.shape, b.windows_dev, b.opt_gain, b.opt_cost, b.workspace, b.best_gain, b.best_cost,
+                            b.feasible, b.status, stream)
+        if ev_dp is not None:
+            ev_dp[1].record(stream)
+        if not fused:
+            turbo.backtrack(b.shape, b.windows_dev, b.opt_cost, b.workspace, b.best_cost, b.feasible, b.exit_out,
+                            stream)
+        turbo.stats(b.shape, b.windows_dev, b.class_id, b.exit_out, b.best_gain, b.best_cost, b.feasible, b.stats,
+                    stream)
+        if dist is not None:
+            dist.all_reduce(b.stats)
+    launches_per_step = 3 if fused else 4
+
+    # L2 flush buffer (> 126 MB L2) written between timed steps (outside the timed events)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize(dev)
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    evd = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clk = ClockSampler(local)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clk.start()
+    for k in range(args.steps):
+        flush.fill_(k & 0xff)
+        evs[k][0].record(stream)
+        step(evd[k])
+        evs[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    clocks = clk.stop()
+    t_step = sum(a.elapsed_time(bb) for a, bb in evs) / args.steps / 1e3          # s per step (this rank)
+    t_dp = sum(a.elapsed_time(bb) for a, bb in evd) / args.steps / 1e3
+
+    # correctness of the timed run (cheap, rank-local): no status errors
+    st = b.status.cpu().numpy()
+    if st[0] != -1 or st[1] != -1:
+        raise RuntimeError(f"status words set during bench: {st}")
+
+    # ---- e2e through the C ABI with HOST buffers (pinned), H2D inputs + D2H results inside
+    F = int(b.shape.total_frames)
+    h_cls = torch.from_numpy(np.ascontiguousarray(wl.class_id)).pin_memory()
+    h_cap = torch.from_numpy(np.ascontiguousarray(wl.capacity)).pin_memory()
+    h_exits = torch.empty(max(F, 1), dtype=torch.uint8).pin_memory()
+    h_gain = torch.empty(max(W, 1), dtype=torch.int32).pin_memory()
+    h_cost = torch.empty(max(W, 1), dtype=torch.int32).pin_memory()
+    h_feas = torch.empty(max(W, 1), dtype=torch.uint8).pin_memory()
+    h_stats = torch.empty(181, dtype=torch.int64).pin_memory()
+    h2d = F + 4 * W
+    d2h = F + 9 * W + 8 * 181
+
+    def e2e_step():
+        b.class_id[:F].copy_(h_cls, non_blocking=True)
+        b.capacity.copy_(h_cap, non_blocking=True)
+        step()
+        h_exits[:F].copy_(b.exit_out[:F], non_blocking=True)
+        h_gain[:W].copy_(b.best_gain[:W], non_blocking=True)
+        h_cost[:W].copy_(b.best_cost[:W], non_blocking=True)
+        h_feas[:W].copy_(b.feasible[:W], non_blocking=True)
+        h_stats.copy_(b.stats, non_blocking=True)
+
+    e2e_steps = max(1, min(args.steps, 50))
+    for _ in range(3):
+        e2e_step()
+    torch.cuda.synchronize(dev)
+    eve = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(e2e_steps)]
+    if dist is not None:
+        dist.barrier()
+    for k in range(e2e_steps):
+        flush.fill_(k & 0xff)
+        eve[k][0].record(stream)
+        e2e_step()
+        eve[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    t_e2e = sum(a.elapsed_time(bb) for a, bb in eve) / e2e_steps / 1e3
+
+    # ---- max over ranks
+    if dist is not None:
+        tt = torch.tensor([t_step, t_dp, t_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step, t_dp, t_e2e = tt.tolist()
+    N = ws
+    total_cells = cells * N
+    value = total_cells / t_step
+
+    # ---- roofline of the dominant kernel (the DP): shared-memory bound
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except Exception:
+        pass
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+    smem_peak = nsm * 128 * sm_max * 1e6 / 1e9                   # GB/s: 32 banks x 4 B per clock per SM
+    Kw = wl.num_exits.astype(np.int64)
+    alg_bytes = int((wl.num_frames.astype(np.int64) * (wl.budget.astype(np.int64) + 1) * (4 * Kw + 4)).sum())
+    achieved = alg_bytes / t_dp / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", f"traffic_{name}.json")
+    if os.path.exists(tfile):
+        try:
+            traffic = json.load(open(tfile)).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int32", "data": "synthetic (seeded splitmix64 generator, synth/; paper-calibrated profiles)",
+        "config": {"workload": f"{name}: {WORKLOADS[name]['desc']}", "windows_per_gpu": W,
+                   "cells_per_gpu_step": cells, "path": "solve (fused a3-a5)" if fused else "plan+backtrack",
+                   "l2": "flushed between timed steps (256 MiB write outside the step events)",
+                   "parallelism": f"weak dp{N} (windows sharded, NCCL allreduce of stats)"},
+        "windows_per_s": W * N / t_step,
+        "dp_ms": t_dp * 1e3,
+        "dp_cell_updates_per_s": total_cells / t_dp,
+        "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
+                     "frac": achieved / smem_peak, "traffic": traffic,
+                     "kernel": "turbo::dp_warp_kernel (turbo_mckp_solve)",
+                     "note": "algorithmic smem bytes = cells x (4K+4) per launch (SURVEY.md 8(d)); "
+                             "peak = SMs x 128 B/clk x sm_max_mhz (MEASURED_PEAKS.json), derived"},
+        "e2e": {"value": total_cells / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": t_e2e * 1e3},
+        "gpu_launches": launches_per_step * args.steps,
+        "clocks": clocks,
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        rate, reps, el = oracle_rate(wl, args.cpu_seconds, os.cpu_count() or 1)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "oracle",
+                                "sample": f"{reps} passes over the rank-0 {name} windows ({wl.num_windows} windows, "
+                                          f"{cells} cells each), {el:.1f} s, table DP, gcc -O2, "
+                                          f"{os.cpu_count()} threads"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["turbo", "reference"], default="turbo")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--unfused", dest="fused", action="store_false")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_turbo(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

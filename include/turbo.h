@@ -1,0 +1,189 @@
+/*
+ * turbo.h -- C ABI of the B200 (sm_100a) hot path of Turbo's online enhancement
+ * scheduler (arXiv 2207.00172, "Turbo: Opportunistic Enhancement for Edge Video
+ * Analytics", §5 Adaptive Enhancement Scheduling).
+ *
+ * Problem (§5.2, Eq. max / s.t.): a window holds m frames x
+ * with estimated difficulty theta'_x (a class = bucket of width 0.1);
+ * choose an enhancement level kappa_x in [0, beta] for every frame to maximise
+ * sum_x P_{kappa_x}^{theta'_x} subject to the window's latency constraint T.
+ * With per-frame additive costs (reading R1 in DESIGN.md) this is a multiple-choice
+ * knapsack, solved EXACTLY (the paper's brute-force "upper") by an
+ * integer max-plus dynamic program. Result = unique maximum of the total order
+ * (gain desc, cost asc, exit vector lexicographically asc, frame 0 first).
+ *
+ * Conventions for every entry point:
+ *  - Pointers are DEVICE pointers unless marked (host). Device buffers are owned by
+ *    the caller and must stay alive until the stream work completes; the library
+ *    keeps no reference after a call returns and never allocates device memory.
+ *  - Calls are stream-ordered on `stream` (a cudaStream_t; NULL = legacy default
+ *    stream), never synchronise the device, and are re-entrant / thread-safe.
+ *  - Host-side validation runs before any launch; on error nothing is launched and
+ *    the status code says why. Launch failures return TURBO_ERR_CUDA.
+ *  - Integer units: gains in 0.01 mAP points (|g| <= 2^24), costs in GPU-time units
+ *    (0 <= c < 2^31), budgets in the same units. Gains of one window must satisfy
+ *    sum_i max_k |g_ik| < 2^25 (range rule R14) -- checked on device per window.
+ */
+#ifndef TURBO_H
+#define TURBO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TURBO_OK = 0,
+    TURBO_ERR_INVALID_ARG = 1,   /* null pointer, bad count, K outside [2,16], C outside [1,256] */
+    TURBO_ERR_RANGE = 2,         /* N_w > 65535, budget outside [0, 2^30), sizes overflow        */
+    TURBO_ERR_WORKSPACE = 3,     /* workspace smaller than turbo_mckp_workspace() demanded       */
+    TURBO_ERR_CUDA = 4,          /* a kernel launch or attribute query failed                    */
+    TURBO_ERR_UNSUPPORTED = 5    /* shape the compiled kernels cannot serve (e.g. row > smem)   */
+} turbo_status_t;
+
+typedef void *turbo_stream_t;    /* cudaStream_t */
+
+/* One offline profile (§5.1): accuracy gain P_kappa^theta per
+ * difficulty bucket and level, and latency cost I_kappa per level, both quantised.
+ * Row-major [class][exit]; exit 0 = "no enhancement" (P_0 = 0 in the paper, not
+ * required here). Costs are INCREMENTAL over mandatory detection (reading R3). */
+typedef struct {
+    int32_t num_classes;         /* C in [1, 256]                                   */
+    int32_t num_exits;           /* K = beta + 1 in [2, 16]                         */
+    const int32_t *gain;         /* device [C*K]                                    */
+    const int32_t *cost;         /* device [C*K], >= 0                              */
+} turbo_profile_t;
+
+/* One scheduling window: the m_w frames reaching the detector and its budget. */
+typedef struct {
+    int64_t first_frame;         /* offset into class_id[] / exit_out[] (caller sets)            */
+    int64_t first_option;        /* offset into opt_gain[] / opt_cost[] (turbo_mckp_workspace)   */
+    int64_t choice_offset;       /* byte offset of this window's choice plane in the workspace  */
+    int32_t num_frames;          /* m_w in [0, 65535] (caller sets)                              */
+    int32_t budget;              /* B_w >= 0 (caller sets, or a1 derives it on device)           */
+    int32_t profile;             /* index into the profile array (caller sets)                   */
+    int32_t num_exits;           /* K of the profile (turbo_mckp_workspace)                      */
+    int32_t budget_bound;        /* layout bound: budget at sizing time (turbo_mckp_workspace);
+                                    a device-side budget above it rejects the window            */
+    int32_t reserved;            /* 0 */
+} turbo_window_t;                /* 48 bytes; array lives on the host (sizing) and the device */
+
+/* Launch shape of a window batch, computed on the host by turbo_mckp_workspace
+ * from the host copies of windows and profiles. Passed (host) to every device
+ * call so the library never reads device memory to configure a launch. */
+typedef struct {
+    int32_t num_windows;
+    int32_t num_profiles;
+    int32_t max_frames;          /* max m_w                                      */
+    int32_t max_budget;          /* max budget_bound                              */
+    int32_t min_exits, max_exits;
+    int32_t num_classes_max;
+    int32_t reserved0;
+    int64_t total_frames;        /* sum m_w                                       */
+    int64_t total_options;       /* sum m_w K_w  (size of opt_gain / opt_cost)    */
+    int64_t total_cells;         /* sum m_w (budget_bound_w + 1)                  */
+    int64_t workspace_bytes;     /* bytes needed by turbo_mckp_plan / backtrack   */
+    int64_t reserved1[4];
+} turbo_shape_t;
+
+/* Number of int64 words of the status vector written by lookup / plan. */
+#define TURBO_STATUS_WORDS 2
+/* status[0]: smallest frame index whose class id is >= C of its profile (-1 = none);
+ *            that frame's option row is written as zeros.
+ * status[1]: smallest window index rejected by the planner (negative cost, gain range
+ *            rule violated, budget above budget_bound; -1 = none); a rejected window
+ *            is planned as all-zero exits, best_gain = best_cost = 0, feasible = 0.
+ * The caller initialises both words to -1 (all bits set). */
+
+/* Layout of the statistics vector (a6), int64[TURBO_STATS_WORDS]. */
+#define TURBO_STATS_WORDS 181
+/* [0,16) exit histogram; [16,176) class x exit histogram for classes 0..9
+ * (row-major, 16 exits per class; classes >= 10 not binned); 176 sum best_gain;
+ * 177 sum best_cost; 178 #windows; 179 #frames; 180 #infeasible windows. */
+
+/* ---------------------------------------------------------------------------
+ * Host-only sizing (no device access). Validates the host copies of profiles and
+ * windows, fills windows_host[w].first_option / choice_offset / num_exits /
+ * budget_bound, and fills *shape (including workspace_bytes).
+ * profiles_host: host array of num_profiles descriptors (gain/cost pointers are
+ *   not dereferenced here). windows_host: host array, modified in place.
+ * Errors: INVALID_ARG (null, K or C out of range, profile index out of range,
+ *   num_frames < 0, budget < 0), RANGE (num_frames > 65535, budget >= 2^30). */
+turbo_status_t turbo_mckp_workspace(const turbo_profile_t *profiles_host, int32_t num_profiles,
+                                    turbo_window_t *windows_host, int32_t num_windows,
+                                    turbo_shape_t *shape /* host, out */);
+
+/* ---------------------------------------------------------------------------
+ * a1 + a2. a1 (§3; reading R3): if capacity != NULL,
+ *   windows[w].budget = max(0, capacity[w] - num_frames_w * base_cost)  (written on device).
+ * a2: opt_gain[first_option_w + i*K + k] = gain[class][k],
+ *   opt_cost[...] = cost[class][k], class = class_id[first_frame_w + i].
+ * profiles: DEVICE array of shape->num_profiles descriptors (same content as the
+ * host copy given to turbo_mckp_workspace). windows: device copy of the sized
+ * windows. class_id: u8 [total_frames]. opt_gain/opt_cost: int32 [total_options].
+ * status: int64[2], see TURBO_STATUS_WORDS. */
+turbo_status_t turbo_profile_lookup(const turbo_shape_t *shape /* host */,
+                                    const turbo_profile_t *profiles, turbo_window_t *windows,
+                                    const uint8_t *class_id, const int32_t *capacity /* nullable */,
+                                    int32_t base_cost, int32_t *opt_gain, int32_t *opt_cost,
+                                    int64_t *status, turbo_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * a3 + a4: for every window, the suffix max-plus DP over frames N-1..0,
+ *   S_N[b] = 0,  S_i[b] = max_{k : c_ik <= b} g_ik + S_{i+1}[b - c_ik]   (b = 0..B),
+ * with the per-cell smallest maximising k written bit-packed to the workspace
+ * (2 bits for K <= 4, 4 bits otherwise); then G* = S_0[B],
+ * C* = min{b : S_0[b] = G*}, feasible = (G* > -inf). Infeasible windows report
+ * best_gain = sum_i g_i0, best_cost = sum_i c_i0 (reading R8).
+ * workspace: >= shape->workspace_bytes device bytes (choice planes).
+ * best_gain, best_cost: int32 [W]; feasible: u8 [W]; status: int64[2]. */
+turbo_status_t turbo_mckp_plan(const turbo_shape_t *shape /* host */, const turbo_window_t *windows,
+                               const int32_t *opt_gain, const int32_t *opt_cost,
+                               void *workspace, size_t workspace_bytes,
+                               int32_t *best_gain, int32_t *best_cost, uint8_t *feasible,
+                               int64_t *status, turbo_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * a5: plan reconstruction from the choice planes of turbo_mckp_plan:
+ *   b = C*; for i = 0..N-1: k_i = choice_i[b]; exit_out[first_frame + i] = k_i; b -= c_{i,k_i}.
+ * Infeasible or rejected windows get all-zero exits. exit_out: u8 [total_frames]. */
+turbo_status_t turbo_backtrack(const turbo_shape_t *shape /* host */, const turbo_window_t *windows,
+                               const int32_t *opt_cost, const void *workspace, size_t workspace_bytes,
+                               const int32_t *best_cost, const uint8_t *feasible,
+                               uint8_t *exit_out, turbo_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * a3 + a4 + a5 fused in one launch (choice planes kept in shared memory when they
+ * fit, else in the workspace). Outputs bit-identical to plan + backtrack.
+ * workspace may be NULL when shape-dependent turbo_mckp_solve_workspace() returns 0. */
+turbo_status_t turbo_mckp_solve(const turbo_shape_t *shape /* host */, const turbo_window_t *windows,
+                                const int32_t *opt_gain, const int32_t *opt_cost,
+                                void *workspace, size_t workspace_bytes,
+                                int32_t *best_gain, int32_t *best_cost, uint8_t *feasible,
+                                uint8_t *exit_out, int64_t *status, turbo_stream_t stream);
+
+/* Bytes of workspace turbo_mckp_solve needs for this shape (0 when every window's
+ * choice plane fits in shared memory). Host only. */
+turbo_status_t turbo_mckp_solve_workspace(const turbo_shape_t *shape, size_t *bytes /* host, out */);
+
+/* ---------------------------------------------------------------------------
+ * a6 (per GPU): ACCUMULATES the plan statistics into stats (int64[181], layout
+ * above; caller zeroes it). The cross-GPU sum (one allreduce over NVLink) is done by
+ * the caller's communicator, not inside the library. */
+turbo_status_t turbo_stats(const turbo_shape_t *shape /* host */, const turbo_window_t *windows,
+                           const uint8_t *class_id, const uint8_t *exit_out,
+                           const int32_t *best_gain, const int32_t *best_cost,
+                           const uint8_t *feasible, int64_t *stats, turbo_stream_t stream);
+
+/* Debug / test hooks: force a DP kernel variant (0 = automatic) and report the last
+ * launch configuration chosen. Not needed in production. */
+turbo_status_t turbo_debug_set_variant(int32_t variant);
+const char *turbo_status_string(turbo_status_t s);
+int32_t turbo_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TURBO_H */

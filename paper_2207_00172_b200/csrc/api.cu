@@ -1,0 +1,265 @@
+// api.cu -- host side of the C ABI (include/turbo.h): validation, sizing, dispatch.
+// No device memory is allocated here and nothing synchronises the device.
+#include <cstring>
+#include <mutex>
+
+#include "turbo_internal.cuh"
+
+namespace turbo {
+
+struct DeviceInfo {
+    int num_sms = 0;
+    int smem_per_sm = 0;
+    int smem_per_cta_optin = 0;
+};
+
+static std::mutex g_mu;
+static DeviceInfo g_dev[64];
+static int g_variant = 0;
+
+static cudaError_t device_info(DeviceInfo *out)
+{
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_dev[dev].num_sms == 0) {
+        DeviceInfo d;
+        if ((e = cudaDeviceGetAttribute(&d.num_sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+        if ((e = cudaDeviceGetAttribute(&d.smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev)) !=
+            cudaSuccess)
+            return e;
+        if ((e = cudaDeviceGetAttribute(&d.smem_per_cta_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) !=
+            cudaSuccess)
+            return e;
+        g_dev[dev] = d;
+    }
+    *out = g_dev[dev];
+    return cudaSuccess;
+}
+
+// smem words per warp for the DP: row (+ choice planes and costs for the fused solve)
+static void dp_smem_words(const turbo_shape_t *s, bool solve_smem, int32_t *row_w, int32_t *chs_w, int32_t *cst_w)
+{
+    const int64_t rows = num_rows(s->max_budget);
+    *row_w = (int32_t)(rows * 32);
+    const int rpt_min = s->max_exits <= 4 ? 16 : 8;
+    const int64_t tiles = (rows + rpt_min - 1) / rpt_min;
+    const int64_t chs = solve_smem ? (int64_t)s->max_frames * tiles * 32 : 0;
+    *chs_w = (int32_t)(chs > INT32_MAX ? INT32_MAX : chs);
+    *cst_w = (int32_t)((int64_t)s->max_frames * s->max_exits);
+}
+
+static size_t smem_choice_limit = 64 * 1024;   // per-warp bytes above which choices go to HBM
+
+}  // namespace turbo
+
+using namespace turbo;
+
+extern "C" {
+
+int32_t turbo_abi_version(void) { return 1; }
+
+const char *turbo_status_string(turbo_status_t s)
+{
+    switch (s) {
+        case TURBO_OK: return "ok";
+        case TURBO_ERR_INVALID_ARG: return "invalid argument";
+        case TURBO_ERR_RANGE: return "value out of range";
+        case TURBO_ERR_WORKSPACE: return "workspace too small";
+        case TURBO_ERR_CUDA: return "CUDA error";
+        case TURBO_ERR_UNSUPPORTED: return "unsupported shape";
+    }
+    return "unknown";
+}
+
+turbo_status_t turbo_debug_set_variant(int32_t variant)
+{
+    if (variant < 0 || variant > 2) return TURBO_ERR_INVALID_ARG;
+    g_variant = variant;
+    return TURBO_OK;
+}
+
+turbo_status_t turbo_mckp_workspace(const turbo_profile_t *profiles_host, int32_t num_profiles,
+                                    turbo_window_t *windows_host, int32_t num_windows, turbo_shape_t *shape)
+{
+    if (!shape || num_profiles < 0 || num_windows < 0) return TURBO_ERR_INVALID_ARG;
+    if ((num_profiles > 0 && !profiles_host) || (num_windows > 0 && !windows_host)) return TURBO_ERR_INVALID_ARG;
+    for (int32_t p = 0; p < num_profiles; ++p) {
+        const turbo_profile_t &pr = profiles_host[p];
+        if (pr.num_exits < 2 || pr.num_exits > MAX_EXITS) return TURBO_ERR_INVALID_ARG;
+        if (pr.num_classes < 1 || pr.num_classes > 256) return TURBO_ERR_INVALID_ARG;
+        if (!pr.gain || !pr.cost) return TURBO_ERR_INVALID_ARG;
+    }
+    turbo_shape_t s;
+    std::memset(&s, 0, sizeof(s));
+    s.num_windows = num_windows;
+    s.num_profiles = num_profiles;
+    s.min_exits = MAX_EXITS;
+    s.max_exits = 2;
+    int64_t opt = 0, ws = 0, frames = 0, cells = 0;
+    for (int32_t w = 0; w < num_windows; ++w) {
+        turbo_window_t &win = windows_host[w];
+        if (win.profile < 0 || win.profile >= num_profiles) return TURBO_ERR_INVALID_ARG;
+        if (win.num_frames < 0 || win.budget < 0 || win.first_frame < 0) return TURBO_ERR_INVALID_ARG;
+        if (win.num_frames > 65535 || win.budget >= (1 << 30)) return TURBO_ERR_RANGE;
+        const int K = profiles_host[win.profile].num_exits;
+        win.num_exits = K;
+        win.budget_bound = win.budget;
+        win.first_option = opt;
+        win.choice_offset = ws;
+        win.reserved = 0;
+        opt += ((int64_t)win.num_frames * K + 3) & ~(int64_t)3;    // 16-B aligned option blocks
+        ws += choice_plane_bytes(win.num_frames, win.budget, K);
+        frames = frames > win.first_frame + win.num_frames ? frames : win.first_frame + win.num_frames;
+        cells += (int64_t)win.num_frames * ((int64_t)win.budget + 1);
+        if (win.num_frames > s.max_frames) s.max_frames = win.num_frames;
+        if (win.budget > s.max_budget) s.max_budget = win.budget;
+        if (K < s.min_exits) s.min_exits = K;
+        if (K > s.max_exits) s.max_exits = K;
+        if (profiles_host[win.profile].num_classes > s.num_classes_max)
+            s.num_classes_max = profiles_host[win.profile].num_classes;
+    }
+    if (num_windows == 0) s.min_exits = s.max_exits = 2;
+    s.total_frames = frames;
+    s.total_options = opt;
+    s.total_cells = cells;
+    s.workspace_bytes = ws;
+    *shape = s;
+    return TURBO_OK;
+}
+
+turbo_status_t turbo_profile_lookup(const turbo_shape_t *shape, const turbo_profile_t *profiles,
+                                    turbo_window_t *windows, const uint8_t *class_id, const int32_t *capacity,
+                                    int32_t base_cost, int32_t *opt_gain, int32_t *opt_cost, int64_t *status,
+                                    turbo_stream_t stream)
+{
+    if (!shape) return TURBO_ERR_INVALID_ARG;
+    if (shape->num_windows == 0) return TURBO_OK;
+    if (!profiles || !windows || !status || base_cost < 0) return TURBO_ERR_INVALID_ARG;
+    if (shape->total_frames > 0 && !class_id) return TURBO_ERR_INVALID_ARG;
+    if (shape->total_options > 0 && (!opt_gain || !opt_cost)) return TURBO_ERR_INVALID_ARG;
+    if ((reinterpret_cast<uintptr_t>(opt_gain) | reinterpret_cast<uintptr_t>(opt_cost)) & 15)
+        return TURBO_ERR_INVALID_ARG;
+    DeviceInfo d;
+    if (device_info(&d) != cudaSuccess) return TURBO_ERR_CUDA;
+    cudaError_t e = launch_lookup(profiles, windows, shape->num_windows, class_id, capacity, base_cost, opt_gain,
+                                  opt_cost, status, d.num_sms, (cudaStream_t)stream);
+    return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
+}
+
+static turbo_status_t run_dp(const turbo_shape_t *shape, int mode, const turbo_window_t *windows,
+                             const int32_t *opt_gain, const int32_t *opt_cost, void *workspace,
+                             int32_t *best_gain, int32_t *best_cost, uint8_t *feasible, uint8_t *exit_out,
+                             int64_t *status, turbo_stream_t stream)
+{
+    DeviceInfo d;
+    if (device_info(&d) != cudaSuccess) return TURBO_ERR_CUDA;
+    DpParams P;
+    std::memset(&P, 0, sizeof(P));
+    dp_smem_words(shape, mode == DP_SOLVE_SMEM, &P.row_words, &P.chs_words, &P.cst_words);
+    if (mode == DP_PLAN) P.cst_words = 0;
+    P.warp_words = (P.row_words + P.chs_words + P.cst_words + 3) & ~3;
+    if ((int64_t)P.warp_words * 4 > (int64_t)d.smem_per_cta_optin) return TURBO_ERR_UNSUPPORTED;
+    P.windows = windows;
+    P.num_windows = shape->num_windows;
+    P.opt_gain = opt_gain;
+    P.opt_cost = opt_cost;
+    P.workspace = reinterpret_cast<uint8_t *>(workspace);
+    P.best_gain = best_gain;
+    P.best_cost = best_cost;
+    P.feasible = feasible;
+    P.exit_out = exit_out;
+    P.status = status;
+    DpLaunch info;
+    cudaError_t e = launch_dp(shape, mode, P, d.num_sms, d.smem_per_sm, d.smem_per_cta_optin,
+                              (cudaStream_t)stream, &info);
+    return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
+}
+
+turbo_status_t turbo_mckp_plan(const turbo_shape_t *shape, const turbo_window_t *windows, const int32_t *opt_gain,
+                               const int32_t *opt_cost, void *workspace, size_t workspace_bytes,
+                               int32_t *best_gain, int32_t *best_cost, uint8_t *feasible, int64_t *status,
+                               turbo_stream_t stream)
+{
+    if (!shape) return TURBO_ERR_INVALID_ARG;
+    if (shape->num_windows == 0) return TURBO_OK;
+    if (!windows || !best_gain || !best_cost || !feasible || !status) return TURBO_ERR_INVALID_ARG;
+    if (shape->total_options > 0 && (!opt_gain || !opt_cost)) return TURBO_ERR_INVALID_ARG;
+    if ((int64_t)workspace_bytes < shape->workspace_bytes || (shape->workspace_bytes > 0 && !workspace))
+        return TURBO_ERR_WORKSPACE;
+    return run_dp(shape, DP_PLAN, windows, opt_gain, opt_cost, workspace, best_gain, best_cost, feasible, nullptr,
+                  status, stream);
+}
+
+turbo_status_t turbo_backtrack(const turbo_shape_t *shape, const turbo_window_t *windows, const int32_t *opt_cost,
+                               const void *workspace, size_t workspace_bytes, const int32_t *best_cost,
+                               const uint8_t *feasible, uint8_t *exit_out, turbo_stream_t stream)
+{
+    if (!shape) return TURBO_ERR_INVALID_ARG;
+    if (shape->num_windows == 0) return TURBO_OK;
+    if (!windows || !best_cost || !feasible) return TURBO_ERR_INVALID_ARG;
+    if (shape->total_frames > 0 && !exit_out) return TURBO_ERR_INVALID_ARG;
+    if (shape->total_options > 0 && !opt_cost) return TURBO_ERR_INVALID_ARG;
+    if ((int64_t)workspace_bytes < shape->workspace_bytes || (shape->workspace_bytes > 0 && !workspace))
+        return TURBO_ERR_WORKSPACE;
+    DeviceInfo d;
+    if (device_info(&d) != cudaSuccess) return TURBO_ERR_CUDA;
+    cudaError_t e = launch_backtrack(windows, shape->num_windows, opt_cost,
+                                     reinterpret_cast<const uint8_t *>(workspace), best_cost, feasible, exit_out,
+                                     d.num_sms, (cudaStream_t)stream);
+    return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
+}
+
+static int solve_mode(const turbo_shape_t *shape)
+{
+    if (g_variant == 1) return DP_SOLVE_SMEM;
+    if (g_variant == 2) return DP_SOLVE_GLOBAL;
+    int32_t r, c, k;
+    dp_smem_words(shape, true, &r, &c, &k);
+    const int64_t bytes = ((int64_t)r + c + k) * 4;
+    return bytes <= (int64_t)smem_choice_limit ? DP_SOLVE_SMEM : DP_SOLVE_GLOBAL;
+}
+
+turbo_status_t turbo_mckp_solve_workspace(const turbo_shape_t *shape, size_t *bytes)
+{
+    if (!shape || !bytes) return TURBO_ERR_INVALID_ARG;
+    *bytes = solve_mode(shape) == DP_SOLVE_SMEM ? 0 : (size_t)shape->workspace_bytes;
+    return TURBO_OK;
+}
+
+turbo_status_t turbo_mckp_solve(const turbo_shape_t *shape, const turbo_window_t *windows, const int32_t *opt_gain,
+                                const int32_t *opt_cost, void *workspace, size_t workspace_bytes,
+                                int32_t *best_gain, int32_t *best_cost, uint8_t *feasible, uint8_t *exit_out,
+                                int64_t *status, turbo_stream_t stream)
+{
+    if (!shape) return TURBO_ERR_INVALID_ARG;
+    if (shape->num_windows == 0) return TURBO_OK;
+    if (!windows || !best_gain || !best_cost || !feasible || !status) return TURBO_ERR_INVALID_ARG;
+    if (shape->total_frames > 0 && !exit_out) return TURBO_ERR_INVALID_ARG;
+    if (shape->total_options > 0 && (!opt_gain || !opt_cost)) return TURBO_ERR_INVALID_ARG;
+    const int mode = solve_mode(shape);
+    if (mode == DP_SOLVE_GLOBAL &&
+        ((int64_t)workspace_bytes < shape->workspace_bytes || (shape->workspace_bytes > 0 && !workspace)))
+        return TURBO_ERR_WORKSPACE;
+    return run_dp(shape, mode, windows, opt_gain, opt_cost, workspace, best_gain, best_cost, feasible, exit_out,
+                  status, stream);
+}
+
+turbo_status_t turbo_stats(const turbo_shape_t *shape, const turbo_window_t *windows, const uint8_t *class_id,
+                           const uint8_t *exit_out, const int32_t *best_gain, const int32_t *best_cost,
+                           const uint8_t *feasible, int64_t *stats, turbo_stream_t stream)
+{
+    if (!shape) return TURBO_ERR_INVALID_ARG;
+    if (shape->num_windows == 0) return TURBO_OK;
+    if (!windows || !best_gain || !best_cost || !feasible || !stats) return TURBO_ERR_INVALID_ARG;
+    if (shape->total_frames > 0 && (!class_id || !exit_out)) return TURBO_ERR_INVALID_ARG;
+    DeviceInfo d;
+    if (device_info(&d) != cudaSuccess) return TURBO_ERR_CUDA;
+    cudaError_t e = launch_stats(windows, shape->num_windows, class_id, exit_out, best_gain, best_cost, feasible,
+                                 stats, d.num_sms, (cudaStream_t)stream);
+    return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
+}
+
+}  // extern "C"

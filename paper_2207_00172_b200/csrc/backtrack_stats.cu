@@ -1,0 +1,157 @@
+// backtrack_stats.cu -- K6 (plan reconstruction, a5) and K7 (plan statistics, a6).
+#include "turbo_internal.cuh"
+
+namespace turbo {
+
+// ---------------------------------------------------------------------------------------------
+// K6 (a5). Forward walk from (frame 0, b = C*): k_i = choice_i[b]; b -= c_{i,k_i}
+// (the realisation of the lexicographic tie-break, reading R7; "we
+// execute each frame according to the plan"). The chain of N dependent loads is latency-bound,
+// so one warp serves one window and SPECULATES: while frame i's word is in flight the lanes
+// already fetch frame i+1's words for all K possible shifts b - c_ik (costs of frame i do not
+// depend on b), so each round trip resolves two frames.
+__global__ void __launch_bounds__(256) backtrack_kernel(const turbo_window_t *__restrict__ windows,
+                                                        int32_t num_windows,
+                                                        const int32_t *__restrict__ opt_cost,
+                                                        const uint8_t *__restrict__ workspace,
+                                                        const int32_t *__restrict__ best_cost,
+                                                        const uint8_t *__restrict__ feasible,
+                                                        uint8_t *__restrict__ exit_out)
+{
+    const int lane = threadIdx.x & 31;
+    const int wpc = blockDim.x >> 5;
+    for (int64_t w = (int64_t)blockIdx.x * wpc + (threadIdx.x >> 5); w < num_windows;
+         w += (int64_t)gridDim.x * wpc) {
+        const int64_t ff = windows[w].first_frame;
+        const int64_t fo = windows[w].first_option;
+        const int32_t N = windows[w].num_frames;
+        const int32_t K = windows[w].num_exits;
+        const int32_t Bb = windows[w].budget_bound;
+        const uint32_t *__restrict__ gch =
+            reinterpret_cast<const uint32_t *>(workspace + windows[w].choice_offset);
+        if (!feasible[w]) {
+            for (int32_t i = lane; i < N; i += 32) exit_out[ff + i] = 0;
+            continue;
+        }
+        const int CB = K <= 4 ? 2 : 4;
+        const int RPT = 32 / CB;
+        const int lg_tile = K <= 4 ? 9 : 8;                   // log2(32 * RPT)
+        const uint32_t cmask = (1u << CB) - 1u;
+        const int32_t gtiles = (((Bb + 32) >> 5) + RPT - 1) / RPT;
+        const int32_t *__restrict__ oc = opt_cost + fo;
+        auto fetch = [&](int32_t i, int32_t b) -> int32_t {  // choice of frame i at cell b
+            const uint32_t word = __ldg(gch + ((int64_t)i * gtiles + (b >> lg_tile)) * 32 + (b & 31));
+            return (int32_t)((word >> (CB * ((b >> 5) & (RPT - 1)))) & cmask);
+        };
+        int32_t b = best_cost[w];
+        int32_t i = 0;
+        while (i < N) {
+            // lane 0 fetches frame i at b; lanes 1..K fetch frame i+1 at b - c_{i,lane-1}
+            // costs do not depend on b: lanes 1..K hold c_{i,lane-1} and c_{i+1,lane-1}
+            const bool opt_lane = lane >= 1 && lane <= K;
+            const int32_t ci = opt_lane ? __ldg(oc + (int64_t)i * K + (lane - 1)) : 0;
+            const int32_t cn = (opt_lane && i + 1 < N) ? __ldg(oc + (int64_t)(i + 1) * K + (lane - 1)) : 0;
+            int32_t kk = 0;
+            if (lane == 0) {
+                kk = fetch(i, b);
+            } else if (lane <= K && i + 1 < N) {
+                const int32_t b1 = b - ci;
+                kk = b1 >= 0 ? fetch(i + 1, b1) : 0;
+            }
+            const int32_t k0 = __shfl_sync(0xffffffffu, kk, 0);
+            const int32_t c0 = __shfl_sync(0xffffffffu, ci, k0 + 1);
+            if (lane == 0) exit_out[ff + i] = (uint8_t)k0;
+            b -= c0;
+            if (i + 1 < N) {
+                const int32_t k1 = __shfl_sync(0xffffffffu, kk, k0 + 1);
+                const int32_t c1 = __shfl_sync(0xffffffffu, cn, k1 + 1);
+                if (lane == 0) exit_out[ff + i + 1] = (uint8_t)k1;
+                b -= c1;
+            }
+            i += 2;
+        }
+    }
+}
+
+cudaError_t launch_backtrack(const turbo_window_t *windows, int32_t num_windows, const int32_t *opt_cost,
+                             const uint8_t *workspace, const int32_t *best_cost, const uint8_t *feasible,
+                             uint8_t *exit_out, int num_sms, cudaStream_t stream)
+{
+    if (num_windows <= 0) return cudaSuccess;
+    const int threads = 128;
+    const int wpc = threads / 32;
+    int64_t blocks = ((int64_t)num_windows + wpc - 1) / wpc;
+    const int64_t cap = (int64_t)num_sms * 16;
+    if (blocks > cap) blocks = cap;
+    backtrack_kernel<<<(unsigned)blocks, threads, 0, stream>>>(windows, num_windows, opt_cost, workspace,
+                                                               best_cost, feasible, exit_out);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------------
+// K7 (a6). Per-GPU statistics of the plans, int64[181] (layout in turbo.h): CTA-private
+// shared-memory histograms, one global atomic per counter per CTA at the end.
+__global__ void __launch_bounds__(256) stats_kernel(const turbo_window_t *__restrict__ windows,
+                                                    int32_t num_windows, const uint8_t *__restrict__ class_id,
+                                                    const uint8_t *__restrict__ exit_out,
+                                                    const int32_t *__restrict__ best_gain,
+                                                    const int32_t *__restrict__ best_cost,
+                                                    const uint8_t *__restrict__ feasible,
+                                                    unsigned long long *__restrict__ stats)
+{
+    __shared__ unsigned int hist[176];
+    __shared__ unsigned long long tot[5];
+    for (int x = threadIdx.x; x < 176; x += blockDim.x) hist[x] = 0;
+    if (threadIdx.x < 5) tot[threadIdx.x] = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int wpc = blockDim.x >> 5;
+    long long sg = 0, sc = 0, nw = 0, nf = 0, ni = 0;
+    for (int64_t w = (int64_t)blockIdx.x * wpc + (threadIdx.x >> 5); w < num_windows;
+         w += (int64_t)gridDim.x * wpc) {
+        const int64_t ff = windows[w].first_frame;
+        const int32_t N = windows[w].num_frames;
+        for (int32_t i = lane; i < N; i += 32) {
+            const uint32_t k = exit_out[ff + i] & 15u;
+            const uint32_t c = class_id[ff + i];
+            atomicAdd(&hist[k], 1u);
+            if (c < 10) atomicAdd(&hist[16 + c * 16 + k], 1u);
+        }
+        if (lane == 0) {
+            sg += best_gain[w];
+            sc += best_cost[w];
+            nw += 1;
+            nf += N;
+            ni += feasible[w] ? 0 : 1;
+        }
+    }
+    if (lane == 0) {
+        atomicAdd(&tot[0], (unsigned long long)sg);
+        atomicAdd(&tot[1], (unsigned long long)sc);
+        atomicAdd(&tot[2], (unsigned long long)nw);
+        atomicAdd(&tot[3], (unsigned long long)nf);
+        atomicAdd(&tot[4], (unsigned long long)ni);
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < 176; x += blockDim.x)
+        if (hist[x]) atomicAdd(&stats[x], (unsigned long long)hist[x]);
+    if (threadIdx.x < 5 && tot[threadIdx.x]) atomicAdd(&stats[176 + threadIdx.x], tot[threadIdx.x]);
+}
+
+cudaError_t launch_stats(const turbo_window_t *windows, int32_t num_windows, const uint8_t *class_id,
+                         const uint8_t *exit_out, const int32_t *best_gain, const int32_t *best_cost,
+                         const uint8_t *feasible, int64_t *stats, int num_sms, cudaStream_t stream)
+{
+    if (num_windows <= 0) return cudaSuccess;
+    const int threads = 256;
+    const int wpc = threads / 32;
+    int64_t blocks = ((int64_t)num_windows + wpc - 1) / wpc;
+    const int64_t cap = (int64_t)num_sms * 2;
+    if (blocks > cap) blocks = cap;
+    stats_kernel<<<(unsigned)blocks, threads, 0, stream>>>(windows, num_windows, class_id, exit_out, best_gain,
+                                                           best_cost, feasible,
+                                                           reinterpret_cast<unsigned long long *>(stats));
+    return cudaGetLastError();
+}
+
+}  // namespace turbo

@@ -1,0 +1,91 @@
+// turbo_internal.cuh -- shared device helpers of the sm_100a kernels (product path).
+// Nothing here is shared with oracle/ (the CPU oracle is independent by design).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "turbo.h"
+
+namespace turbo {
+
+// ---------------------------------------------------------------------------------------------
+// Packed DP key: a row cell holds R = S << 4 (low 4 bits zero).
+// Option k of a frame is pre-packed as gp_k = (g_k << 4) | (15 - k), so the max-plus update
+//   key = max_k (R_old[b - c_k] + gp_k)
+// carries the argmax in its low 4 bits; equal S prefer the larger tag = the SMALLER k, which
+// is the per-cell tie-break that realises the lexicographic order (reading R7).
+//   R_new = key & ~15,   choice = 15 - (key & 15) = (key & 15) ^ 15.
+// -inf: NEG_R = -2^30. With the range rule sum_i max_k |g_ik| < 2^25 every reachable value of
+// a feasible cell lies in (-2^29, 2^29) and every infeasible one in (-1.5*2^30, -2^29), so the
+// two bands never mix and nothing overflows int32 (reading R14).
+constexpr int32_t NEG_R = -(1 << 30);
+constexpr int32_t VALID_MIN_R = -(1 << 29);     // feasible  <=>  R > VALID_MIN_R
+constexpr int64_t GAIN_RANGE_LIMIT = (int64_t)1 << 25;
+constexpr int MAX_EXITS = 16;
+
+__host__ __device__ __forceinline__ int choice_bits(int K) { return K <= 4 ? 2 : 4; }
+// rows of 32 cells per choice word (= per tile): 16 for 2-bit, 8 for 4-bit choices
+__host__ __device__ __forceinline__ int rows_per_tile(int K) { return 32 / choice_bits(K); }
+__host__ __device__ __forceinline__ int64_t num_rows(int64_t B) { return (B + 1 + 31) / 32; }
+__host__ __device__ __forceinline__ int64_t num_tiles(int64_t B, int K) {
+    int64_t rpt = rows_per_tile(K);
+    return (num_rows(B) + rpt - 1) / rpt;
+}
+// bytes of one window's choice plane: N frames x tiles x 32 lanes x 4 B
+__host__ __device__ __forceinline__ int64_t choice_plane_bytes(int64_t N, int64_t B, int K) {
+    return N * num_tiles(B, K) * 128;
+}
+
+__device__ __forceinline__ int32_t max_plus(int32_t a, int32_t b, int32_t c) {
+    return __viaddmax_s32(a, b, c);          // max(a + b, c): one VIADDMNMX on sm_90+/sm_100a
+}
+
+__device__ __forceinline__ void atomic_min_i64(int64_t *p, int64_t v) {
+    // status words use -1 (all ones) as "none": an unsigned min keeps the smallest index
+    atomicMin(reinterpret_cast<unsigned long long *>(p), (unsigned long long)v);
+}
+
+
+// ---------------------------------------------------------------------------------------------
+// DP launch parameters (dp_warp.cu) and the host-side launchers of every kernel.
+enum DpMode { DP_PLAN = 0, DP_SOLVE_SMEM = 1, DP_SOLVE_GLOBAL = 2 };
+
+struct DpParams {
+    const turbo_window_t *windows;
+    int32_t num_windows;
+    int32_t row_words;      // per-warp row capacity (multiple of 32)
+    int32_t chs_words;      // per-warp smem choice capacity (DP_SOLVE_SMEM)
+    int32_t cst_words;      // per-warp smem cost table capacity (solve modes)
+    int32_t warp_words;     // total smem words per warp
+    int32_t warps_per_cta;
+    const int32_t *opt_gain;
+    const int32_t *opt_cost;
+    uint8_t *workspace;
+    int32_t *best_gain;
+    int32_t *best_cost;
+    uint8_t *feasible;
+    uint8_t *exit_out;
+    int64_t *status;
+};
+
+struct DpLaunch {
+    int mode;
+    int warps_per_cta;
+    int blocks;
+    size_t smem_bytes;
+};
+
+cudaError_t launch_lookup(const turbo_profile_t *profiles, turbo_window_t *windows, int32_t num_windows,
+                          const uint8_t *class_id, const int32_t *capacity, int32_t base_cost, int32_t *opt_gain,
+                          int32_t *opt_cost, int64_t *status, int num_sms, cudaStream_t stream);
+cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P, int num_sms, int smem_per_sm,
+                      int smem_per_cta_max, cudaStream_t stream, DpLaunch *info);
+cudaError_t launch_backtrack(const turbo_window_t *windows, int32_t num_windows, const int32_t *opt_cost,
+                             const uint8_t *workspace, const int32_t *best_cost, const uint8_t *feasible,
+                             uint8_t *exit_out, int num_sms, cudaStream_t stream);
+cudaError_t launch_stats(const turbo_window_t *windows, int32_t num_windows, const uint8_t *class_id,
+                         const uint8_t *exit_out, const int32_t *best_gain, const int32_t *best_cost,
+                         const uint8_t *feasible, int64_t *stats, int num_sms, cudaStream_t stream);
+
+}  // namespace turbo

@@ -1,0 +1,289 @@
+"""Thin ctypes binding of libturbo.so (include/turbo.h). Argument marshalling only.
+
+PyTorch is used for device memory and streams (tensor.data_ptr(), the current CUDA
+stream); every step of the hot path runs in the library's sm_100a kernels. There is no
+CPU fallback: if the library or a GPU is missing, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libturbo.so")
+
+TURBO_OK = 0
+STATUS_NAMES = {0: "ok", 1: "invalid argument", 2: "value out of range", 3: "workspace too small",
+                4: "CUDA error", 5: "unsupported shape"}
+STATS_WORDS = 181
+STATUS_WORDS = 2
+
+
+class TurboError(RuntimeError):
+    def __init__(self, fn: str, code: int):
+        super().__init__(f"{fn} failed: {STATUS_NAMES.get(code, code)} ({code})")
+        self.code = code
+
+
+class Profile(ctypes.Structure):
+    _fields_ = [("num_classes", ctypes.c_int32), ("num_exits", ctypes.c_int32),
+                ("gain", ctypes.c_void_p), ("cost", ctypes.c_void_p)]
+
+
+class Window(ctypes.Structure):
+    _fields_ = [("first_frame", ctypes.c_int64), ("first_option", ctypes.c_int64),
+                ("choice_offset", ctypes.c_int64), ("num_frames", ctypes.c_int32),
+                ("budget", ctypes.c_int32), ("profile", ctypes.c_int32), ("num_exits", ctypes.c_int32),
+                ("budget_bound", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class Shape(ctypes.Structure):
+    _fields_ = [("num_windows", ctypes.c_int32), ("num_profiles", ctypes.c_int32),
+                ("max_frames", ctypes.c_int32), ("max_budget", ctypes.c_int32),
+                ("min_exits", ctypes.c_int32), ("max_exits", ctypes.c_int32),
+                ("num_classes_max", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("total_frames", ctypes.c_int64), ("total_options", ctypes.c_int64),
+                ("total_cells", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
+                ("reserved1", ctypes.c_int64 * 4)]
+
+
+assert ctypes.sizeof(Window) == 48
+WINDOW_DTYPE = np.dtype([("first_frame", "<i8"), ("first_option", "<i8"), ("choice_offset", "<i8"),
+                         ("num_frames", "<i4"), ("budget", "<i4"), ("profile", "<i4"), ("num_exits", "<i4"),
+                         ("budget_bound", "<i4"), ("reserved", "<i4")])
+assert WINDOW_DTYPE.itemsize == 48
+
+EXPORTS = ["turbo_mckp_workspace", "turbo_profile_lookup", "turbo_mckp_plan", "turbo_backtrack",
+           "turbo_mckp_solve", "turbo_mckp_solve_workspace", "turbo_stats", "turbo_debug_set_variant",
+           "turbo_status_string", "turbo_abi_version"]
+
+_lib = None
+
+
+def load(path: Optional[str] = None):
+    """Load libturbo.so (raises if absent: there is no fallback path)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise RuntimeError(f"libturbo.so not built at {p}; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    lib = ctypes.CDLL(p)
+    vp, i32, i64, sz = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_size_t
+    lib.turbo_mckp_workspace.argtypes = [vp, i32, vp, i32, vp]
+    lib.turbo_profile_lookup.argtypes = [vp, vp, vp, vp, vp, i32, vp, vp, vp, vp]
+    lib.turbo_mckp_plan.argtypes = [vp, vp, vp, vp, vp, sz, vp, vp, vp, vp, vp]
+    lib.turbo_backtrack.argtypes = [vp, vp, vp, vp, sz, vp, vp, vp, vp]
+    lib.turbo_mckp_solve.argtypes = [vp, vp, vp, vp, vp, sz, vp, vp, vp, vp, vp, vp]
+    lib.turbo_mckp_solve_workspace.argtypes = [vp, vp]
+    lib.turbo_stats.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    lib.turbo_debug_set_variant.argtypes = [i32]
+    lib.turbo_status_string.restype = ctypes.c_char_p
+    lib.turbo_abi_version.restype = i32
+    for name in EXPORTS:
+        getattr(lib, name)
+    if path is None:
+        _lib = lib
+    return lib
+
+
+def _check(fn: str, code: int):
+    if code != TURBO_OK:
+        raise TurboError(fn, code)
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+def _stream(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+# ----------------------------------------------------------------------------- C-ABI mirrors
+def mckp_workspace(profiles_host: Sequence[Profile], windows_host: np.ndarray) -> Shape:
+    """Host-only sizing; fills the layout fields of windows_host (structured WINDOW_DTYPE array)."""
+    lib = load()
+    P = len(profiles_host)
+    parr = (Profile * max(P, 1))(*profiles_host)
+    shape = Shape()
+    assert windows_host.dtype == WINDOW_DTYPE and windows_host.flags.c_contiguous
+    _check("turbo_mckp_workspace",
+           lib.turbo_mckp_workspace(ctypes.addressof(parr), P, windows_host.ctypes.data, len(windows_host),
+                                    ctypes.addressof(shape)))
+    return shape
+
+
+def profile_lookup(shape, profiles_dev, windows_dev, class_id, capacity, base_cost, opt_gain, opt_cost,
+                   status, stream=None):
+    _check("turbo_profile_lookup",
+           load().turbo_profile_lookup(ctypes.addressof(shape), _ptr(profiles_dev), _ptr(windows_dev),
+                                       _ptr(class_id), _ptr(capacity), int(base_cost), _ptr(opt_gain),
+                                       _ptr(opt_cost), _ptr(status), _stream(stream)))
+
+
+def mckp_plan(shape, windows_dev, opt_gain, opt_cost, workspace, best_gain, best_cost, feasible, status,
+              stream=None):
+    nbytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check("turbo_mckp_plan",
+           load().turbo_mckp_plan(ctypes.addressof(shape), _ptr(windows_dev), _ptr(opt_gain), _ptr(opt_cost),
+                                  _ptr(workspace), nbytes, _ptr(best_gain), _ptr(best_cost), _ptr(feasible),
+                                  _ptr(status), _stream(stream)))
+
+
+def backtrack(shape, windows_dev, opt_cost, workspace, best_cost, feasible, exit_out, stream=None):
+    nbytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check("turbo_backtrack",
+           load().turbo_backtrack(ctypes.addressof(shape), _ptr(windows_dev), _ptr(opt_cost), _ptr(workspace),
+                                  nbytes, _ptr(best_cost), _ptr(feasible), _ptr(exit_out), _stream(stream)))
+
+
+def mckp_solve_workspace(shape) -> int:
+    out = ctypes.c_size_t(0)
+    _check("turbo_mckp_solve_workspace",
+           load().turbo_mckp_solve_workspace(ctypes.addressof(shape), ctypes.addressof(out)))
+    return int(out.value)
+
+
+def mckp_solve(shape, windows_dev, opt_gain, opt_cost, workspace, best_gain, best_cost, feasible, exit_out,
+               status, stream=None):
+    nbytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check("turbo_mckp_solve",
+           load().turbo_mckp_solve(ctypes.addressof(shape), _ptr(windows_dev), _ptr(opt_gain), _ptr(opt_cost),
+                                   _ptr(workspace), nbytes, _ptr(best_gain), _ptr(best_cost), _ptr(feasible),
+                                   _ptr(exit_out), _ptr(status), _stream(stream)))
+
+
+def stats(shape, windows_dev, class_id, exit_out, best_gain, best_cost, feasible, stats_out, stream=None):
+    _check("turbo_stats",
+           load().turbo_stats(ctypes.addressof(shape), _ptr(windows_dev), _ptr(class_id), _ptr(exit_out),
+                              _ptr(best_gain), _ptr(best_cost), _ptr(feasible), _ptr(stats_out), _stream(stream)))
+
+
+def debug_set_variant(v: int):
+    _check("turbo_debug_set_variant", load().turbo_debug_set_variant(int(v)))
+
+
+# ----------------------------------------------------------------------------- planner object
+@dataclass
+class Batch:
+    """Device-resident buffers of one window batch (inputs and outputs of the hot path)."""
+    shape: Shape
+    windows_host: np.ndarray
+    profiles_host: list
+    profile_tensors: list
+    profiles_dev: object
+    windows_dev: object
+    class_id: object
+    capacity: object
+    base_cost: int
+    opt_gain: object
+    opt_cost: object
+    workspace: object
+    best_gain: object
+    best_cost: object
+    feasible: object
+    exit_out: object
+    status: object
+    stats: object
+    solve_ws: object
+
+
+def make_batch(profiles_gain: List[np.ndarray], profiles_cost: List[np.ndarray], profiles_shape: List[tuple],
+               num_frames: np.ndarray, budget_bound: np.ndarray, profile: np.ndarray,
+               class_id: Optional[np.ndarray] = None, capacity: Optional[np.ndarray] = None,
+               base_cost: int = 0, device="cuda", with_plan_workspace: bool = True) -> Batch:
+    """Allocate device buffers for a batch and size it (turbo_mckp_workspace).
+
+    budget_bound: per-window budget used for the layout (the true budget, or an upper
+    bound when a1 derives the budget on device from capacity)."""
+    import torch
+    load()
+    dev = torch.device(device)
+    ptens, phost = [], []
+    for g, c, (C, K) in zip(profiles_gain, profiles_cost, profiles_shape):
+        gt = torch.as_tensor(np.ascontiguousarray(g, dtype=np.int32), device=dev)
+        ct = torch.as_tensor(np.ascontiguousarray(c, dtype=np.int32), device=dev)
+        ptens += [gt, ct]
+        phost.append(Profile(int(C), int(K), gt.data_ptr(), ct.data_ptr()))
+    W = len(num_frames)
+    wins = np.zeros(W, dtype=WINDOW_DTYPE)
+    nf = np.asarray(num_frames, dtype=np.int64)
+    ff = np.zeros(W, dtype=np.int64)
+    if W > 1:
+        ff[1:] = np.cumsum(nf[:-1])
+    wins["first_frame"] = ff
+    wins["num_frames"] = nf
+    wins["budget"] = np.asarray(budget_bound, dtype=np.int32)
+    wins["profile"] = np.asarray(profile, dtype=np.int32)
+    shape = mckp_workspace(phost, wins)
+    pbytes = np.frombuffer(bytes((Profile * max(len(phost), 1))(*phost)), dtype=np.uint8)
+    profiles_dev = torch.as_tensor(pbytes.copy(), device=dev)
+    windows_dev = torch.as_tensor(wins.view(np.uint8).copy(), device=dev)
+    F = int(shape.total_frames)
+    cls = torch.zeros(max(F, 1), dtype=torch.uint8, device=dev)
+    if class_id is not None and F:
+        cls[:F] = torch.as_tensor(np.ascontiguousarray(class_id, dtype=np.uint8), device=dev)
+    cap = None
+    if capacity is not None:
+        cap = torch.as_tensor(np.ascontiguousarray(capacity, dtype=np.int32), device=dev)
+    nopt = max(int(shape.total_options), 4)
+    ws_bytes = int(shape.workspace_bytes) if with_plan_workspace else 0
+    solve_bytes = mckp_solve_workspace(shape)
+    return Batch(shape=shape, windows_host=wins, profiles_host=phost, profile_tensors=ptens,
+                 profiles_dev=profiles_dev, windows_dev=windows_dev, class_id=cls, capacity=cap,
+                 base_cost=int(base_cost),
+                 opt_gain=torch.zeros(nopt, dtype=torch.int32, device=dev),
+                 opt_cost=torch.zeros(nopt, dtype=torch.int32, device=dev),
+                 workspace=torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev) if ws_bytes else None,
+                 best_gain=torch.zeros(max(W, 1), dtype=torch.int32, device=dev),
+                 best_cost=torch.zeros(max(W, 1), dtype=torch.int32, device=dev),
+                 feasible=torch.zeros(max(W, 1), dtype=torch.uint8, device=dev),
+                 exit_out=torch.zeros(max(F, 1), dtype=torch.uint8, device=dev),
+                 status=torch.full((STATUS_WORDS,), -1, dtype=torch.int64, device=dev),
+                 stats=torch.zeros(STATS_WORDS, dtype=torch.int64, device=dev),
+                 solve_ws=torch.empty(solve_bytes, dtype=torch.uint8, device=dev) if solve_bytes else None)
+
+
+def batch_from_workload(wl, device="cuda", with_plan_workspace: bool = True) -> Batch:
+    """Device batch for a synth.Workload (budgets derived on device by a1 from capacity)."""
+    return make_batch(wl.profiles_gain, wl.profiles_cost, wl.profiles_shape, wl.num_frames, wl.budget,
+                      wl.profile, wl.class_id, wl.capacity, wl.base_cost, device, with_plan_workspace)
+
+
+def run_path(b: Batch, fused: bool = True, stream=None, with_stats: bool = True, reset: bool = True):
+    """One pass of the hot path: a1+a2 lookup -> a3..a5 (solve, or plan + backtrack) -> a6 stats."""
+    if reset:
+        b.status.fill_(-1)
+        if with_stats:
+            b.stats.zero_()
+    profile_lookup(b.shape, b.profiles_dev, b.windows_dev, b.class_id, b.capacity, b.base_cost, b.opt_gain,
+                   b.opt_cost, b.status, stream)
+    if fused:
+        mckp_solve(b.shape, b.windows_dev, b.opt_gain, b.opt_cost, b.solve_ws, b.best_gain, b.best_cost,
+                   b.feasible, b.exit_out, b.status, stream)
+    else:
+        mckp_plan(b.shape, b.windows_dev, b.opt_gain, b.opt_cost, b.workspace, b.best_gain, b.best_cost,
+                  b.feasible, b.status, stream)
+        backtrack(b.shape, b.windows_dev, b.opt_cost, b.workspace, b.best_cost, b.feasible, b.exit_out, stream)
+    if with_stats:
+        stats(b.shape, b.windows_dev, b.class_id, b.exit_out, b.best_gain, b.best_cost, b.feasible, b.stats,
+              stream)
+
+
+def results(b: Batch) -> dict:
+    """Copy the outputs back to the host (numpy)."""
+    W = int(b.shape.num_windows)
+    F = int(b.shape.total_frames)
+    wins = b.windows_dev.cpu().numpy().view(WINDOW_DTYPE)
+    return dict(exits=b.exit_out[:F].cpu().numpy(), best_gain=b.best_gain[:W].cpu().numpy(),
+                best_cost=b.best_cost[:W].cpu().numpy(), feasible=b.feasible[:W].cpu().numpy(),
+                status=b.status.cpu().numpy(), stats=b.stats.cpu().numpy(), budget=wins["budget"].copy(),
+                opt_gain=b.opt_gain.cpu().numpy(), opt_cost=b.opt_cost.cpu().numpy(),
+                first_option=b.windows_host["first_option"].copy())

@@ -1,0 +1,131 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit-exact.
+
+Every test here needs a B200 and is marked gpu. Inputs are seeded synthetic workloads
+(synth/); both sides see the same arrays. Kernel variants are forced through the debug
+hook so each variant sees the same windows: 0 = automatic, 1 = fused solve with choice
+planes in shared memory, 2 = fused solve with choice planes in HBM; fused=False runs
+turbo_mckp_plan + turbo_backtrack (choice planes in HBM, separate backtrack kernel).
+"""
+import numpy as np
+import pytest
+
+import synth
+from tests.parity import compare, gpu_run, oracle_run
+
+pytestmark = pytest.mark.gpu
+
+PATHS = [(True, 0), (True, 1), (True, 2), (False, 0)]
+PATH_IDS = ["solve-auto", "solve-smem", "solve-hbm", "plan+backtrack"]
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2207_00172_b200 import build, turbo
+    build.build()
+    turbo.load()
+
+
+@pytest.mark.parametrize("fused,variant", PATHS, ids=PATH_IDS)
+def test_config1(fused, variant):
+    wl = synth.make_config(1)
+    compare(wl, gpu_run(wl, fused, variant), oracle_run(wl))
+
+
+@pytest.mark.parametrize("fused,variant", PATHS, ids=PATH_IDS)
+def test_config2_all_windows(fused, variant):
+    wl = synth.make_config(2)
+    compare(wl, gpu_run(wl, fused, variant), oracle_run(wl))
+
+
+@pytest.mark.parametrize("fused,variant", PATHS, ids=PATH_IDS)
+def test_tie_heavy_small(fused, variant):
+    wl = synth.make_tie_heavy(seed=101, W=4000, max_frames=8, max_exits=4)
+    compare(wl, gpu_run(wl, fused, variant), oracle_run(wl))
+
+
+@pytest.mark.parametrize("fused,variant", PATHS, ids=PATH_IDS)
+def test_tie_heavy_wide(fused, variant):
+    """K up to 16, up to 80 frames, budgets spanning several 256/512-cell tiles."""
+    wl = synth.make_tie_heavy(seed=202, W=600, max_frames=80, max_exits=16, max_budget=1300)
+    compare(wl, gpu_run(wl, fused, variant), oracle_run(wl))
+
+
+@pytest.mark.parametrize("fused,variant", PATHS, ids=PATH_IDS)
+def test_adversarial(fused, variant):
+    wl = synth.make_adversarial()
+    compare(wl, gpu_run(wl, fused, variant), oracle_run(wl))
+
+
+@pytest.mark.parametrize("fused,variant", PATHS, ids=PATH_IDS)
+def test_config5_subset(fused, variant):
+    """Mixed sweep (K 2..16, B 64..16384, N 30..300, skewed histograms): 384 windows."""
+    wl = synth.make_config(5, num_windows=384)
+    compare(wl, gpu_run(wl, fused, variant), oracle_run(wl))
+
+
+@pytest.mark.parametrize("fused,variant", [(True, 0), (False, 0)], ids=["solve", "plan+backtrack"])
+def test_config3_subset(fused, variant):
+    wl = synth.make_config(3, window_offset=4096, num_windows=96)
+    compare(wl, gpu_run(wl, fused, variant), oracle_run(wl))
+
+
+def test_config3_shard_sampled():
+    """One 8-GPU shard of config 3 (8192 windows, the per-GPU share) at full size and in the
+    launch configuration bench.py times; the oracle recomputes 64 sampled windows one by one."""
+    wl = synth.make_config(3, window_offset=8192 * 3, num_windows=8192)
+    got = gpu_run(wl, True, 0)
+    rng = np.random.default_rng(0)
+    sample = np.sort(rng.choice(wl.num_windows, 64, replace=False))
+    ff = wl.first_frame
+    for w in sample:
+        sub = wl.subset(int(w), int(w) + 1)
+        want = oracle_run(sub, threads=1)
+        assert int(got["best_gain"][w]) == int(want["best_gain"][0])
+        assert int(got["best_cost"][w]) == int(want["best_cost"][0])
+        assert int(got["feasible"][w]) == int(want["feasible"][0])
+        np.testing.assert_array_equal(got["exits"][ff[w]: ff[w] + 300], want["exits"])
+    # properties on every window: chosen costs / gains sum to (C*, G*), C* <= B
+    og = got["opt_gain"]
+    oc = got["opt_cost"]
+    fo = got["first_option"]
+    ex = got["exits"].astype(np.int64)
+    for w in range(0, wl.num_windows, 97):
+        g = og[fo[w]: fo[w] + 2400].reshape(300, 8)
+        c = oc[fo[w]: fo[w] + 2400].reshape(300, 8)
+        e = ex[ff[w]: ff[w] + 300]
+        assert g[np.arange(300), e].sum() == got["best_gain"][w]
+        assert c[np.arange(300), e].sum() == got["best_cost"][w] <= 4096
+
+
+def test_plan_and_solve_identical_config5():
+    wl = synth.make_config(5, num_windows=256)
+    a = gpu_run(wl, True, 0)
+    b = gpu_run(wl, False, 0)
+    for k in ("exits", "best_gain", "best_cost", "feasible", "stats"):
+        np.testing.assert_array_equal(a[k], b[k])
+
+
+def test_determinism_repeated_runs():
+    wl = synth.make_config(2)
+    a = gpu_run(wl)
+    b = gpu_run(wl)
+    for k in ("exits", "best_gain", "best_cost", "feasible", "stats"):
+        np.testing.assert_array_equal(a[k], b[k])
+
+
+def test_worked_instance_gpu():
+    """SPEC.md:269 worked instance through the whole GPU path (a1 budget 50 - 3*10 = 20)."""
+    gain = np.zeros((10, 3), np.int32)
+    gain[9] = [0, 400, 600]
+    gain[5] = [0, 100, 150]
+    cost = np.tile(np.array([0, 5, 10], np.int32), (10, 1))
+    wl = synth.Workload("worked", [gain.reshape(-1)], [cost.reshape(-1)], [(10, 3)], np.array([3], np.int32),
+                        np.array([20], np.int32), np.array([50], np.int32), 10, np.array([0], np.int32),
+                        np.array([9, 5, 9], np.uint8))
+    got = gpu_run(wl)
+    assert got["exits"].tolist() == [2, 0, 2]
+    assert int(got["best_gain"][0]) == 1200 and int(got["best_cost"][0]) == 20
+    assert int(got["budget"][0]) == 20
