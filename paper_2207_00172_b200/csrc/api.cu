@@ -51,7 +51,7 @@ static void dp_smem_words(const turbo_shape_t *s, bool solve_smem, int32_t *row_
     *cst_w = (int32_t)((int64_t)s->max_frames * s->max_exits);
 }
 
-static size_t smem_choice_limit = 64 * 1024;   // per-warp bytes above which choices go to HBM
+static size_t smem_choice_limit = 64 * 1024;   // per-CTA bytes above which choices go to HBM
 
 }  // namespace turbo
 
@@ -160,8 +160,8 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int mode, const turbo_w
     std::memset(&P, 0, sizeof(P));
     dp_smem_words(shape, mode == DP_SOLVE_SMEM, &P.row_words, &P.chs_words, &P.cst_words);
     if (mode == DP_PLAN) P.cst_words = 0;
-    P.warp_words = (P.row_words + P.chs_words + P.cst_words + 3) & ~3;
-    if ((int64_t)P.warp_words * 4 > (int64_t)d.smem_per_cta_optin) return TURBO_ERR_UNSUPPORTED;
+    P.warp_words = 0;
+    if (dp_smem_bytes(P, dp_warps_per_window(shape)) > (size_t)d.smem_per_cta_optin) return TURBO_ERR_UNSUPPORTED;
     P.windows = windows;
     P.num_windows = shape->num_windows;
     P.opt_gain = opt_gain;
@@ -212,13 +212,20 @@ turbo_status_t turbo_backtrack(const turbo_shape_t *shape, const turbo_window_t 
     return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
 }
 
+// Fused-solve variant: choice planes in shared memory when one warp's planes fit under
+// smem_choice_limit (or, when forced by the debug hook, under the per-CTA maximum).
 static int solve_mode(const turbo_shape_t *shape)
 {
-    if (g_variant == 1) return DP_SOLVE_SMEM;
     if (g_variant == 2) return DP_SOLVE_GLOBAL;
-    int32_t r, c, k;
-    dp_smem_words(shape, true, &r, &c, &k);
-    const int64_t bytes = ((int64_t)r + c + k) * 4;
+    DpParams P;
+    std::memset(&P, 0, sizeof(P));
+    dp_smem_words(shape, true, &P.row_words, &P.chs_words, &P.cst_words);
+    const int64_t bytes = (int64_t)dp_smem_bytes(P, dp_warps_per_window(shape));
+    if (g_variant == 1) {
+        DeviceInfo d;
+        if (device_info(&d) == cudaSuccess && bytes <= (int64_t)d.smem_per_cta_optin) return DP_SOLVE_SMEM;
+        return DP_SOLVE_GLOBAL;
+    }
     return bytes <= (int64_t)smem_choice_limit ? DP_SOLVE_SMEM : DP_SOLVE_GLOBAL;
 }
 

@@ -1,0 +1,300 @@
+// dp_kernel.cuh -- K2/K3/K5 (+ fused K6): the MCKP max-plus DP, one CTA of G warps per window.
+//
+// Method (§5.2, with f = sum, reading R1; exact = the paper's "upper",
+// PAPER.md:858 §6.4). Frames are processed in REVERSE (i = N-1 .. 0) so that the forward
+// backtrack realises the lexicographic tie-break with frame 0 most significant (reading R7):
+//     S_N[b] = 0,   S_i[b] = max_{k : c_ik <= b} ( g_ik + S_{i+1}[b - c_ik] ),   b = 0..B
+//     choice_i[b] = smallest maximising k;  G* = S_0[B];  C* = #{b <= B : S_0[b] < G*}
+// (S_0 is non-decreasing in b, so the count is the first b reaching G*).
+//
+// B200 mapping:
+//  * the budget row lives in shared memory; cell b = row*32 + lane, so for a warp-uniform shift
+//    c the 32 lanes read 32 consecutive words (conflict-free LDS) and one VIADDMNMX (add+max)
+//    does one option of one cell; the argmax rides in the low 4 bits of the packed key;
+//  * a tile = 8 (4-bit choices) or 16 (2-bit) rows of 32 cells: each lane packs its tile's
+//    choices into one u32 -> one coalesced 128-B store per warp per tile, to HBM (plan) or to
+//    shared memory (fused solve, when the window's planes fit);
+//  * G = 1 warp: ONE row buffer updated IN PLACE tile by tile from the top down (a cell only
+//    reads cells <= itself) with only __syncwarp; G > 1 warps: tiles t = warp, warp+G, ...,
+//    rows double-buffered, one CTA barrier per frame;
+//  * per frame, lane k < K of every warp holds option k (prefetched one frame ahead) and the
+//    warp broadcasts it with shuffles.
+#pragma once
+
+#include "turbo_internal.cuh"
+
+namespace turbo {
+
+__device__ __forceinline__ int64_t warp_sum_i64(int64_t v)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// One tile of one frame: keys of RPT rows (cells b_lo + r*32 + lane) from row `src`.
+template <int K, int RPT>
+__device__ __forceinline__ void tile_keys(const int32_t *__restrict__ src, int32_t b_lo, int32_t nr,
+                                          const int32_t (&gp)[K], const int32_t (&cc)[K], int lane,
+                                          int32_t (&key)[RPT])
+{
+    const int32_t b_hi = b_lo + nr * 32 - 1;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) key[r] = NEG_R;
+    if (nr == RPT) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int32_t c = cc[k];
+            const int32_t g = gp[k];
+            if (c <= b_lo) {                                   // every cell of the tile can take k
+                const int32_t *__restrict__ s = src + (b_lo + lane - c);
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) key[r] = max_plus(s[r * 32], g, key[r]);
+            } else if (c <= b_hi) {                            // low cells: b < c reads -inf
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) {
+                    const int32_t idx = b_lo + r * 32 + lane - c;
+                    int32_t v = src[idx < 0 ? 0 : idx];
+                    v = idx < 0 ? NEG_R : v;
+                    key[r] = max_plus(v, g, key[r]);
+                }
+            }
+        }
+    } else {                                                   // the budget row's partial top tile
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int32_t c = cc[k];
+            const int32_t g = gp[k];
+            if (c <= b_hi) {
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) {
+                    if (r < nr) {
+                        const int32_t idx = b_lo + r * 32 + lane - c;
+                        int32_t v = src[idx < 0 ? 0 : idx];
+                        v = idx < 0 ? NEG_R : v;
+                        key[r] = max_plus(v, g, key[r]);
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <int K, int MODE>
+__device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t *__restrict__ rowA,
+                                          int32_t *__restrict__ rowB, uint32_t *__restrict__ sch,
+                                          int32_t *__restrict__ cst, int64_t *__restrict__ red, int warp,
+                                          int nwarps, int lane)
+{
+    constexpr int CB = (K <= 4) ? 2 : 4;          // choice bits
+    constexpr int RPT = 32 / CB;                   // rows of 32 cells per tile (per choice word)
+    constexpr uint32_t CMASK = (1u << CB) - 1u;
+    const bool inplace = (nwarps == 1);
+
+    const turbo_window_t *win = P.windows + w;
+    const int64_t ff = win->first_frame;
+    const int64_t fo = win->first_option;
+    const int32_t N = win->num_frames;
+    const int32_t B = win->budget;
+    const int32_t Bb = win->budget_bound;
+    const int64_t choff = win->choice_offset;
+
+    const int32_t *__restrict__ og = P.opt_gain + fo;
+    const int32_t *__restrict__ oc = P.opt_cost + fo;
+
+    // ---- prologue (warp 0): validation + sums for the infeasible report (reading R8)
+    if (warp == 0) {
+        int64_t abs_sum = 0, g0_sum = 0, c0_sum = 0;
+        bool bad = (B < 0) || (B > Bb);
+        for (int32_t i = lane; i < N; i += 32) {
+            int32_t m = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int32_t g = __ldg(og + (int64_t)i * K + k);
+                const int32_t c = __ldg(oc + (int64_t)i * K + k);
+                const int32_t a = g < 0 ? -g : g;
+                m = a > m ? a : m;
+                bad |= (c < 0) || (c >= (1 << 30)) || (g > (1 << 24)) || (g < -(1 << 24));
+                if (k == 0) {
+                    g0_sum += g;
+                    c0_sum += c;
+                }
+            }
+            abs_sum += m;
+        }
+        abs_sum = warp_sum_i64(abs_sum);
+        g0_sum = warp_sum_i64(g0_sum);
+        c0_sum = warp_sum_i64(c0_sum);
+        bad = __any_sync(0xffffffffu, bad) || abs_sum >= GAIN_RANGE_LIMIT || c0_sum >= 0x7fffffffll;
+        if (lane == 0) {
+            red[0] = bad ? 1 : 0;
+            red[1] = g0_sum;
+            red[2] = c0_sum;
+            red[3] = 0;                                   // C* counter
+        }
+    }
+    const int32_t nrows = (B + 32) >> 5;
+    const int32_t ntiles = (nrows + RPT - 1) / RPT;
+    // S_N = 0 on every cell (including the padding cells above B in the top row)
+    for (int32_t x = warp * 32 + lane; x < nrows * 32; x += nwarps * 32) rowA[x] = 0;
+    if (nwarps > 1) __syncthreads(); else __syncwarp();
+    if (red[0]) {
+        if (warp == 0 && lane == 0) {
+            P.best_gain[w] = 0;
+            P.best_cost[w] = 0;
+            P.feasible[w] = 0;
+            atomic_min_i64(&P.status[1], w);
+        }
+        if (MODE != DP_PLAN)
+            for (int32_t i = warp * 32 + lane; i < N; i += nwarps * 32) P.exit_out[ff + i] = 0;
+        return;
+    }
+
+    // choice-plane stride (tiles per frame): the layout bound for HBM planes, exact for smem
+    const int32_t gtiles = (int32_t)(((Bb + 32) >> 5) + RPT - 1) / RPT;
+    uint32_t *__restrict__ gch = reinterpret_cast<uint32_t *>(P.workspace + choff);
+
+    int32_t my_gp = 0, my_c = 0;                          // option `lane` of the current frame
+    if (N > 0 && lane < K) {
+        my_gp = (__ldg(og + (int64_t)(N - 1) * K + lane) << 4) | (15 - lane);
+        my_c = __ldg(oc + (int64_t)(N - 1) * K + lane);
+    }
+    int32_t *__restrict__ cur = rowA;
+    int32_t *__restrict__ nxt = inplace ? rowA : rowB;
+
+    for (int32_t i = N - 1; i >= 0; --i) {
+        int32_t gp[K], cc[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            gp[k] = __shfl_sync(0xffffffffu, my_gp, k);
+            cc[k] = __shfl_sync(0xffffffffu, my_c, k);
+        }
+        if (MODE != DP_PLAN && warp == 0 && lane < K) cst[i * K + lane] = my_c;
+        if (i > 0 && lane < K) {                          // prefetch frame i-1
+            my_gp = (__ldg(og + (int64_t)(i - 1) * K + lane) << 4) | (15 - lane);
+            my_c = __ldg(oc + (int64_t)(i - 1) * K + lane);
+        }
+        // in place: top-down so a tile's reads never see the updated tiles above it
+        const int32_t t0 = inplace ? ntiles - 1 : warp;
+        const int32_t dt = inplace ? -1 : nwarps;
+        for (int32_t t = t0; t >= 0 && t < ntiles; t += dt) {
+            const int32_t b_lo = t * RPT * 32;
+            const int32_t nr = min(RPT, nrows - t * RPT);
+            int32_t key[RPT];
+            tile_keys<K, RPT>(cur, b_lo, nr, gp, cc, lane, key);
+            if (inplace) __syncwarp();                    // all reads of this tile done
+            uint32_t word = 0;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                if (r < nr) nxt[b_lo + r * 32 + lane] = key[r] & ~15;
+                word |= ((uint32_t)key[r] & CMASK) << (CB * r);
+            }
+            word ^= 0xffffffffu;                          // tag (15 - k) -> k per field
+            if (MODE == DP_SOLVE_SMEM)
+                sch[(i * ntiles + t) * 32 + lane] = word;
+            else
+                gch[((int64_t)i * gtiles + t) * 32 + lane] = word;
+        }
+        if (nwarps > 1) __syncthreads(); else __syncwarp();   // frame i visible to frame i-1
+        int32_t *tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+    }
+    // after the swap `cur` holds S_0 (in place: cur == nxt == rowA)
+
+    // ---- a4: optimum extraction
+    const int32_t RB = cur[B];
+    const bool feas = RB > VALID_MIN_R;
+    int32_t cnt = 0;
+    for (int32_t b = warp * 32 + lane; b <= B; b += nwarps * 32) cnt += cur[b] < RB ? 1 : 0;
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (nwarps > 1) {
+        if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(&red[3]), (unsigned long long)cnt);
+        __syncthreads();
+        cnt = (int32_t)red[3];
+    }
+    const int32_t G = feas ? (RB >> 4) : (int32_t)red[1];
+    const int32_t Cst = feas ? cnt : (int32_t)red[2];
+    if (warp == 0 && lane == 0) {
+        P.best_gain[w] = G;
+        P.best_cost[w] = Cst;
+        P.feasible[w] = feas ? 1 : 0;
+    }
+    if (MODE == DP_PLAN) return;
+
+    // ---- a5 fused: forward backtrack from (frame 0, b = C*)
+    if (!feas) {
+        for (int32_t i = warp * 32 + lane; i < N; i += nwarps * 32) P.exit_out[ff + i] = 0;
+        return;
+    }
+    if (warp == 0 && lane == 0) {
+        int32_t b = Cst;
+        for (int32_t i = 0; i < N; ++i) {
+            const int32_t t = b / (32 * RPT);
+            const int32_t j = (b >> 5) & (RPT - 1);
+            uint32_t word;
+            if (MODE == DP_SOLVE_SMEM)
+                word = sch[(i * ntiles + t) * 32 + (b & 31)];
+            else
+                word = gch[((int64_t)i * gtiles + t) * 32 + (b & 31)];
+            const int32_t k = (int32_t)((word >> (CB * j)) & CMASK);
+            P.exit_out[ff + i] = (uint8_t)k;
+            b -= cst[i * K + k];
+        }
+    }
+}
+
+// smem layout per CTA: [red: 4 x int64][rowA][rowB (G > 1)][choice planes (solve smem)][costs]
+template <int KSEL, int MODE>
+__global__ void __launch_bounds__(256) dp_cta_kernel(DpParams P)
+{
+    extern __shared__ int4 smem_raw[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int nwarps = blockDim.x >> 5;
+    int64_t *red = reinterpret_cast<int64_t *>(smem_raw);
+    int32_t *rowA = reinterpret_cast<int32_t *>(smem_raw) + 8;
+    int32_t *rowB = rowA + P.row_words;
+    int32_t *after = rowA + (nwarps > 1 ? 2 : 1) * P.row_words;
+    uint32_t *sch = reinterpret_cast<uint32_t *>(after);
+    int32_t *cst = after + P.chs_words;
+    for (int64_t w = blockIdx.x; w < P.num_windows; w += gridDim.x) {
+        if (KSEL != 0) {
+            dp_window<(KSEL > 0 ? KSEL : 2), MODE>(P, w, rowA, rowB, sch, cst, red, warp, nwarps, lane);
+        } else {
+            switch (P.windows[w].num_exits) {
+#define TURBO_K_CASE(KK) \
+    case KK: dp_window<KK, MODE>(P, w, rowA, rowB, sch, cst, red, warp, nwarps, lane); break;
+                TURBO_K_CASE(2) TURBO_K_CASE(3) TURBO_K_CASE(4) TURBO_K_CASE(5) TURBO_K_CASE(6)
+                TURBO_K_CASE(7) TURBO_K_CASE(8) TURBO_K_CASE(9) TURBO_K_CASE(10) TURBO_K_CASE(11)
+                TURBO_K_CASE(12) TURBO_K_CASE(13) TURBO_K_CASE(14) TURBO_K_CASE(15) TURBO_K_CASE(16)
+#undef TURBO_K_CASE
+                default: break;
+            }
+        }
+        __syncthreads();                              // smem reused by the next window
+    }
+}
+
+typedef void (*dp_kernel_t)(DpParams);
+
+template <int MODE>
+dp_kernel_t pick_dp_kernel(int kmin, int kmax)
+{
+    if (kmin != kmax) return dp_cta_kernel<0, MODE>;
+    switch (kmin) {
+#define TURBO_K_PICK(KK) \
+    case KK: return dp_cta_kernel<KK, MODE>;
+        TURBO_K_PICK(2) TURBO_K_PICK(3) TURBO_K_PICK(4) TURBO_K_PICK(5) TURBO_K_PICK(6)
+        TURBO_K_PICK(7) TURBO_K_PICK(8) TURBO_K_PICK(9) TURBO_K_PICK(10) TURBO_K_PICK(11)
+        TURBO_K_PICK(12) TURBO_K_PICK(13) TURBO_K_PICK(14) TURBO_K_PICK(15) TURBO_K_PICK(16)
+#undef TURBO_K_PICK
+        default: return dp_cta_kernel<0, MODE>;
+    }
+}
+
+dp_kernel_t dp_kernel_plan(int kmin, int kmax);
+dp_kernel_t dp_kernel_solve_smem(int kmin, int kmax);
+dp_kernel_t dp_kernel_solve_global(int kmin, int kmax);
+
+}  // namespace turbo

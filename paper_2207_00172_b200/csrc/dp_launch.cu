@@ -1,0 +1,103 @@
+// dp_launch.cu -- launch configuration of the DP kernels (dp_kernel.cuh).
+#include <map>
+#include <mutex>
+#include <utility>
+
+#include "dp_kernel.cuh"
+
+namespace turbo {
+
+// Windows resident per SM, s, minimising ceil(W / (num_sms * s)) * s: equal windows finish in
+// waves, so the partly filled last wave is the quantisation loss; ties go to the larger s.
+static int pick_concurrency(int64_t W, int num_sms, int s_max)
+{
+    int best_s = 1;
+    int64_t best_cost = INT64_MAX;
+    for (int s = 1; s <= s_max; ++s) {
+        const int64_t slots = (int64_t)num_sms * s;
+        const int64_t cost = ((W + slots - 1) / slots) * s;
+        if (cost < best_cost || (cost == best_cost && s > best_s)) {
+            best_cost = cost;
+            best_s = s;
+        }
+    }
+    return best_s;
+}
+
+// Warps per window: one warp (in-place row) when the row is a single tile, else up to 8
+// warps sharing the tiles (double-buffered row).
+int dp_warps_per_window(const turbo_shape_t *s)
+{
+    const int rpt = s->max_exits <= 4 ? 16 : 8;
+    const int64_t tiles = (num_rows(s->max_budget) + rpt - 1) / rpt;
+    if (tiles <= 1) return 1;
+    return tiles >= 8 ? 8 : (int)tiles;
+}
+
+static cudaError_t prepare(dp_kernel_t kern, size_t smem)
+{
+    static std::mutex mu;
+    static std::map<std::pair<int, const void *>, size_t> limit;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(dev, (const void *)kern);
+    auto it = limit.find(key);
+    if (it == limit.end()) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                             (int)cudaSharedmemCarveoutMaxShared);
+        if (e != cudaSuccess) return e;
+        it = limit.emplace(key, 0).first;
+    }
+    if (smem > it->second) {     // the attribute call is not free: only when the need grows
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        it->second = smem;
+    }
+    return cudaSuccess;
+}
+
+size_t dp_smem_bytes(const DpParams &P, int nwarps)
+{
+    return 64 + (size_t)4 * ((size_t)(nwarps > 1 ? 2 : 1) * P.row_words + P.chs_words + P.cst_words);
+}
+
+cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P0, int num_sms, int smem_per_sm,
+                      int smem_per_cta_max, cudaStream_t stream, DpLaunch *info)
+{
+    DpParams P = P0;
+    const int64_t W = shape->num_windows;
+    if (W <= 0) return cudaSuccess;
+    const int G = dp_warps_per_window(shape);
+    P.warps_per_cta = G;
+    const size_t need = dp_smem_bytes(P, G);
+    if (need > (size_t)smem_per_cta_max) return cudaErrorInvalidConfiguration;
+    const size_t reserve = 1024;                       // per-CTA system reservation on sm_100
+    int s_max = (int)(smem_per_sm / (need + reserve));
+    const int s_thr = 2048 / (32 * G);
+    if (s_max > s_thr) s_max = s_thr;
+    if (s_max > 32) s_max = 32;
+    if (s_max < 1) s_max = 1;
+    const int s = pick_concurrency(W, num_sms, s_max);
+    size_t smem = need;                                // pad so that exactly s CTAs fit per SM
+    size_t padded = (size_t)smem_per_sm / s - reserve;
+    if (padded > (size_t)smem_per_cta_max) padded = smem_per_cta_max;
+    padded &= ~(size_t)15;
+    if (padded > smem) smem = padded;
+    dp_kernel_t kern = mode == DP_PLAN         ? dp_kernel_plan(shape->min_exits, shape->max_exits)
+                       : mode == DP_SOLVE_SMEM ? dp_kernel_solve_smem(shape->min_exits, shape->max_exits)
+                                               : dp_kernel_solve_global(shape->min_exits, shape->max_exits);
+    cudaError_t e = prepare(kern, smem);
+    if (e != cudaSuccess) return e;
+    const int64_t blocks = W;
+    kern<<<(unsigned)blocks, 32 * G, smem, stream>>>(P);
+    if (info) {
+        info->mode = mode;
+        info->warps_per_cta = G;
+        info->blocks = (int)blocks;
+        info->smem_bytes = smem;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace turbo

@@ -81,6 +81,8 @@ cudaError_t launch_lookup(const turbo_profile_t *profiles, turbo_window_t *windo
                           int32_t *opt_cost, int64_t *status, int num_sms, cudaStream_t stream);
 cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P, int num_sms, int smem_per_sm,
                       int smem_per_cta_max, cudaStream_t stream, DpLaunch *info);
+int dp_warps_per_window(const turbo_shape_t *shape);
+size_t dp_smem_bytes(const DpParams &P, int nwarps);
 cudaError_t launch_backtrack(const turbo_window_t *windows, int32_t num_windows, const int32_t *opt_cost,
                              const uint8_t *workspace, const int32_t *best_cost, const uint8_t *feasible,
                              uint8_t *exit_out, int num_sms, cudaStream_t stream);
