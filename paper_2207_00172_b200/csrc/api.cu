@@ -51,6 +51,14 @@ static void dp_smem_words(const turbo_shape_t *s, bool solve_smem, int32_t *row_
     *cst_w = (int32_t)((int64_t)s->max_frames * s->max_exits);
 }
 
+// -inf pad below each row: shifts up to this many cells need no bounds check (one 4-bit tile;
+// capped by the row itself, since a shift above B + 1 is never feasible anyway)
+static int32_t dp_pad_words(const turbo_shape_t *s)
+{
+    const int64_t row = num_rows(s->max_budget) * 32;
+    return (int32_t)(row < 256 ? row : 256);
+}
+
 static size_t smem_choice_limit = 64 * 1024;   // per-CTA bytes above which choices go to HBM
 
 }  // namespace turbo
@@ -161,6 +169,7 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int mode, const turbo_w
     dp_smem_words(shape, mode == DP_SOLVE_SMEM, &P.row_words, &P.chs_words, &P.cst_words);
     if (mode == DP_PLAN) P.cst_words = 0;
     P.warp_words = 0;
+    P.pad_words = dp_pad_words(shape);
     if (dp_smem_bytes(P, dp_warps_per_window(shape)) > (size_t)d.smem_per_cta_optin) return TURBO_ERR_UNSUPPORTED;
     P.windows = windows;
     P.num_windows = shape->num_windows;
@@ -220,6 +229,7 @@ static int solve_mode(const turbo_shape_t *shape)
     DpParams P;
     std::memset(&P, 0, sizeof(P));
     dp_smem_words(shape, true, &P.row_words, &P.chs_words, &P.cst_words);
+    P.pad_words = dp_pad_words(shape);
     const int64_t bytes = (int64_t)dp_smem_bytes(P, dp_warps_per_window(shape));
     if (g_variant == 1) {
         DeviceInfo d;

@@ -33,47 +33,39 @@ __device__ __forceinline__ int64_t warp_sum_i64(int64_t v)
 }
 
 // One tile of one frame: keys of RPT rows (cells b_lo + r*32 + lane) from row `src`.
+// `src` is preceded by `pad` words of -inf, so an option whose shift stays inside the pad
+// (c <= b_lo + pad) needs no bounds check; only larger shifts in the lowest tiles take the
+// predicated path (cells b < c read -inf).
 template <int K, int RPT>
-__device__ __forceinline__ void tile_keys(const int32_t *__restrict__ src, int32_t b_lo, int32_t nr,
+__device__ __forceinline__ void tile_keys(const int32_t *__restrict__ src, int32_t b_lo, int32_t nr, int32_t pad,
                                           const int32_t (&gp)[K], const int32_t (&cc)[K], int lane,
                                           int32_t (&key)[RPT])
 {
     const int32_t b_hi = b_lo + nr * 32 - 1;
 #pragma unroll
     for (int r = 0; r < RPT; ++r) key[r] = NEG_R;
-    if (nr == RPT) {
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const int32_t c = cc[k];
-            const int32_t g = gp[k];
-            if (c <= b_lo) {                                   // every cell of the tile can take k
-                const int32_t *__restrict__ s = src + (b_lo + lane - c);
+    for (int k = 0; k < K; ++k) {
+        const int32_t c = cc[k];
+        const int32_t g = gp[k];
+        if (c <= b_lo + pad) {                                // unchecked: shifts stay in the pad
+            const int32_t *__restrict__ s = src + (b_lo + lane - c);
+            if (nr == RPT) {
 #pragma unroll
                 for (int r = 0; r < RPT; ++r) key[r] = max_plus(s[r * 32], g, key[r]);
-            } else if (c <= b_hi) {                            // low cells: b < c reads -inf
+            } else {
 #pragma unroll
-                for (int r = 0; r < RPT; ++r) {
+                for (int r = 0; r < RPT; ++r)
+                    if (r < nr) key[r] = max_plus(s[r * 32], g, key[r]);
+            }
+        } else if (c <= b_hi) {                               // low cells: b < c reads -inf
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) {
+                if (r < nr) {
                     const int32_t idx = b_lo + r * 32 + lane - c;
                     int32_t v = src[idx < 0 ? 0 : idx];
                     v = idx < 0 ? NEG_R : v;
                     key[r] = max_plus(v, g, key[r]);
-                }
-            }
-        }
-    } else {                                                   // the budget row's partial top tile
-#pragma unroll
-        for (int k = 0; k < K; ++k) {
-            const int32_t c = cc[k];
-            const int32_t g = gp[k];
-            if (c <= b_hi) {
-#pragma unroll
-                for (int r = 0; r < RPT; ++r) {
-                    if (r < nr) {
-                        const int32_t idx = b_lo + r * 32 + lane - c;
-                        int32_t v = src[idx < 0 ? 0 : idx];
-                        v = idx < 0 ? NEG_R : v;
-                        key[r] = max_plus(v, g, key[r]);
-                    }
                 }
             }
         }
@@ -181,7 +173,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
             const int32_t b_lo = t * RPT * 32;
             const int32_t nr = min(RPT, nrows - t * RPT);
             int32_t key[RPT];
-            tile_keys<K, RPT>(cur, b_lo, nr, gp, cc, lane, key);
+            tile_keys<K, RPT>(cur, b_lo, nr, P.pad_words, gp, cc, lane, key);
             if (inplace) __syncwarp();                    // all reads of this tile done
             uint32_t word = 0;
 #pragma unroll
@@ -244,7 +236,8 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     }
 }
 
-// smem layout per CTA: [red: 4 x int64][rowA][rowB (G > 1)][choice planes (solve smem)][costs]
+// smem layout per CTA: [red: 8 x int64][pad][rowA][pad][rowB (G > 1)][choice planes (solve)][costs]
+// The pads (pad_words of -inf below each row buffer) are written once and never overwritten.
 template <int KSEL, int MODE>
 __global__ void __launch_bounds__(256) dp_cta_kernel(DpParams P)
 {
@@ -253,11 +246,18 @@ __global__ void __launch_bounds__(256) dp_cta_kernel(DpParams P)
     const int warp = threadIdx.x >> 5;
     const int nwarps = blockDim.x >> 5;
     int64_t *red = reinterpret_cast<int64_t *>(smem_raw);
-    int32_t *rowA = reinterpret_cast<int32_t *>(smem_raw) + 8;
-    int32_t *rowB = rowA + P.row_words;
-    int32_t *after = rowA + (nwarps > 1 ? 2 : 1) * P.row_words;
+    int32_t *base = reinterpret_cast<int32_t *>(smem_raw) + 16;
+    const int32_t stride = P.pad_words + P.row_words;
+    int32_t *rowA = base + P.pad_words;
+    int32_t *rowB = rowA + stride;
+    int32_t *after = base + (nwarps > 1 ? 2 : 1) * stride;
     uint32_t *sch = reinterpret_cast<uint32_t *>(after);
     int32_t *cst = after + P.chs_words;
+    for (int32_t x = threadIdx.x; x < P.pad_words; x += blockDim.x) {
+        rowA[x - P.pad_words] = NEG_R;
+        if (nwarps > 1) rowB[x - P.pad_words] = NEG_R;
+    }
+    __syncthreads();
     for (int64_t w = blockIdx.x; w < P.num_windows; w += gridDim.x) {
         if (KSEL != 0) {
             dp_window<(KSEL > 0 ? KSEL : 2), MODE>(P, w, rowA, rowB, sch, cst, red, warp, nwarps, lane);

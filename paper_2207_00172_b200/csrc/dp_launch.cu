@@ -59,7 +59,8 @@ static cudaError_t prepare(dp_kernel_t kern, size_t smem)
 
 size_t dp_smem_bytes(const DpParams &P, int nwarps)
 {
-    return 64 + (size_t)4 * ((size_t)(nwarps > 1 ? 2 : 1) * P.row_words + P.chs_words + P.cst_words);
+    return 64 + (size_t)4 * ((size_t)(nwarps > 1 ? 2 : 1) * (P.pad_words + P.row_words) + P.chs_words +
+                             P.cst_words);
 }
 
 cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P0, int num_sms, int smem_per_sm,

@@ -57,7 +57,8 @@ struct DpParams {
     int32_t row_words;      // per-warp row capacity (multiple of 32)
     int32_t chs_words;      // per-warp smem choice capacity (DP_SOLVE_SMEM)
     int32_t cst_words;      // per-warp smem cost table capacity (solve modes)
-    int32_t warp_words;     // total smem words per warp
+    int32_t warp_words;     // unused (0)
+    int32_t pad_words;      // -inf words below each row buffer (unchecked shifts up to this)
     int32_t warps_per_cta;
     const int32_t *opt_gain;
     const int32_t *opt_cost;
