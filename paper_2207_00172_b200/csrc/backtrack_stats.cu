@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(256) backtrack_kernel(const turbo_window_t *__
         const int32_t *__restrict__ oc = opt_cost + fo;
         auto fetch = [&](int32_t i, int32_t b) -> int32_t {  // choice of frame i at cell b
             const uint32_t word = __ldg(gch + ((int64_t)i * gtiles + (b >> lg_tile)) * 32 + (b & 31));
-            return (int32_t)((word >> (CB * ((b >> 5) & (RPT - 1)))) & cmask);
+            return (int32_t)((word >> choice_shift((b >> 5) & (RPT - 1), CB)) & cmask);
         };
         int32_t b = best_cost[w];
         int32_t i = 0;

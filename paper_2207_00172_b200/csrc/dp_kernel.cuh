@@ -72,6 +72,44 @@ __device__ __forceinline__ void tile_keys(const int32_t *__restrict__ src, int32
     }
 }
 
+// Fast path of one full tile whose every shift stays inside the -inf pad (no bounds checks):
+// per option one address add, RPT conflict-free LDS and RPT VIADDMNMX.
+template <int K, int RPT>
+__device__ __forceinline__ void tile_keys_fast(const int32_t *__restrict__ src_lane, int32_t b_lo,
+                                               const int32_t (&gp)[K], const int32_t (&cc)[K],
+                                               int32_t (&key)[RPT])
+{
+    {
+        const int32_t *__restrict__ s = src_lane + (b_lo - cc[0]);
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) key[r] = s[r * 32] + gp[0];
+    }
+#pragma unroll
+    for (int k = 1; k < K; ++k) {
+        const int32_t *__restrict__ s = src_lane + (b_lo - cc[k]);
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) key[r] = max_plus(s[r * 32], gp[k], key[r]);
+    }
+}
+
+// Choice word of a tile: the tags (low CB bits of every key) of its RPT rows, gathered with
+// byte permutes. Row j's field sits at bit choice_shift(j) = 8 (j & 3) + CB (j >> 2); the final
+// NOT turns every tag (15 - k) into k (all 32 bits are fields).
+template <int RPT, int CB>
+__device__ __forceinline__ uint32_t pack_choices(const int32_t (&key)[RPT])
+{
+    constexpr uint32_t FM = ((1u << CB) - 1u) * 0x01010101u;
+    uint32_t w = 0;
+#pragma unroll
+    for (int m = 0; m < RPT / 4; ++m) {
+        const uint32_t lo = __byte_perm((uint32_t)key[4 * m], (uint32_t)key[4 * m + 1], 0x0040);
+        const uint32_t hi = __byte_perm((uint32_t)key[4 * m + 2], (uint32_t)key[4 * m + 3], 0x0040);
+        const uint32_t q = __byte_perm(lo, hi, 0x5410);
+        w |= (q & FM) << (CB * m);
+    }
+    return ~w;
+}
+
 template <int K, int MODE>
 __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t *__restrict__ rowA,
                                           int32_t *__restrict__ rowB, uint32_t *__restrict__ sch,
@@ -166,6 +204,10 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
             my_gp = (__ldg(og + (int64_t)(i - 1) * K + lane) << 4) | (15 - lane);
             my_c = __ldg(oc + (int64_t)(i - 1) * K + lane);
         }
+        int32_t cmax = cc[0];
+#pragma unroll
+        for (int k = 1; k < K; ++k) cmax = max(cmax, cc[k]);
+        const int32_t *__restrict__ cur_lane = cur + lane;
         // in place: top-down so a tile's reads never see the updated tiles above it
         const int32_t t0 = inplace ? ntiles - 1 : warp;
         const int32_t dt = inplace ? -1 : nwarps;
@@ -173,15 +215,22 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
             const int32_t b_lo = t * RPT * 32;
             const int32_t nr = min(RPT, nrows - t * RPT);
             int32_t key[RPT];
-            tile_keys<K, RPT>(cur, b_lo, nr, P.pad_words, gp, cc, lane, key);
+            const bool fast = (nr == RPT) && (cmax <= b_lo + P.pad_words);
+            if (fast)
+                tile_keys_fast<K, RPT>(cur_lane, b_lo, gp, cc, key);
+            else
+                tile_keys<K, RPT>(cur, b_lo, nr, P.pad_words, gp, cc, lane, key);
             if (inplace) __syncwarp();                    // all reads of this tile done
-            uint32_t word = 0;
+            int32_t *__restrict__ dst = nxt + b_lo + lane;
+            if (fast) {
 #pragma unroll
-            for (int r = 0; r < RPT; ++r) {
-                if (r < nr) nxt[b_lo + r * 32 + lane] = key[r] & ~15;
-                word |= ((uint32_t)key[r] & CMASK) << (CB * r);
+                for (int r = 0; r < RPT; ++r) dst[r * 32] = key[r] & ~15;
+            } else {
+#pragma unroll
+                for (int r = 0; r < RPT; ++r)
+                    if (r < nr) dst[r * 32] = key[r] & ~15;
             }
-            word ^= 0xffffffffu;                          // tag (15 - k) -> k per field
+            const uint32_t word = pack_choices<RPT, CB>(key);
             if (MODE == DP_SOLVE_SMEM)
                 sch[(i * ntiles + t) * 32 + lane] = word;
             else
@@ -229,7 +278,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
                 word = sch[(i * ntiles + t) * 32 + (b & 31)];
             else
                 word = gch[((int64_t)i * gtiles + t) * 32 + (b & 31)];
-            const int32_t k = (int32_t)((word >> (CB * j)) & CMASK);
+            const int32_t k = (int32_t)((word >> choice_shift(j, CB)) & CMASK);
             P.exit_out[ff + i] = (uint8_t)k;
             b -= cst[i * K + k];
         }

@@ -1,6 +1,7 @@
 // dp_launch.cu -- launch configuration of the DP kernels (dp_kernel.cuh).
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <utility>
 
 #include "dp_kernel.cuh"
@@ -73,23 +74,51 @@ cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P0, 
     P.warps_per_cta = G;
     const size_t need = dp_smem_bytes(P, G);
     if (need > (size_t)smem_per_cta_max) return cudaErrorInvalidConfiguration;
-    const size_t reserve = 1024;                       // per-CTA system reservation on sm_100
-    int s_max = (int)(smem_per_sm / (need + reserve));
-    const int s_thr = 2048 / (32 * G);
-    if (s_max > s_thr) s_max = s_thr;
-    if (s_max > 32) s_max = 32;
-    if (s_max < 1) s_max = 1;
-    const int s = pick_concurrency(W, num_sms, s_max);
-    size_t smem = need;                                // pad so that exactly s CTAs fit per SM
-    size_t padded = (size_t)smem_per_sm / s - reserve;
-    if (padded > (size_t)smem_per_cta_max) padded = smem_per_cta_max;
-    padded &= ~(size_t)15;
-    if (padded > smem) smem = padded;
     dp_kernel_t kern = mode == DP_PLAN         ? dp_kernel_plan(shape->min_exits, shape->max_exits)
                        : mode == DP_SOLVE_SMEM ? dp_kernel_solve_smem(shape->min_exits, shape->max_exits)
                                                : dp_kernel_solve_global(shape->min_exits, shape->max_exits);
-    cudaError_t e = prepare(kern, smem);
+    cudaError_t e = prepare(kern, (size_t)smem_per_cta_max);
     if (e != cudaSuccess) return e;
+    // s_max from the occupancy calculator (it knows the per-CTA reservation and the carveout);
+    // results are cached per (device, kernel, G, need, W) -- the queries are host-side only
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void *, int, size_t, int64_t>, size_t> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto ckey = std::make_tuple(dev, (const void *)kern, G, need, W);
+    size_t smem = need;
+    bool cached = false;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(ckey);
+        if (it != cache.end()) {
+            smem = it->second;
+            cached = true;
+        }
+    }
+    int s_max = 0;
+    if (!cached) {
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s_max, kern, 32 * G, need);
+        if (e != cudaSuccess) return e;
+        if (s_max < 1) return cudaErrorInvalidConfiguration;
+    }
+    const int s = cached ? 0 : pick_concurrency(W, num_sms, s_max);
+    // pad the dynamic smem so that exactly s CTAs fit per SM (occupancy as a knob)
+    if (!cached && s < s_max) {
+        size_t hi = (size_t)smem_per_cta_max, lo = need;     // largest smem with occupancy >= s
+        while (hi - lo > 16) {
+            const size_t mid = ((lo + hi) / 2) & ~(size_t)15;
+            int occ = 0;
+            e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 32 * G, mid);
+            if (e != cudaSuccess) return e;
+            if (occ >= s) lo = mid; else hi = mid;
+        }
+        smem = lo;
+    }
+    if (!cached) {
+        std::lock_guard<std::mutex> lk(mu);
+        cache[ckey] = smem;
+    }
     const int64_t blocks = W;
     kern<<<(unsigned)blocks, 32 * G, smem, stream>>>(P);
     if (info) {

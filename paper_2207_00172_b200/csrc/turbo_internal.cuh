@@ -37,6 +37,9 @@ __host__ __device__ __forceinline__ int64_t choice_plane_bytes(int64_t N, int64_
     return N * num_tiles(B, K) * 128;
 }
 
+// bit offset of row j's choice field inside its tile word (see pack_choices in dp_kernel.cuh)
+__host__ __device__ __forceinline__ int choice_shift(int j, int CB) { return 8 * (j & 3) + CB * (j >> 2); }
+
 __device__ __forceinline__ int32_t max_plus(int32_t a, int32_t b, int32_t c) {
     return __viaddmax_s32(a, b, c);          // max(a + b, c): one VIADDMNMX on sm_90+/sm_100a
 }
