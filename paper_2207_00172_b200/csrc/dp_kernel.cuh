@@ -288,7 +288,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
 // smem layout per CTA: [red: 8 x int64][pad][rowA][pad][rowB (G > 1)][choice planes (solve)][costs]
 // The pads (pad_words of -inf below each row buffer) are written once and never overwritten.
 template <int KSEL, int MODE>
-__global__ void __launch_bounds__(256) dp_cta_kernel(DpParams P)
+__global__ void __launch_bounds__(256, 4) dp_cta_kernel(DpParams P)
 {
     extern __shared__ int4 smem_raw[];
     const int lane = threadIdx.x & 31;

@@ -1,4 +1,5 @@
 // dp_launch.cu -- launch configuration of the DP kernels (dp_kernel.cuh).
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -8,21 +9,24 @@
 
 namespace turbo {
 
-// Windows resident per SM, s, minimising ceil(W / (num_sms * s)) * s: equal windows finish in
-// waves, so the partly filled last wave is the quantisation loss; ties go to the larger s.
+// Windows resident per SM, s. Equal windows finish in waves; when the SM is throughput-bound a
+// wave of s windows costs ~s, so ceil(W / (num_sms * s)) * s measures the partly filled last
+// wave. More resident warps also hide latency, so take the LARGEST s whose cost is within 5%
+// of the minimum.
 static int pick_concurrency(int64_t W, int num_sms, int s_max)
 {
-    int best_s = 1;
     int64_t best_cost = INT64_MAX;
     for (int s = 1; s <= s_max; ++s) {
         const int64_t slots = (int64_t)num_sms * s;
         const int64_t cost = ((W + slots - 1) / slots) * s;
-        if (cost < best_cost || (cost == best_cost && s > best_s)) {
-            best_cost = cost;
-            best_s = s;
-        }
+        if (cost < best_cost) best_cost = cost;
     }
-    return best_s;
+    for (int s = s_max; s >= 1; --s) {
+        const int64_t slots = (int64_t)num_sms * s;
+        const int64_t cost = ((W + slots - 1) / slots) * s;
+        if (cost * 100 <= best_cost * 105) return s;
+    }
+    return 1;
 }
 
 // Warps per window: one warp (in-place row) when the row is a single tile, else up to 8
@@ -31,6 +35,12 @@ int dp_warps_per_window(const turbo_shape_t *s)
 {
     const int rpt = s->max_exits <= 4 ? 16 : 8;
     const int64_t tiles = (num_rows(s->max_budget) + rpt - 1) / rpt;
+    static int forced = -1;
+    if (forced < 0) {
+        const char *e = getenv("TURBO_DP_WARPS");          // tuning override (1, 2, 4, 8)
+        forced = e ? atoi(e) : 0;
+    }
+    if (forced > 0 && tiles > 1) return forced > 8 ? 8 : forced;
     if (tiles <= 1) return 1;
     return tiles >= 8 ? 8 : (int)tiles;
 }
