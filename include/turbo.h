@@ -177,8 +177,10 @@ turbo_status_t turbo_stats(const turbo_shape_t *shape /* host */, const turbo_wi
                            const int32_t *best_gain, const int32_t *best_cost,
                            const uint8_t *feasible, int64_t *stats, turbo_stream_t stream);
 
-/* Debug / test hooks: force a DP kernel variant (0 = automatic) and report the last
- * launch configuration chosen. Not needed in production. */
+/* Debug / test hook: force a DP kernel variant. variant & 3: 0 = automatic, 1 = fused solve
+ * keeps choice planes in shared memory (when they fit the per-CTA maximum), 2 = in HBM;
+ * variant & 4: do not stage option tables in shared memory (shuffle broadcast instead).
+ * Returns INVALID_ARG for other values. Process-wide; not needed in production. */
 turbo_status_t turbo_debug_set_variant(int32_t variant);
 const char *turbo_status_string(turbo_status_t s);
 int32_t turbo_abi_version(void);

@@ -39,16 +39,20 @@ static cudaError_t device_info(DeviceInfo *out)
     return cudaSuccess;
 }
 
-// smem words per warp for the DP: row (+ choice planes and costs for the fused solve)
-static void dp_smem_words(const turbo_shape_t *s, bool solve_smem, int32_t *row_w, int32_t *chs_w, int32_t *cst_w)
+// smem words per CTA for the DP: row, option table (osm) or backtrack costs, choice planes
+static const int64_t OSM_LIMIT_BYTES = 48 * 1024;   // largest per-window option table staged in smem
+
+static void dp_smem_words(const turbo_shape_t *s, int mode, DpParams *P)
 {
     const int64_t rows = num_rows(s->max_budget);
-    *row_w = (int32_t)(rows * 32);
+    P->row_words = (int32_t)(rows * 32);
     const int rpt_min = s->max_exits <= 4 ? 16 : 8;
     const int64_t tiles = (rows + rpt_min - 1) / rpt_min;
-    const int64_t chs = solve_smem ? (int64_t)s->max_frames * tiles * 32 : 0;
-    *chs_w = (int32_t)(chs > INT32_MAX ? INT32_MAX : chs);
-    *cst_w = (int32_t)((int64_t)s->max_frames * s->max_exits);
+    const int64_t chs = mode == DP_SOLVE_SMEM ? (int64_t)s->max_frames * tiles * 32 : 0;
+    P->chs_words = (int32_t)(chs > INT32_MAX ? INT32_MAX : chs);
+    const int64_t opts = (int64_t)s->max_frames * s->max_exits;
+    P->osm = (opts * 8 <= OSM_LIMIT_BYTES && !(g_variant & 4)) ? 1 : 0;
+    P->cst_words = P->osm ? (int32_t)(2 * opts) : (mode == DP_PLAN ? 0 : (int32_t)opts);
 }
 
 // -inf pad below each row: shifts up to this many cells need no bounds check (one 4-bit tile;
@@ -84,7 +88,7 @@ const char *turbo_status_string(turbo_status_t s)
 
 turbo_status_t turbo_debug_set_variant(int32_t variant)
 {
-    if (variant < 0 || variant > 2) return TURBO_ERR_INVALID_ARG;
+    if (variant < 0 || variant > 6 || (variant & 3) == 3) return TURBO_ERR_INVALID_ARG;
     g_variant = variant;
     return TURBO_OK;
 }
@@ -166,8 +170,7 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int mode, const turbo_w
     if (device_info(&d) != cudaSuccess) return TURBO_ERR_CUDA;
     DpParams P;
     std::memset(&P, 0, sizeof(P));
-    dp_smem_words(shape, mode == DP_SOLVE_SMEM, &P.row_words, &P.chs_words, &P.cst_words);
-    if (mode == DP_PLAN) P.cst_words = 0;
+    dp_smem_words(shape, mode, &P);
     P.warp_words = 0;
     P.pad_words = dp_pad_words(shape);
     if (dp_smem_bytes(P, dp_warps_per_window(shape)) > (size_t)d.smem_per_cta_optin) return TURBO_ERR_UNSUPPORTED;
@@ -225,13 +228,13 @@ turbo_status_t turbo_backtrack(const turbo_shape_t *shape, const turbo_window_t 
 // smem_choice_limit (or, when forced by the debug hook, under the per-CTA maximum).
 static int solve_mode(const turbo_shape_t *shape)
 {
-    if (g_variant == 2) return DP_SOLVE_GLOBAL;
+    if ((g_variant & 3) == 2) return DP_SOLVE_GLOBAL;
     DpParams P;
     std::memset(&P, 0, sizeof(P));
-    dp_smem_words(shape, true, &P.row_words, &P.chs_words, &P.cst_words);
+    dp_smem_words(shape, DP_SOLVE_SMEM, &P);
     P.pad_words = dp_pad_words(shape);
     const int64_t bytes = (int64_t)dp_smem_bytes(P, dp_warps_per_window(shape));
-    if (g_variant == 1) {
+    if ((g_variant & 3) == 1) {
         DeviceInfo d;
         if (device_info(&d) == cudaSuccess && bytes <= (int64_t)d.smem_per_cta_optin) return DP_SOLVE_SMEM;
         return DP_SOLVE_GLOBAL;

@@ -110,16 +110,70 @@ __device__ __forceinline__ uint32_t pack_choices(const int32_t (&key)[RPT])
     return ~w;
 }
 
-template <int K, int MODE>
+// One tile t of frame i: keys from `cur`, stripped values to `nxt`, choice word to the plane.
+// OWN: the warp's first tile, whose own cells' previous values are held in registers `own`
+// (a cost-0 option 0 then needs no shared-memory read); `own` is refreshed with the new values.
+template <int K, int MODE, bool OWN>
+__device__ __forceinline__ void dp_tile(const DpParams &P, int32_t t, int32_t i, int32_t nrows, int32_t ntiles,
+                                        int32_t gtiles, const int32_t *__restrict__ cur, int32_t *__restrict__ nxt,
+                                        uint32_t *__restrict__ sch, uint32_t *__restrict__ gch,
+                                        const int32_t (&gp)[K], const int32_t (&cc)[K], int32_t cmax, bool inplace,
+                                        int lane, int32_t (&own)[(K <= 4) ? 16 : 8])
+{
+    constexpr int CB = (K <= 4) ? 2 : 4;
+    constexpr int RPT = 32 / CB;
+    const int32_t b_lo = t * RPT * 32;
+    const int32_t nr = min(RPT, nrows - t * RPT);
+    int32_t key[RPT];
+    const bool fast = (nr == RPT) && (cmax <= b_lo + P.pad_words);
+    if (fast) {
+        const int32_t *__restrict__ src = cur + lane + b_lo;
+        if (OWN && cc[0] == 0) {
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) key[r] = own[r] + gp[0];
+        } else {
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) key[r] = src[r * 32 - cc[0]] + gp[0];
+        }
+#pragma unroll
+        for (int k = 1; k < K; ++k) {
+            const int32_t *__restrict__ s = src - cc[k];
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) key[r] = max_plus(s[r * 32], gp[k], key[r]);
+        }
+    } else {
+        tile_keys<K, RPT>(cur, b_lo, nr, P.pad_words, gp, cc, lane, key);
+    }
+    if (inplace) __syncwarp();                            // all reads of this tile done
+    int32_t *__restrict__ dst = nxt + b_lo + lane;
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        const int32_t v = key[r] & ~15;
+        if (OWN) own[r] = v;
+        if (fast || r < nr) dst[r * 32] = v;
+    }
+    const uint32_t word = pack_choices<RPT, CB>(key);
+    if (MODE == DP_SOLVE_SMEM)
+        sch[(i * ntiles + t) * 32 + lane] = word;
+    else
+        gch[((int64_t)i * gtiles + t) * 32 + lane] = word;
+}
+
+// OSM: the window's options staged in shared memory as packed (g << 4 | 15 - k, c) pairs and read
+// with broadcast LDS.64; otherwise lane k holds option k (prefetched a frame ahead) and the warp
+// broadcasts it with shuffles (windows whose option table does not fit).
+template <int K, int MODE, bool OSM>
 __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t *__restrict__ rowA,
                                           int32_t *__restrict__ rowB, uint32_t *__restrict__ sch,
-                                          int32_t *__restrict__ cst, int64_t *__restrict__ red, int warp,
-                                          int nwarps, int lane)
+                                          int32_t *__restrict__ cst, int2 *__restrict__ opt_s,
+                                          int64_t *__restrict__ red, int warp, int nwarps, int lane)
 {
     constexpr int CB = (K <= 4) ? 2 : 4;          // choice bits
     constexpr int RPT = 32 / CB;                   // rows of 32 cells per tile (per choice word)
     constexpr uint32_t CMASK = (1u << CB) - 1u;
     const bool inplace = (nwarps == 1);
+    const int tid = warp * 32 + lane;
+    const int nthr = nwarps * 32;
 
     const turbo_window_t *win = P.windows + w;
     const int64_t ff = win->first_frame;
@@ -132,19 +186,40 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     const int32_t *__restrict__ og = P.opt_gain + fo;
     const int32_t *__restrict__ oc = P.opt_cost + fo;
 
-    // ---- prologue (warp 0): validation + sums for the infeasible report (reading R8)
+    // ---- prologue: stage options (OSM), validate, sums for the infeasible report (reading R8)
+    bool bad = (B < 0) || (B > Bb);
+    if (OSM) {
+        const int32_t n_opt = N * K;
+        for (int32_t o = tid; o < n_opt; o += nthr) {
+            const int32_t g = __ldg(og + o);
+            const int32_t c = __ldg(oc + o);
+            bad |= (c < 0) || (c >= (1 << 30)) || (g > (1 << 24)) || (g < -(1 << 24));
+            const int32_t k = o % K;
+            opt_s[o] = make_int2((g << 4) | (15 - k), c);
+        }
+        if (nwarps > 1)
+            bad = __syncthreads_or(bad);
+        else
+            bad = __any_sync(0xffffffffu, bad);
+    }
     if (warp == 0) {
         int64_t abs_sum = 0, g0_sum = 0, c0_sum = 0;
-        bool bad = (B < 0) || (B > Bb);
         for (int32_t i = lane; i < N; i += 32) {
             int32_t m = 0;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                const int32_t g = __ldg(og + (int64_t)i * K + k);
-                const int32_t c = __ldg(oc + (int64_t)i * K + k);
+                int32_t g, c;
+                if (OSM) {
+                    const int2 v = opt_s[i * K + k];
+                    g = v.x >> 4;
+                    c = v.y;
+                } else {
+                    g = __ldg(og + (int64_t)i * K + k);
+                    c = __ldg(oc + (int64_t)i * K + k);
+                    bad |= (c < 0) || (c >= (1 << 30)) || (g > (1 << 24)) || (g < -(1 << 24));
+                }
                 const int32_t a = g < 0 ? -g : g;
                 m = a > m ? a : m;
-                bad |= (c < 0) || (c >= (1 << 30)) || (g > (1 << 24)) || (g < -(1 << 24));
                 if (k == 0) {
                     g0_sum += g;
                     c0_sum += c;
@@ -166,17 +241,17 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     const int32_t nrows = (B + 32) >> 5;
     const int32_t ntiles = (nrows + RPT - 1) / RPT;
     // S_N = 0 on every cell (including the padding cells above B in the top row)
-    for (int32_t x = warp * 32 + lane; x < nrows * 32; x += nwarps * 32) rowA[x] = 0;
+    for (int32_t x = tid; x < nrows * 32; x += nthr) rowA[x] = 0;
     if (nwarps > 1) __syncthreads(); else __syncwarp();
     if (red[0]) {
-        if (warp == 0 && lane == 0) {
+        if (tid == 0) {
             P.best_gain[w] = 0;
             P.best_cost[w] = 0;
             P.feasible[w] = 0;
             atomic_min_i64(&P.status[1], w);
         }
         if (MODE != DP_PLAN)
-            for (int32_t i = warp * 32 + lane; i < N; i += nwarps * 32) P.exit_out[ff + i] = 0;
+            for (int32_t i = tid; i < N; i += nthr) P.exit_out[ff + i] = 0;
         return;
     }
 
@@ -184,58 +259,50 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     const int32_t gtiles = (int32_t)(((Bb + 32) >> 5) + RPT - 1) / RPT;
     uint32_t *__restrict__ gch = reinterpret_cast<uint32_t *>(P.workspace + choff);
 
-    int32_t my_gp = 0, my_c = 0;                          // option `lane` of the current frame
-    if (N > 0 && lane < K) {
+    int32_t my_gp = 0, my_c = 0;                          // !OSM: option `lane` of the current frame
+    if (!OSM && N > 0 && lane < K) {
         my_gp = (__ldg(og + (int64_t)(N - 1) * K + lane) << 4) | (15 - lane);
         my_c = __ldg(oc + (int64_t)(N - 1) * K + lane);
     }
     int32_t *__restrict__ cur = rowA;
     int32_t *__restrict__ nxt = inplace ? rowA : rowB;
+    int32_t own[RPT];                                      // S_{i+1} of the warp's first tile
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) own[r] = 0;
+    // in place: top-down so a tile's reads never see the updated tiles above it
+    const int32_t t0 = inplace ? ntiles - 1 : warp;
+    const int32_t dt = inplace ? -1 : nwarps;
 
     for (int32_t i = N - 1; i >= 0; --i) {
         int32_t gp[K], cc[K];
+        if (OSM) {
 #pragma unroll
-        for (int k = 0; k < K; ++k) {
-            gp[k] = __shfl_sync(0xffffffffu, my_gp, k);
-            cc[k] = __shfl_sync(0xffffffffu, my_c, k);
-        }
-        if (MODE != DP_PLAN && warp == 0 && lane < K) cst[i * K + lane] = my_c;
-        if (i > 0 && lane < K) {                          // prefetch frame i-1
-            my_gp = (__ldg(og + (int64_t)(i - 1) * K + lane) << 4) | (15 - lane);
-            my_c = __ldg(oc + (int64_t)(i - 1) * K + lane);
+            for (int k = 0; k < K; ++k) {
+                const int2 v = opt_s[i * K + k];
+                gp[k] = v.x;
+                cc[k] = v.y;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                gp[k] = __shfl_sync(0xffffffffu, my_gp, k);
+                cc[k] = __shfl_sync(0xffffffffu, my_c, k);
+            }
+            if (MODE != DP_PLAN && warp == 0 && lane < K) cst[i * K + lane] = my_c;
+            if (i > 0 && lane < K) {                      // prefetch frame i-1
+                my_gp = (__ldg(og + (int64_t)(i - 1) * K + lane) << 4) | (15 - lane);
+                my_c = __ldg(oc + (int64_t)(i - 1) * K + lane);
+            }
         }
         int32_t cmax = cc[0];
 #pragma unroll
         for (int k = 1; k < K; ++k) cmax = max(cmax, cc[k]);
-        const int32_t *__restrict__ cur_lane = cur + lane;
-        // in place: top-down so a tile's reads never see the updated tiles above it
-        const int32_t t0 = inplace ? ntiles - 1 : warp;
-        const int32_t dt = inplace ? -1 : nwarps;
-        for (int32_t t = t0; t >= 0 && t < ntiles; t += dt) {
-            const int32_t b_lo = t * RPT * 32;
-            const int32_t nr = min(RPT, nrows - t * RPT);
-            int32_t key[RPT];
-            const bool fast = (nr == RPT) && (cmax <= b_lo + P.pad_words);
-            if (fast)
-                tile_keys_fast<K, RPT>(cur_lane, b_lo, gp, cc, key);
-            else
-                tile_keys<K, RPT>(cur, b_lo, nr, P.pad_words, gp, cc, lane, key);
-            if (inplace) __syncwarp();                    // all reads of this tile done
-            int32_t *__restrict__ dst = nxt + b_lo + lane;
-            if (fast) {
-#pragma unroll
-                for (int r = 0; r < RPT; ++r) dst[r * 32] = key[r] & ~15;
-            } else {
-#pragma unroll
-                for (int r = 0; r < RPT; ++r)
-                    if (r < nr) dst[r * 32] = key[r] & ~15;
-            }
-            const uint32_t word = pack_choices<RPT, CB>(key);
-            if (MODE == DP_SOLVE_SMEM)
-                sch[(i * ntiles + t) * 32 + lane] = word;
-            else
-                gch[((int64_t)i * gtiles + t) * 32 + lane] = word;
-        }
+        if (t0 < ntiles)
+            dp_tile<K, MODE, true>(P, t0, i, nrows, ntiles, gtiles, cur, nxt, sch, gch, gp, cc, cmax, inplace, lane,
+                                   own);
+        for (int32_t t = t0 + dt; t >= 0 && t < ntiles; t += dt)
+            dp_tile<K, MODE, false>(P, t, i, nrows, ntiles, gtiles, cur, nxt, sch, gch, gp, cc, cmax, inplace, lane,
+                                    own);
         if (nwarps > 1) __syncthreads(); else __syncwarp();   // frame i visible to frame i-1
         int32_t *tmp = cur;
         cur = nxt;
@@ -247,7 +314,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     const int32_t RB = cur[B];
     const bool feas = RB > VALID_MIN_R;
     int32_t cnt = 0;
-    for (int32_t b = warp * 32 + lane; b <= B; b += nwarps * 32) cnt += cur[b] < RB ? 1 : 0;
+    for (int32_t b = tid; b <= B; b += nthr) cnt += cur[b] < RB ? 1 : 0;
     cnt = __reduce_add_sync(0xffffffffu, cnt);
     if (nwarps > 1) {
         if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(&red[3]), (unsigned long long)cnt);
@@ -256,7 +323,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     }
     const int32_t G = feas ? (RB >> 4) : (int32_t)red[1];
     const int32_t Cst = feas ? cnt : (int32_t)red[2];
-    if (warp == 0 && lane == 0) {
+    if (tid == 0) {
         P.best_gain[w] = G;
         P.best_cost[w] = Cst;
         P.feasible[w] = feas ? 1 : 0;
@@ -265,10 +332,10 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
 
     // ---- a5 fused: forward backtrack from (frame 0, b = C*)
     if (!feas) {
-        for (int32_t i = warp * 32 + lane; i < N; i += nwarps * 32) P.exit_out[ff + i] = 0;
+        for (int32_t i = tid; i < N; i += nthr) P.exit_out[ff + i] = 0;
         return;
     }
-    if (warp == 0 && lane == 0) {
+    if (tid == 0) {
         int32_t b = Cst;
         for (int32_t i = 0; i < N; ++i) {
             const int32_t t = b / (32 * RPT);
@@ -280,14 +347,15 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
                 word = gch[((int64_t)i * gtiles + t) * 32 + (b & 31)];
             const int32_t k = (int32_t)((word >> choice_shift(j, CB)) & CMASK);
             P.exit_out[ff + i] = (uint8_t)k;
-            b -= cst[i * K + k];
+            b -= OSM ? opt_s[i * K + k].y : cst[i * K + k];
         }
     }
 }
 
-// smem layout per CTA: [red: 8 x int64][pad][rowA][pad][rowB (G > 1)][choice planes (solve)][costs]
-// The pads (pad_words of -inf below each row buffer) are written once and never overwritten.
-template <int KSEL, int MODE>
+// smem layout per CTA: [red: 8 x int64][pad][rowA][pad][rowB (G > 1)][options (OSM) | costs]
+// [choice planes (solve smem)]. The pads (pad_words of -inf below each row buffer) are written
+// once and never overwritten.
+template <int KSEL, int MODE, bool OSM>
 __global__ void __launch_bounds__(256, 4) dp_cta_kernel(DpParams P)
 {
     extern __shared__ int4 smem_raw[];
@@ -299,9 +367,10 @@ __global__ void __launch_bounds__(256, 4) dp_cta_kernel(DpParams P)
     const int32_t stride = P.pad_words + P.row_words;
     int32_t *rowA = base + P.pad_words;
     int32_t *rowB = rowA + stride;
-    int32_t *after = base + (nwarps > 1 ? 2 : 1) * stride;
-    uint32_t *sch = reinterpret_cast<uint32_t *>(after);
-    int32_t *cst = after + P.chs_words;
+    int32_t *after = base + (nwarps > 1 ? 2 : 1) * stride;   // 16-B aligned (row_words % 32 == 0)
+    int2 *opt_s = reinterpret_cast<int2 *>(after);
+    int32_t *cst = after;                                      // !OSM: costs for the backtrack
+    uint32_t *sch = reinterpret_cast<uint32_t *>(after + P.cst_words);
     for (int32_t x = threadIdx.x; x < P.pad_words; x += blockDim.x) {
         rowA[x - P.pad_words] = NEG_R;
         if (nwarps > 1) rowB[x - P.pad_words] = NEG_R;
@@ -309,11 +378,11 @@ __global__ void __launch_bounds__(256, 4) dp_cta_kernel(DpParams P)
     __syncthreads();
     for (int64_t w = blockIdx.x; w < P.num_windows; w += gridDim.x) {
         if (KSEL != 0) {
-            dp_window<(KSEL > 0 ? KSEL : 2), MODE>(P, w, rowA, rowB, sch, cst, red, warp, nwarps, lane);
+            dp_window<(KSEL > 0 ? KSEL : 2), MODE, OSM>(P, w, rowA, rowB, sch, cst, opt_s, red, warp, nwarps, lane);
         } else {
             switch (P.windows[w].num_exits) {
 #define TURBO_K_CASE(KK) \
-    case KK: dp_window<KK, MODE>(P, w, rowA, rowB, sch, cst, red, warp, nwarps, lane); break;
+    case KK: dp_window<KK, MODE, OSM>(P, w, rowA, rowB, sch, cst, opt_s, red, warp, nwarps, lane); break;
                 TURBO_K_CASE(2) TURBO_K_CASE(3) TURBO_K_CASE(4) TURBO_K_CASE(5) TURBO_K_CASE(6)
                 TURBO_K_CASE(7) TURBO_K_CASE(8) TURBO_K_CASE(9) TURBO_K_CASE(10) TURBO_K_CASE(11)
                 TURBO_K_CASE(12) TURBO_K_CASE(13) TURBO_K_CASE(14) TURBO_K_CASE(15) TURBO_K_CASE(16)
@@ -327,23 +396,23 @@ __global__ void __launch_bounds__(256, 4) dp_cta_kernel(DpParams P)
 
 typedef void (*dp_kernel_t)(DpParams);
 
-template <int MODE>
+template <int MODE, bool OSM>
 dp_kernel_t pick_dp_kernel(int kmin, int kmax)
 {
-    if (kmin != kmax) return dp_cta_kernel<0, MODE>;
+    if (kmin != kmax) return dp_cta_kernel<0, MODE, OSM>;
     switch (kmin) {
 #define TURBO_K_PICK(KK) \
-    case KK: return dp_cta_kernel<KK, MODE>;
+    case KK: return dp_cta_kernel<KK, MODE, OSM>;
         TURBO_K_PICK(2) TURBO_K_PICK(3) TURBO_K_PICK(4) TURBO_K_PICK(5) TURBO_K_PICK(6)
         TURBO_K_PICK(7) TURBO_K_PICK(8) TURBO_K_PICK(9) TURBO_K_PICK(10) TURBO_K_PICK(11)
         TURBO_K_PICK(12) TURBO_K_PICK(13) TURBO_K_PICK(14) TURBO_K_PICK(15) TURBO_K_PICK(16)
 #undef TURBO_K_PICK
-        default: return dp_cta_kernel<0, MODE>;
+        default: return dp_cta_kernel<0, MODE, OSM>;
     }
 }
 
-dp_kernel_t dp_kernel_plan(int kmin, int kmax);
-dp_kernel_t dp_kernel_solve_smem(int kmin, int kmax);
-dp_kernel_t dp_kernel_solve_global(int kmin, int kmax);
+dp_kernel_t dp_kernel_plan(int kmin, int kmax, bool osm);
+dp_kernel_t dp_kernel_solve_smem(int kmin, int kmax, bool osm);
+dp_kernel_t dp_kernel_solve_global(int kmin, int kmax, bool osm);
 
 }  // namespace turbo

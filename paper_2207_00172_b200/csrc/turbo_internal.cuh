@@ -59,9 +59,10 @@ struct DpParams {
     int32_t num_windows;
     int32_t row_words;      // per-warp row capacity (multiple of 32)
     int32_t chs_words;      // per-warp smem choice capacity (DP_SOLVE_SMEM)
-    int32_t cst_words;      // per-warp smem cost table capacity (solve modes)
+    int32_t cst_words;      // smem words after the rows: option table (osm) or costs (solve)
     int32_t warp_words;     // unused (0)
     int32_t pad_words;      // -inf words below each row buffer (unchecked shifts up to this)
+    int32_t osm;            // 1: options staged in smem (cst_words = 2 * frames * exits)
     int32_t warps_per_cta;
     const int32_t *opt_gain;
     const int32_t *opt_cost;

@@ -13,7 +13,7 @@ def gpu_run(wl, fused=True, variant=0, with_stats=True):
     from paper_2207_00172_b200 import turbo
     turbo.debug_set_variant(variant)
     try:
-        b = turbo.batch_from_workload(wl, with_plan_workspace=not fused or variant == 2)
+        b = turbo.batch_from_workload(wl, with_plan_workspace=not fused or (variant & 3) == 2)
         turbo.run_path(b, fused=fused, with_stats=with_stats)
         torch.cuda.synchronize()
         out = turbo.results(b)

@@ -114,7 +114,7 @@ def test_device_calls_reject_null_shape(tb):
     assert lib.turbo_mckp_plan(None, None, None, None, None, 0, None, None, None, None, None) == 1
     assert lib.turbo_backtrack(None, None, None, None, 0, None, None, None, None) == 1
     assert lib.turbo_stats(None, None, None, None, None, None, None, None, None) == 1
-    assert lib.turbo_debug_set_variant(7) == 1
+    assert lib.turbo_debug_set_variant(7) == 1 and lib.turbo_debug_set_variant(3) == 1
 
 
 def test_empty_batch_is_noop(tb):

@@ -3,7 +3,8 @@
 Every test here needs a B200 and is marked gpu. Inputs are seeded synthetic workloads
 (synth/); both sides see the same arrays. Kernel variants are forced through the debug
 hook so each variant sees the same windows: 0 = automatic, 1 = fused solve with choice
-planes in shared memory, 2 = fused solve with choice planes in HBM; fused=False runs
+planes in shared memory, 2 = fused solve with choice planes in HBM, +4 = option tables
+broadcast by shuffles instead of staged in shared memory; fused=False runs
 turbo_mckp_plan + turbo_backtrack (choice planes in HBM, separate backtrack kernel).
 """
 import numpy as np
@@ -14,8 +15,8 @@ from tests.parity import compare, gpu_run, oracle_run
 
 pytestmark = pytest.mark.gpu
 
-PATHS = [(True, 0), (True, 1), (True, 2), (False, 0)]
-PATH_IDS = ["solve-auto", "solve-smem", "solve-hbm", "plan+backtrack"]
+PATHS = [(True, 0), (True, 1), (True, 2), (False, 0), (True, 5), (True, 6), (False, 4)]
+PATH_IDS = ["solve-auto", "solve-smem", "solve-hbm", "plan+backtrack", "solve-smem-shfl", "solve-hbm-shfl", "plan-shfl"]
 
 
 @pytest.fixture(scope="module", autouse=True)
