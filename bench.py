@@ -357,7 +357,7 @@ def run_turbo(args):
         "dp_cell_updates_per_s": total_cells / t_dp,
         "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
                      "frac": achieved / smem_peak, "traffic": traffic,
-                     "kernel": "turbo::dp_warp_kernel (turbo_mckp_solve)",
+                     "kernel": "turbo::dp_cta_kernel (turbo_mckp_solve)",
                      "note": "algorithmic smem bytes = cells x (4K+4) per launch (SURVEY.md 8(d)); "
                              "peak = SMs x 128 B/clk x sm_max_mhz (MEASURED_PEAKS.json), derived"},
         "e2e": {"value": total_cells / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
