@@ -5,8 +5,8 @@
     torchrun --nproc-per-node N ... bench.py --gpus N      (N > 1, NCCL allreduce of the stats)
 
 A step is one pass of the whole path over the rank's windows:
-turbo_profile_lookup (a1+a2) -> turbo_mckp_solve (a3+a4+a5, fused) -> turbo_stats (a6)
-[-> allreduce of the int64[181] stats over NCCL when N > 1]. Inputs are generated on the
+turbo_schedule (a1..a6 in one launch; --path solve: turbo_profile_lookup -> turbo_mckp_solve ->
+turbo_stats) [-> allreduce of the int64[181] stats over NCCL when N > 1]. Inputs are generated on the
 host from the seeded generator (synth/) and copied to HBM before timing. Weak scaling: each
 rank plans its own windows (window ids offset by rank), per-GPU work fixed.
 The metric is BASELINE.json's: DP cell-updates/s (sum over windows of N_w (B_w + 1) per
@@ -189,16 +189,31 @@ def run_turbo(args):
 
     name = args.workload
     wl = make_workload(name, rank)
-    b = turbo.batch_from_workload(wl, device=dev, with_plan_workspace=not args.fused)
+    path = args.path
+    b = turbo.batch_from_workload(wl, device=dev, with_plan_workspace=(path == "plan"))
     stream = torch.cuda.current_stream(dev)
-    fused = args.fused
+    fused = path == "solve"
     cells = wl.total_cells
     W = wl.num_windows
+
+    def dominant():
+        if path == "schedule":       # a1..a6 in one launch
+            turbo.schedule(b.shape, b.profiles_dev, b.windows_dev, b.class_id, b.capacity, b.base_cost, b.solve_ws,
+                           b.best_gain, b.best_cost, b.feasible, b.exit_out, b.stats, b.status)
+        elif path == "solve":
+            turbo.mckp_solve(b.shape, b.windows_dev, b.opt_gain, b.opt_cost, b.solve_ws, b.best_gain,
+                             b.best_cost, b.feasible, b.exit_out, b.status)
+        else:
+            turbo.mckp_plan(b.shape, b.windows_dev, b.opt_gain, b.opt_cost, b.workspace, b.best_gain,
+                            b.best_cost, b.feasible, b.status)
 
     def step():
         stream = torch.cuda.current_stream(dev)
         b.status.fill_(-1)
         b.stats.zero_()
+        if path == "schedule":
+            dominant()
+            return
         turbo.profile_lookup(b.shape, b.profiles_dev, b.windows_dev, b.class_id, b.capacity, b.base_cost,
                              b.opt_gain, b.opt_cost, b.status, stream)
         if fused:
@@ -212,7 +227,7 @@ def run_turbo(args):
                             stream)
         turbo.stats(b.shape, b.windows_dev, b.class_id, b.exit_out, b.best_gain, b.best_cost, b.feasible, b.stats,
                     stream)
-    launches_per_step = 3 if fused else 4
+    launches_per_step = {"schedule": 1, "solve": 3, "plan": 4}[path]
 
     # L2 flush buffer (> 126 MB L2) written between timed steps (outside the timed events)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -230,12 +245,7 @@ def run_turbo(args):
         step()
     g_dp = torch.cuda.CUDAGraph()                        # the dominant kernel alone
     with torch.cuda.graph(g_dp):
-        if fused:
-            turbo.mckp_solve(b.shape, b.windows_dev, b.opt_gain, b.opt_cost, b.solve_ws, b.best_gain,
-                             b.best_cost, b.feasible, b.exit_out, b.status)
-        else:
-            turbo.mckp_plan(b.shape, b.windows_dev, b.opt_gain, b.opt_cost, b.workspace, b.best_gain,
-                            b.best_cost, b.feasible, b.status)
+        dominant()
     stream = torch.cuda.current_stream(dev)
     for _ in range(3):
         g_step.replay()
@@ -349,7 +359,8 @@ def run_turbo(args):
         "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "int32", "data": "synthetic (seeded splitmix64 generator, synth/; paper-calibrated profiles)",
         "config": {"workload": f"{name}: {WORKLOADS[name]['desc']}", "windows_per_gpu": W,
-                   "cells_per_gpu_step": cells, "path": "solve (fused a3-a5)" if fused else "plan+backtrack",
+                   "cells_per_gpu_step": cells, "path": {"schedule": "turbo_schedule (a1-a6 in one launch)", "solve": "lookup + solve (a3-a5 fused) + stats",
+                            "plan": "lookup + plan + backtrack + stats"}[path],
                    "l2": "flushed between timed steps (256 MiB write outside the step events)",
                    "parallelism": f"weak dp{N} (windows sharded, NCCL allreduce of stats)"},
         "windows_per_s": W * N / t_step,
@@ -357,7 +368,8 @@ def run_turbo(args):
         "dp_cell_updates_per_s": total_cells / t_dp,
         "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
                      "frac": achieved / smem_peak, "traffic": traffic,
-                     "kernel": "turbo::dp_cta_kernel (turbo_mckp_solve)",
+                     "kernel": "turbo::dp_cta_kernel (" + {"schedule": "turbo_schedule", "solve": "turbo_mckp_solve",
+                                                           "plan": "turbo_mckp_plan"}[path] + ")",
                      "note": "algorithmic smem bytes = cells x (4K+4) per launch (SURVEY.md 8(d)); "
                              "peak = SMs x 128 B/clk x sm_max_mhz (MEASURED_PEAKS.json), derived"},
         "e2e": {"value": total_cells / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -386,7 +398,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["turbo", "reference"], default="turbo")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
-    ap.add_argument("--unfused", dest="fused", action="store_false")
+    ap.add_argument("--path", choices=["schedule", "solve", "plan"], default="schedule",
+                    help="schedule: one fused a1..a6 launch; solve: lookup, solve, stats; plan: 4 launches")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()

@@ -169,6 +169,22 @@ turbo_status_t turbo_mckp_solve(const turbo_shape_t *shape /* host */, const tur
 turbo_status_t turbo_mckp_solve_workspace(const turbo_shape_t *shape, size_t *bytes /* host, out */);
 
 /* ---------------------------------------------------------------------------
+ * The whole path a1..a6 in ONE launch (one CTA per window): a1 budget from capacity (when
+ * capacity != NULL, written back to windows[w].budget), a2 option rows read straight from
+ * class_id and the profiles into shared memory (no option table in HBM; a class >= C sets
+ * status[0] and gives a zero row, exactly as turbo_profile_lookup), a3..a5 as
+ * turbo_mckp_solve, a6 ACCUMULATED into stats (int64[181], caller zeroes it).
+ * Outputs are bit-identical to lookup -> solve -> stats. Workspace as turbo_mckp_solve
+ * (turbo_mckp_solve_workspace() bytes). Returns TURBO_ERR_UNSUPPORTED when one window's
+ * option table (max_frames x max_exits x 8 B) exceeds 48 KiB; use the separate calls then. */
+turbo_status_t turbo_schedule(const turbo_shape_t *shape /* host */, const turbo_profile_t *profiles,
+                              turbo_window_t *windows, const uint8_t *class_id,
+                              const int32_t *capacity /* nullable */, int32_t base_cost,
+                              void *workspace, size_t workspace_bytes,
+                              int32_t *best_gain, int32_t *best_cost, uint8_t *feasible,
+                              uint8_t *exit_out, int64_t *stats, int64_t *status, turbo_stream_t stream);
+
+/* ---------------------------------------------------------------------------
  * a6 (per GPU): ACCUMULATES the plan statistics into stats (int64[181], layout
  * above; caller zeroes it). The cross-GPU sum (one allreduce over NVLink) is done by
  * the caller's communicator, not inside the library. */

@@ -7,5 +7,5 @@ It never imports oracle/ (the CPU oracle is test infrastructure only).
 from . import turbo  # noqa: F401
 from .turbo import (  # noqa: F401
     TurboError, load, make_batch, batch_from_workload, run_path, results,
-    mckp_workspace, profile_lookup, mckp_plan, backtrack, mckp_solve, mckp_solve_workspace, stats,
+    mckp_workspace, profile_lookup, mckp_plan, backtrack, mckp_solve, mckp_solve_workspace, schedule, stats,
 )

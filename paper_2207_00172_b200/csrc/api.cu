@@ -267,6 +267,49 @@ turbo_status_t turbo_mckp_solve(const turbo_shape_t *shape, const turbo_window_t
                   status, stream);
 }
 
+turbo_status_t turbo_schedule(const turbo_shape_t *shape, const turbo_profile_t *profiles, turbo_window_t *windows,
+                              const uint8_t *class_id, const int32_t *capacity, int32_t base_cost, void *workspace,
+                              size_t workspace_bytes, int32_t *best_gain, int32_t *best_cost, uint8_t *feasible,
+                              uint8_t *exit_out, int64_t *stats, int64_t *status, turbo_stream_t stream)
+{
+    if (!shape) return TURBO_ERR_INVALID_ARG;
+    if (shape->num_windows == 0) return TURBO_OK;
+    if (!profiles || !windows || !best_gain || !best_cost || !feasible || !stats || !status || base_cost < 0)
+        return TURBO_ERR_INVALID_ARG;
+    if (shape->total_frames > 0 && (!class_id || !exit_out)) return TURBO_ERR_INVALID_ARG;
+    const int mode = solve_mode(shape);
+    if (mode == DP_SOLVE_GLOBAL &&
+        ((int64_t)workspace_bytes < shape->workspace_bytes || (shape->workspace_bytes > 0 && !workspace)))
+        return TURBO_ERR_WORKSPACE;
+    DeviceInfo d;
+    if (device_info(&d) != cudaSuccess) return TURBO_ERR_CUDA;
+    DpParams P;
+    std::memset(&P, 0, sizeof(P));
+    dp_smem_words(shape, mode, &P);
+    if (!P.osm) return TURBO_ERR_UNSUPPORTED;         // option table must be staged in smem
+    P.pad_words = dp_pad_words(shape);
+    if (dp_smem_bytes(P, dp_warps_per_window(shape)) > (size_t)d.smem_per_cta_optin) return TURBO_ERR_UNSUPPORTED;
+    P.windows = windows;
+    P.windows_rw = windows;
+    P.num_windows = shape->num_windows;
+    P.workspace = reinterpret_cast<uint8_t *>(workspace);
+    P.best_gain = best_gain;
+    P.best_cost = best_cost;
+    P.feasible = feasible;
+    P.exit_out = exit_out;
+    P.status = status;
+    P.profiles = profiles;
+    P.class_id = class_id;
+    P.capacity = capacity;
+    P.base_cost = base_cost;
+    P.fuse = 1;
+    P.stats = stats;
+    DpLaunch info;
+    cudaError_t e = launch_dp(shape, mode, P, d.num_sms, d.smem_per_sm, d.smem_per_cta_optin, (cudaStream_t)stream,
+                              &info);
+    return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
+}
+
 turbo_status_t turbo_stats(const turbo_shape_t *shape, const turbo_window_t *windows, const uint8_t *class_id,
                            const uint8_t *exit_out, const int32_t *best_gain, const int32_t *best_cost,
                            const uint8_t *feasible, int64_t *stats, turbo_stream_t stream)

@@ -162,11 +162,34 @@ __device__ __forceinline__ void dp_tile(const DpParams &P, int32_t t, int32_t i,
 // OSM: the window's options staged in shared memory as packed (g << 4 | 15 - k, c) pairs and read
 // with broadcast LDS.64; otherwise lane k holds option k (prefetched a frame ahead) and the warp
 // broadcasts it with shuffles (windows whose option table does not fit).
-template <int K, int MODE, bool OSM>
+// a6 fused: accumulate one window's plan statistics (turbo.h layout) into the per-GPU vector.
+// The CTA-private histogram `hist` (176 u32) was filled by thread 0; every counter goes to
+// global memory with one fire-and-forget reduction (RED) per non-zero entry.
+__device__ __forceinline__ void flush_window_stats(const DpParams &P, uint32_t *__restrict__ hist, int32_t G,
+                                                   int32_t Cst, bool feas, int32_t N, int tid, int nthr)
+{
+    unsigned long long *st = reinterpret_cast<unsigned long long *>(P.stats);
+    for (int x = tid; x < 176; x += nthr) {
+        const uint32_t v = hist[x];
+        if (v) atomicAdd(&st[x], (unsigned long long)v);
+    }
+    if (tid == 0) {
+        atomicAdd(&st[176], (unsigned long long)(long long)G);
+        atomicAdd(&st[177], (unsigned long long)(long long)Cst);
+        atomicAdd(&st[178], 1ull);
+        atomicAdd(&st[179], (unsigned long long)N);
+        if (!feas) atomicAdd(&st[180], 1ull);
+    }
+}
+
+// FUSE (turbo_schedule): a1 (budget from capacity) and a2 (options straight from class ids and
+// the profile, never materialised in HBM) in the prologue, a6 (statistics) in the epilogue.
+template <int K, int MODE, bool OSM, bool FUSE>
 __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t *__restrict__ rowA,
                                           int32_t *__restrict__ rowB, uint32_t *__restrict__ sch,
                                           int32_t *__restrict__ cst, int2 *__restrict__ opt_s,
-                                          int64_t *__restrict__ red, int warp, int nwarps, int lane)
+                                          int64_t *__restrict__ red, uint32_t *__restrict__ hist, int warp,
+                                          int nwarps, int lane)
 {
     constexpr int CB = (K <= 4) ? 2 : 4;          // choice bits
     constexpr int RPT = 32 / CB;                   // rows of 32 cells per tile (per choice word)
@@ -179,23 +202,56 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     const int64_t ff = win->first_frame;
     const int64_t fo = win->first_option;
     const int32_t N = win->num_frames;
-    const int32_t B = win->budget;
+    int32_t B = win->budget;
     const int32_t Bb = win->budget_bound;
     const int64_t choff = win->choice_offset;
 
     const int32_t *__restrict__ og = P.opt_gain + fo;
     const int32_t *__restrict__ oc = P.opt_cost + fo;
 
+    if (FUSE) {
+        // a1 (reading R3): B_w = max(0, capacity_w - m_w * u0)
+        if (P.capacity != nullptr) {
+            const int64_t b = (int64_t)P.capacity[w] - (int64_t)N * (int64_t)P.base_cost;
+            B = (int32_t)(b < 0 ? 0 : (b > 0x7fffffffll ? 0x7fffffff : b));
+            if (tid == 0) P.windows_rw[w].budget = B;
+        }
+        for (int x = tid; x < 176; x += nthr) hist[x] = 0;
+    }
+
     // ---- prologue: stage options (OSM), validate, sums for the infeasible report (reading R8)
     bool bad = (B < 0) || (B > Bb);
     if (OSM) {
         const int32_t n_opt = N * K;
-        for (int32_t o = tid; o < n_opt; o += nthr) {
-            const int32_t g = __ldg(og + o);
-            const int32_t c = __ldg(oc + o);
-            bad |= (c < 0) || (c >= (1 << 30)) || (g > (1 << 24)) || (g < -(1 << 24));
-            const int32_t k = o % K;
-            opt_s[o] = make_int2((g << 4) | (15 - k), c);
+        if (FUSE) {
+            // a2: the option row of frame i is the profile row of its class
+            const turbo_profile_t &pr = P.profiles[win->profile];
+            const int32_t C = pr.num_classes;
+            const int32_t *__restrict__ pg = pr.gain;
+            const int32_t *__restrict__ pc = pr.cost;
+            const uint8_t *__restrict__ cls_w = P.class_id + ff;
+            for (int32_t o = tid; o < n_opt; o += nthr) {
+                const int32_t i = o / K;
+                const int32_t k = o - i * K;
+                const int32_t cls = cls_w[i];
+                int32_t g = 0, c = 0;
+                if (cls < C) {
+                    g = __ldg(pg + cls * K + k);
+                    c = __ldg(pc + cls * K + k);
+                } else if (k == 0) {
+                    atomic_min_i64(&P.status[0], ff + i);
+                }
+                bad |= (c < 0) || (c >= (1 << 30)) || (g > (1 << 24)) || (g < -(1 << 24));
+                opt_s[o] = make_int2((g << 4) | (15 - k), c);
+            }
+        } else {
+            for (int32_t o = tid; o < n_opt; o += nthr) {
+                const int32_t g = __ldg(og + o);
+                const int32_t c = __ldg(oc + o);
+                bad |= (c < 0) || (c >= (1 << 30)) || (g > (1 << 24)) || (g < -(1 << 24));
+                const int32_t k = o % K;
+                opt_s[o] = make_int2((g << 4) | (15 - k), c);
+            }
         }
         if (nwarps > 1)
             bad = __syncthreads_or(bad);
@@ -252,6 +308,16 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
         }
         if (MODE != DP_PLAN)
             for (int32_t i = tid; i < N; i += nthr) P.exit_out[ff + i] = 0;
+        if (FUSE) {
+            if (tid == 0)
+                for (int32_t i = 0; i < N; ++i) {
+                    const uint32_t cls = P.class_id[ff + i];
+                    hist[0] += 1;
+                    if (cls < 10) hist[16 + cls * 16] += 1;
+                }
+            if (nwarps > 1) __syncthreads(); else __syncwarp();
+            flush_window_stats(P, hist, 0, 0, false, N, tid, nthr);
+        }
         return;
     }
 
@@ -331,31 +397,43 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     if (MODE == DP_PLAN) return;
 
     // ---- a5 fused: forward backtrack from (frame 0, b = C*)
-    if (!feas) {
+    if (!feas && !FUSE) {
         for (int32_t i = tid; i < N; i += nthr) P.exit_out[ff + i] = 0;
         return;
     }
     if (tid == 0) {
         int32_t b = Cst;
         for (int32_t i = 0; i < N; ++i) {
-            const int32_t t = b / (32 * RPT);
-            const int32_t j = (b >> 5) & (RPT - 1);
-            uint32_t word;
-            if (MODE == DP_SOLVE_SMEM)
-                word = sch[(i * ntiles + t) * 32 + (b & 31)];
-            else
-                word = gch[((int64_t)i * gtiles + t) * 32 + (b & 31)];
-            const int32_t k = (int32_t)((word >> choice_shift(j, CB)) & CMASK);
+            int32_t k = 0;
+            if (feas) {
+                const int32_t t = b / (32 * RPT);
+                const int32_t j = (b >> 5) & (RPT - 1);
+                uint32_t word;
+                if (MODE == DP_SOLVE_SMEM)
+                    word = sch[(i * ntiles + t) * 32 + (b & 31)];
+                else
+                    word = gch[((int64_t)i * gtiles + t) * 32 + (b & 31)];
+                k = (int32_t)((word >> choice_shift(j, CB)) & CMASK);
+                b -= OSM ? opt_s[i * K + k].y : cst[i * K + k];
+            }
             P.exit_out[ff + i] = (uint8_t)k;
-            b -= OSM ? opt_s[i * K + k].y : cst[i * K + k];
+            if (FUSE) {                                   // a6: CTA-private histograms
+                const uint32_t cls = P.class_id[ff + i];
+                hist[k] += 1;
+                if (cls < 10) hist[16 + cls * 16 + k] += 1;
+            }
         }
+    }
+    if (FUSE) {
+        if (nwarps > 1) __syncthreads(); else __syncwarp();
+        flush_window_stats(P, hist, G, Cst, feas, N, tid, nthr);
     }
 }
 
 // smem layout per CTA: [red: 8 x int64][pad][rowA][pad][rowB (G > 1)][options (OSM) | costs]
 // [choice planes (solve smem)]. The pads (pad_words of -inf below each row buffer) are written
 // once and never overwritten.
-template <int KSEL, int MODE, bool OSM>
+template <int KSEL, int MODE, bool OSM, bool FUSE>
 __global__ void __launch_bounds__(256, 4) dp_cta_kernel(DpParams P)
 {
     extern __shared__ int4 smem_raw[];
@@ -371,6 +449,7 @@ __global__ void __launch_bounds__(256, 4) dp_cta_kernel(DpParams P)
     int2 *opt_s = reinterpret_cast<int2 *>(after);
     int32_t *cst = after;                                      // !OSM: costs for the backtrack
     uint32_t *sch = reinterpret_cast<uint32_t *>(after + P.cst_words);
+    __shared__ uint32_t hist[FUSE ? 176 : 1];
     for (int32_t x = threadIdx.x; x < P.pad_words; x += blockDim.x) {
         rowA[x - P.pad_words] = NEG_R;
         if (nwarps > 1) rowB[x - P.pad_words] = NEG_R;
@@ -378,11 +457,12 @@ __global__ void __launch_bounds__(256, 4) dp_cta_kernel(DpParams P)
     __syncthreads();
     for (int64_t w = blockIdx.x; w < P.num_windows; w += gridDim.x) {
         if (KSEL != 0) {
-            dp_window<(KSEL > 0 ? KSEL : 2), MODE, OSM>(P, w, rowA, rowB, sch, cst, opt_s, red, warp, nwarps, lane);
+            dp_window<(KSEL > 0 ? KSEL : 2), MODE, OSM, FUSE>(P, w, rowA, rowB, sch, cst, opt_s, red, hist, warp, nwarps,
+                                                             lane);
         } else {
             switch (P.windows[w].num_exits) {
 #define TURBO_K_CASE(KK) \
-    case KK: dp_window<KK, MODE, OSM>(P, w, rowA, rowB, sch, cst, opt_s, red, warp, nwarps, lane); break;
+    case KK: dp_window<KK, MODE, OSM, FUSE>(P, w, rowA, rowB, sch, cst, opt_s, red, hist, warp, nwarps, lane); break;
                 TURBO_K_CASE(2) TURBO_K_CASE(3) TURBO_K_CASE(4) TURBO_K_CASE(5) TURBO_K_CASE(6)
                 TURBO_K_CASE(7) TURBO_K_CASE(8) TURBO_K_CASE(9) TURBO_K_CASE(10) TURBO_K_CASE(11)
                 TURBO_K_CASE(12) TURBO_K_CASE(13) TURBO_K_CASE(14) TURBO_K_CASE(15) TURBO_K_CASE(16)
@@ -396,23 +476,24 @@ __global__ void __launch_bounds__(256, 4) dp_cta_kernel(DpParams P)
 
 typedef void (*dp_kernel_t)(DpParams);
 
-template <int MODE, bool OSM>
+template <int MODE, bool OSM, bool FUSE = false>
 dp_kernel_t pick_dp_kernel(int kmin, int kmax)
 {
-    if (kmin != kmax) return dp_cta_kernel<0, MODE, OSM>;
+    if (kmin != kmax) return dp_cta_kernel<0, MODE, OSM, FUSE>;
     switch (kmin) {
 #define TURBO_K_PICK(KK) \
-    case KK: return dp_cta_kernel<KK, MODE, OSM>;
+    case KK: return dp_cta_kernel<KK, MODE, OSM, FUSE>;
         TURBO_K_PICK(2) TURBO_K_PICK(3) TURBO_K_PICK(4) TURBO_K_PICK(5) TURBO_K_PICK(6)
         TURBO_K_PICK(7) TURBO_K_PICK(8) TURBO_K_PICK(9) TURBO_K_PICK(10) TURBO_K_PICK(11)
         TURBO_K_PICK(12) TURBO_K_PICK(13) TURBO_K_PICK(14) TURBO_K_PICK(15) TURBO_K_PICK(16)
 #undef TURBO_K_PICK
-        default: return dp_cta_kernel<0, MODE, OSM>;
+        default: return dp_cta_kernel<0, MODE, OSM, FUSE>;
     }
 }
 
 dp_kernel_t dp_kernel_plan(int kmin, int kmax, bool osm);
 dp_kernel_t dp_kernel_solve_smem(int kmin, int kmax, bool osm);
 dp_kernel_t dp_kernel_solve_global(int kmin, int kmax, bool osm);
+dp_kernel_t dp_kernel_schedule(int kmin, int kmax, int mode);
 
 }  // namespace turbo

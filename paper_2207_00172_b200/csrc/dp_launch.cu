@@ -85,7 +85,8 @@ cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P0, 
     const size_t need = dp_smem_bytes(P, G);
     if (need > (size_t)smem_per_cta_max) return cudaErrorInvalidConfiguration;
     const bool osm = P.osm != 0;
-    dp_kernel_t kern = mode == DP_PLAN         ? dp_kernel_plan(shape->min_exits, shape->max_exits, osm)
+    dp_kernel_t kern = P.fuse                  ? dp_kernel_schedule(shape->min_exits, shape->max_exits, mode)
+                       : mode == DP_PLAN         ? dp_kernel_plan(shape->min_exits, shape->max_exits, osm)
                        : mode == DP_SOLVE_SMEM ? dp_kernel_solve_smem(shape->min_exits, shape->max_exits, osm)
                                                : dp_kernel_solve_global(shape->min_exits, shape->max_exits, osm);
     cudaError_t e = prepare(kern, (size_t)smem_per_cta_max);

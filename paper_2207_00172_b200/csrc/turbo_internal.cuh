@@ -72,6 +72,14 @@ struct DpParams {
     uint8_t *feasible;
     uint8_t *exit_out;
     int64_t *status;
+    // turbo_schedule (fused a1..a6) only
+    const turbo_profile_t *profiles;
+    turbo_window_t *windows_rw;
+    const uint8_t *class_id;
+    const int32_t *capacity;
+    int32_t base_cost;
+    int32_t fuse;
+    int64_t *stats;
 };
 
 struct DpLaunch {

@@ -58,7 +58,7 @@ WINDOW_DTYPE = np.dtype([("first_frame", "<i8"), ("first_option", "<i8"), ("choi
 assert WINDOW_DTYPE.itemsize == 48
 
 EXPORTS = ["turbo_mckp_workspace", "turbo_profile_lookup", "turbo_mckp_plan", "turbo_backtrack",
-           "turbo_mckp_solve", "turbo_mckp_solve_workspace", "turbo_stats", "turbo_debug_set_variant",
+           "turbo_mckp_solve", "turbo_mckp_solve_workspace", "turbo_schedule", "turbo_stats", "turbo_debug_set_variant",
            "turbo_status_string", "turbo_abi_version"]
 
 _lib = None
@@ -81,6 +81,7 @@ def load(path: Optional[str] = None):
     lib.turbo_mckp_solve.argtypes = [vp, vp, vp, vp, vp, sz, vp, vp, vp, vp, vp, vp]
     lib.turbo_mckp_solve_workspace.argtypes = [vp, vp]
     lib.turbo_stats.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    lib.turbo_schedule.argtypes = [vp, vp, vp, vp, vp, i32, vp, sz, vp, vp, vp, vp, vp, vp, vp]
     lib.turbo_debug_set_variant.argtypes = [i32]
     lib.turbo_status_string.restype = ctypes.c_char_p
     lib.turbo_abi_version.restype = i32
@@ -158,6 +159,16 @@ def mckp_solve(shape, windows_dev, opt_gain, opt_cost, workspace, best_gain, bes
            load().turbo_mckp_solve(ctypes.addressof(shape), _ptr(windows_dev), _ptr(opt_gain), _ptr(opt_cost),
                                    _ptr(workspace), nbytes, _ptr(best_gain), _ptr(best_cost), _ptr(feasible),
                                    _ptr(exit_out), _ptr(status), _stream(stream)))
+
+
+def schedule(shape, profiles_dev, windows_dev, class_id, capacity, base_cost, workspace, best_gain, best_cost,
+             feasible, exit_out, stats_out, status, stream=None):
+    nbytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check("turbo_schedule",
+           load().turbo_schedule(ctypes.addressof(shape), _ptr(profiles_dev), _ptr(windows_dev), _ptr(class_id),
+                                 _ptr(capacity), int(base_cost), _ptr(workspace), nbytes, _ptr(best_gain),
+                                 _ptr(best_cost), _ptr(feasible), _ptr(exit_out), _ptr(stats_out), _ptr(status),
+                                 _stream(stream)))
 
 
 def stats(shape, windows_dev, class_id, exit_out, best_gain, best_cost, feasible, stats_out, stream=None):
@@ -257,12 +268,17 @@ def batch_from_workload(wl, device="cuda", with_plan_workspace: bool = True) -> 
                       wl.profile, wl.class_id, wl.capacity, wl.base_cost, device, with_plan_workspace)
 
 
-def run_path(b: Batch, fused: bool = True, stream=None, with_stats: bool = True, reset: bool = True):
-    """One pass of the hot path: a1+a2 lookup -> a3..a5 (solve, or plan + backtrack) -> a6 stats."""
+def run_path(b: Batch, fused=True, stream=None, with_stats: bool = True, reset: bool = True):
+    """One pass of the hot path: a1+a2 lookup -> a3..a5 (solve, or plan + backtrack) -> a6 stats.
+    fused="all" runs the single-launch turbo_schedule (a1..a6) instead."""
     if reset:
         b.status.fill_(-1)
         if with_stats:
             b.stats.zero_()
+    if fused == "all":
+        schedule(b.shape, b.profiles_dev, b.windows_dev, b.class_id, b.capacity, b.base_cost, b.solve_ws,
+                 b.best_gain, b.best_cost, b.feasible, b.exit_out, b.stats, b.status, stream)
+        return
     profile_lookup(b.shape, b.profiles_dev, b.windows_dev, b.class_id, b.capacity, b.base_cost, b.opt_gain,
                    b.opt_cost, b.status, stream)
     if fused:

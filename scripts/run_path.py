@@ -13,7 +13,7 @@ def main():
     ap.add_argument("--workload", default="c2")
     ap.add_argument("--windows", type=int, default=0, help="0 = bench.py's per-GPU share")
     ap.add_argument("--reps", type=int, default=3)
-    ap.add_argument("--unfused", action="store_true")
+    ap.add_argument("--path", choices=["schedule", "solve", "plan"], default="schedule")
     ap.add_argument("--variant", type=int, default=0)
     args = ap.parse_args()
     import torch
@@ -24,9 +24,10 @@ def main():
     n = args.windows or spec["per_gpu"]
     wl = synth.make_config(spec["config"], num_windows=n)
     turbo.debug_set_variant(args.variant)
-    b = turbo.batch_from_workload(wl, with_plan_workspace=args.unfused or args.variant == 2)
+    b = turbo.batch_from_workload(wl, with_plan_workspace=args.path == "plan" or (args.variant & 3) == 2)
+    fused = {"schedule": "all", "solve": True, "plan": False}[args.path]
     for _ in range(args.reps):
-        turbo.run_path(b, fused=not args.unfused)
+        turbo.run_path(b, fused=fused)
     torch.cuda.synchronize()
     st = b.status.cpu().numpy()
     assert st[0] == -1 and st[1] == -1, st

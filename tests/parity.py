@@ -20,6 +20,7 @@ def gpu_run(wl, fused=True, variant=0, with_stats=True):
     finally:
         turbo.debug_set_variant(0)
     out["batch"] = b
+    out["path"] = fused
     return out
 
 
