@@ -83,13 +83,31 @@ cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P0, 
     const int G = dp_warps_per_window(shape);
     P.warps_per_cta = G;
     const size_t need = dp_smem_bytes(P, G);
-    if (need > (size_t)smem_per_cta_max) return cudaErrorInvalidConfiguration;
+
     const bool osm = P.osm != 0;
     dp_kernel_t kern = P.fuse                  ? dp_kernel_schedule(shape->min_exits, shape->max_exits, mode)
                        : mode == DP_PLAN         ? dp_kernel_plan(shape->min_exits, shape->max_exits, osm)
                        : mode == DP_SOLVE_SMEM ? dp_kernel_solve_smem(shape->min_exits, shape->max_exits, osm)
                                                : dp_kernel_solve_global(shape->min_exits, shape->max_exits, osm);
-    cudaError_t e = prepare(kern, (size_t)smem_per_cta_max);
+    // the dynamic-smem ceiling is the per-CTA opt-in maximum minus the kernel's static smem
+    static std::mutex amu;
+    static std::map<const void *, size_t> static_smem;
+    size_t st_bytes = 0;
+    cudaError_t e = cudaSuccess;
+    {
+        std::lock_guard<std::mutex> lk(amu);
+        auto it = static_smem.find((const void *)kern);
+        if (it == static_smem.end()) {
+            cudaFuncAttributes fa;
+            e = cudaFuncGetAttributes(&fa, kern);
+            if (e != cudaSuccess) return e;
+            it = static_smem.emplace((const void *)kern, fa.sharedSizeBytes).first;
+        }
+        st_bytes = it->second;
+    }
+    const size_t dyn_max = (size_t)smem_per_cta_max - st_bytes;
+    if (need > dyn_max) return cudaErrorInvalidConfiguration;
+    e = prepare(kern, dyn_max);
     if (e != cudaSuccess) return e;
     // s_max from the occupancy calculator (it knows the per-CTA reservation and the carveout);
     // results are cached per (device, kernel, G, need, W) -- the queries are host-side only
@@ -117,7 +135,7 @@ cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P0, 
     const int s = cached ? 0 : pick_concurrency(W, num_sms, s_max);
     // pad the dynamic smem so that exactly s CTAs fit per SM (occupancy as a knob)
     if (!cached && s < s_max) {
-        size_t hi = (size_t)smem_per_cta_max, lo = need;     // largest smem with occupancy >= s
+        size_t hi = dyn_max, lo = need;                       // largest smem with occupancy >= s
         while (hi - lo > 16) {
             const size_t mid = ((lo + hi) / 2) & ~(size_t)15;
             int occ = 0;
