@@ -80,7 +80,7 @@ typedef struct {
     int32_t max_budget;          /* max budget_bound                              */
     int32_t min_exits, max_exits;
     int32_t num_classes_max;
-    int32_t reserved0;
+    int32_t max_options;         /* max over windows of m_w K_w (one window's option table)  */
     int64_t total_frames;        /* sum m_w                                       */
     int64_t total_options;       /* sum m_w K_w  (size of opt_gain / opt_cost)    */
     int64_t total_cells;         /* sum m_w (budget_bound_w + 1)                  */

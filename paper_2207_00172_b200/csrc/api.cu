@@ -50,9 +50,10 @@ static void dp_smem_words(const turbo_shape_t *s, int mode, DpParams *P)
     const int64_t tiles = (rows + rpt_min - 1) / rpt_min;
     const int64_t chs = mode == DP_SOLVE_SMEM ? (int64_t)s->max_frames * tiles * 32 : 0;
     P->chs_words = (int32_t)(chs > INT32_MAX ? INT32_MAX : chs);
-    const int64_t opts = (int64_t)s->max_frames * s->max_exits;
+    const int64_t opts = s->max_options;
     P->osm = (opts * 8 <= OSM_LIMIT_BYTES && !(g_variant & 4)) ? 1 : 0;
-    P->cst_words = P->osm ? (int32_t)(2 * opts) : (mode == DP_PLAN ? 0 : (int32_t)opts);
+    P->cst_words = P->osm ? (int32_t)(2 * opts) : (mode == DP_PLAN ? 0 : (int32_t)((int64_t)s->max_frames * s->max_exits));
+    P->max_options = (int32_t)opts;
 }
 
 // -inf pad below each row: shifts up to this many cells need no bounds check (one 4-bit tile;
@@ -127,6 +128,7 @@ turbo_status_t turbo_mckp_workspace(const turbo_profile_t *profiles_host, int32_
         frames = frames > win.first_frame + win.num_frames ? frames : win.first_frame + win.num_frames;
         cells += (int64_t)win.num_frames * ((int64_t)win.budget + 1);
         if (win.num_frames > s.max_frames) s.max_frames = win.num_frames;
+        if ((int64_t)win.num_frames * K > s.max_options) s.max_options = win.num_frames * K;
         if (win.budget > s.max_budget) s.max_budget = win.budget;
         if (K < s.min_exits) s.min_exits = K;
         if (K > s.max_exits) s.max_exits = K;
@@ -287,6 +289,9 @@ turbo_status_t turbo_schedule(const turbo_shape_t *shape, const turbo_profile_t 
     std::memset(&P, 0, sizeof(P));
     dp_smem_words(shape, mode, &P);
     if (!P.osm) return TURBO_ERR_UNSUPPORTED;         // option table must be staged in smem
+    // fused scratch after the option table: the profile (C*K int2) and the class ids (N bytes)
+    P.prof_entries = shape->num_classes_max * shape->max_exits;
+    P.cst_words += 2 * P.prof_entries + (shape->max_frames + 3) / 4;
     P.pad_words = dp_pad_words(shape);
     if (dp_smem_bytes(P, dp_warps_per_window(shape)) > (size_t)d.smem_per_cta_optin) return TURBO_ERR_UNSUPPORTED;
     P.windows = windows;

@@ -224,20 +224,27 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     if (OSM) {
         const int32_t n_opt = N * K;
         if (FUSE) {
-            // a2: the option row of frame i is the profile row of its class
+            // a2: the option row of frame i is the profile row of its
+            // class. Class ids and the profile table are loaded concurrently into shared memory
+            // (one global latency), then every option is a shared-memory gather.
             const turbo_profile_t &pr = P.profiles[win->profile];
             const int32_t C = pr.num_classes;
             const int32_t *__restrict__ pg = pr.gain;
             const int32_t *__restrict__ pc = pr.cost;
-            const uint8_t *__restrict__ cls_w = P.class_id + ff;
+            int2 *__restrict__ prof_s = opt_s + P.max_options;
+            uint8_t *__restrict__ cls_s = reinterpret_cast<uint8_t *>(prof_s + P.prof_entries);
+            for (int32_t x = tid; x < N; x += nthr) cls_s[x] = P.class_id[ff + x];
+            for (int32_t x = tid; x < C * K; x += nthr) prof_s[x] = make_int2(__ldg(pg + x), __ldg(pc + x));
+            if (nwarps > 1) __syncthreads(); else __syncwarp();
             for (int32_t o = tid; o < n_opt; o += nthr) {
                 const int32_t i = o / K;
                 const int32_t k = o - i * K;
-                const int32_t cls = cls_w[i];
+                const int32_t cls = cls_s[i];
                 int32_t g = 0, c = 0;
                 if (cls < C) {
-                    g = __ldg(pg + cls * K + k);
-                    c = __ldg(pc + cls * K + k);
+                    const int2 v = prof_s[cls * K + k];
+                    g = v.x;
+                    c = v.y;
                 } else if (k == 0) {
                     atomic_min_i64(&P.status[0], ff + i);
                 }
@@ -311,7 +318,8 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
         if (FUSE) {
             if (tid == 0)
                 for (int32_t i = 0; i < N; ++i) {
-                    const uint32_t cls = P.class_id[ff + i];
+                    const uint32_t cls =
+                        reinterpret_cast<const uint8_t *>(opt_s + P.max_options + P.prof_entries)[i];
                     hist[0] += 1;
                     if (cls < 10) hist[16 + cls * 16] += 1;
                 }
@@ -418,7 +426,8 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
             }
             P.exit_out[ff + i] = (uint8_t)k;
             if (FUSE) {                                   // a6: CTA-private histograms
-                const uint32_t cls = P.class_id[ff + i];
+                const uint32_t cls =
+                    reinterpret_cast<const uint8_t *>(opt_s + P.max_options + P.prof_entries)[i];
                 hist[k] += 1;
                 if (cls < 10) hist[16 + cls * 16 + k] += 1;
             }

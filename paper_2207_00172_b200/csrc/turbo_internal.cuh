@@ -79,6 +79,8 @@ struct DpParams {
     const int32_t *capacity;
     int32_t base_cost;
     int32_t fuse;
+    int32_t max_options;    // option-table entries per window (osm); fused scratch follows it
+    int32_t prof_entries;   // fused: staged profile entries (max C*K)
     int64_t *stats;
 };
 

@@ -45,7 +45,7 @@ class Shape(ctypes.Structure):
     _fields_ = [("num_windows", ctypes.c_int32), ("num_profiles", ctypes.c_int32),
                 ("max_frames", ctypes.c_int32), ("max_budget", ctypes.c_int32),
                 ("min_exits", ctypes.c_int32), ("max_exits", ctypes.c_int32),
-                ("num_classes_max", ctypes.c_int32), ("reserved0", ctypes.c_int32),
+                ("num_classes_max", ctypes.c_int32), ("max_options", ctypes.c_int32),
                 ("total_frames", ctypes.c_int64), ("total_options", ctypes.c_int64),
                 ("total_cells", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
                 ("reserved1", ctypes.c_int64 * 4)]
