@@ -291,7 +291,7 @@ turbo_status_t turbo_schedule(const turbo_shape_t *shape, const turbo_profile_t 
     if (!P.osm) return TURBO_ERR_UNSUPPORTED;         // option table must be staged in smem
     // fused scratch after the option table: the profile (C*K int2) and the class ids (N bytes)
     P.prof_entries = shape->num_classes_max * shape->max_exits;
-    P.cst_words += 2 * P.prof_entries + (shape->max_frames + 3) / 4;
+    P.cst_words += 2 * P.prof_entries + 2 * ((shape->max_frames + 3) / 4);   // + class ids + exits
     P.pad_words = dp_pad_words(shape);
     if (dp_smem_bytes(P, dp_warps_per_window(shape)) > (size_t)d.smem_per_cta_optin) return TURBO_ERR_UNSUPPORTED;
     P.windows = windows;

@@ -162,6 +162,79 @@ __device__ __forceinline__ void dp_tile(const DpParams &P, int32_t t, int32_t i,
 // OSM: the window's options staged in shared memory as packed (g << 4 | 15 - k, c) pairs and read
 // with broadcast LDS.64; otherwise lane k holds option k (prefetched a frame ahead) and the warp
 // broadcasts it with shuffles (windows whose option table does not fit).
+// a5 inside the DP kernel: warp 0 walks the choice planes from (frame 0, b = C*) and resolves
+// D frames per dependent round trip. Costs do not depend on b, so while lane 0 reads frame i's
+// choice at b, lane 1 + a reads frame i+1's at b - c_{i,a} and (D = 3, when 1 + K + K^2 <= 32)
+// lane 1 + K + a K + a' reads frame i+2's at b - c_{i,a} - c_{i+1,a'}; shuffles then pick the
+// realised branch. Lane 0 writes the exits (global, and shared when exit_s != nullptr).
+template <int K, int MODE, bool OSM>
+__device__ __forceinline__ void backtrack_warp(int32_t N, int32_t b, const uint32_t *__restrict__ sch,
+                                               const uint32_t *__restrict__ gch, int32_t ntiles, int32_t gtiles,
+                                               const int2 *__restrict__ opt_s, const int32_t *__restrict__ cst,
+                                               uint8_t *__restrict__ exit_g, uint8_t *__restrict__ exit_s, int lane)
+{
+    constexpr int CB = (K <= 4) ? 2 : 4;
+    constexpr int RPT = 32 / CB;
+    constexpr uint32_t CMASK = (1u << CB) - 1u;
+    constexpr int D = (1 + K + K * K <= 32) ? 3 : 2;
+    int depth = -1, a = 0, a2 = 0;
+    if (lane == 0) {
+        depth = 0;
+    } else if (lane <= K) {
+        depth = 1;
+        a = lane - 1;
+    } else if (D == 3 && lane <= K + K * K) {
+        depth = 2;
+        a = (lane - 1 - K) / K;
+        a2 = (lane - 1 - K) % K;
+    }
+    auto cost = [&](int32_t i, int32_t k) -> int32_t { return OSM ? opt_s[i * K + k].y : cst[i * K + k]; };
+    auto choice = [&](int32_t i, int32_t cell) -> int32_t {
+        const int32_t t = cell / (32 * RPT);
+        const int32_t j = (cell >> 5) & (RPT - 1);
+        const uint32_t word = (MODE == DP_SOLVE_SMEM) ? sch[(i * ntiles + t) * 32 + (cell & 31)]
+                                                      : gch[((int64_t)i * gtiles + t) * 32 + (cell & 31)];
+        return (int32_t)((word >> choice_shift(j, CB)) & CMASK);
+    };
+    for (int32_t i = 0; i < N; i += D) {
+        const int32_t ca = (depth >= 1 && i + 1 < N) ? cost(i, a) : 0;
+        const int32_t cb = (depth == 2 && i + 2 < N) ? cost(i + 1, a2) : 0;
+        const int32_t cl = (lane < K && i + D - 1 < N) ? cost(i + D - 1, lane) : 0;   // last frame's costs
+        int32_t kk = 0;
+        if (depth == 0) {
+            kk = choice(i, b);
+        } else if (depth >= 1 && i + depth < N) {
+            const int32_t bt = b - ca - cb;
+            kk = bt >= 0 ? choice(i + depth, bt) : 0;
+        }
+        const int32_t k0 = __shfl_sync(0xffffffffu, kk, 0);
+        const int32_t c0 = __shfl_sync(0xffffffffu, ca, 1 + k0);
+        const int32_t k1 = __shfl_sync(0xffffffffu, kk, 1 + k0);
+        int32_t k2 = 0, step;
+        if (D == 3) {
+            const int32_t l2 = 1 + K + k0 * K + k1;
+            const int32_t c1 = __shfl_sync(0xffffffffu, cb, l2);
+            k2 = __shfl_sync(0xffffffffu, kk, l2);
+            step = c0 + c1 + __shfl_sync(0xffffffffu, cl, k2);
+        } else {
+            step = c0 + __shfl_sync(0xffffffffu, cl, k1);
+        }
+        if (lane == 0) {
+            exit_g[i] = (uint8_t)k0;
+            if (exit_s) exit_s[i] = (uint8_t)k0;
+            if (i + 1 < N) {
+                exit_g[i + 1] = (uint8_t)k1;
+                if (exit_s) exit_s[i + 1] = (uint8_t)k1;
+            }
+            if (D == 3 && i + 2 < N) {
+                exit_g[i + 2] = (uint8_t)k2;
+                if (exit_s) exit_s[i + 2] = (uint8_t)k2;
+            }
+        }
+        b -= step;
+    }
+}
+
 // a6 fused: accumulate one window's plan statistics (turbo.h layout) into the per-GPU vector.
 // The CTA-private histogram `hist` (176 u32) was filled by thread 0; every counter goes to
 // global memory with one fire-and-forget reduction (RED) per non-zero entry.
@@ -405,35 +478,26 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     if (MODE == DP_PLAN) return;
 
     // ---- a5 fused: forward backtrack from (frame 0, b = C*)
-    if (!feas && !FUSE) {
-        for (int32_t i = tid; i < N; i += nthr) P.exit_out[ff + i] = 0;
-        return;
-    }
-    if (tid == 0) {
-        int32_t b = Cst;
-        for (int32_t i = 0; i < N; ++i) {
-            int32_t k = 0;
-            if (feas) {
-                const int32_t t = b / (32 * RPT);
-                const int32_t j = (b >> 5) & (RPT - 1);
-                uint32_t word;
-                if (MODE == DP_SOLVE_SMEM)
-                    word = sch[(i * ntiles + t) * 32 + (b & 31)];
-                else
-                    word = gch[((int64_t)i * gtiles + t) * 32 + (b & 31)];
-                k = (int32_t)((word >> choice_shift(j, CB)) & CMASK);
-                b -= OSM ? opt_s[i * K + k].y : cst[i * K + k];
-            }
-            P.exit_out[ff + i] = (uint8_t)k;
-            if (FUSE) {                                   // a6: CTA-private histograms
-                const uint32_t cls =
-                    reinterpret_cast<const uint8_t *>(opt_s + P.max_options + P.prof_entries)[i];
-                hist[k] += 1;
-                if (cls < 10) hist[16 + cls * 16 + k] += 1;
-            }
+    uint8_t *exit_s = nullptr;
+    if (FUSE)
+        exit_s = reinterpret_cast<uint8_t *>(opt_s + P.max_options + P.prof_entries) + ((N + 3) & ~3);
+    if (!feas) {
+        for (int32_t i = tid; i < N; i += nthr) {
+            P.exit_out[ff + i] = 0;
+            if (FUSE) exit_s[i] = 0;
         }
+    } else if (warp == 0) {
+        backtrack_warp<K, MODE, OSM>(N, Cst, sch, gch, ntiles, gtiles, opt_s, cst, P.exit_out + ff, exit_s, lane);
     }
-    if (FUSE) {
+    if (FUSE) {                                           // a6: CTA-private histograms
+        if (nwarps > 1) __syncthreads(); else __syncwarp();
+        const uint8_t *cls_s = reinterpret_cast<const uint8_t *>(opt_s + P.max_options + P.prof_entries);
+        for (int32_t i = tid; i < N; i += nthr) {
+            const uint32_t k = exit_s[i];
+            const uint32_t cls = cls_s[i];
+            atomicAdd(&hist[k], 1u);
+            if (cls < 10) atomicAdd(&hist[16 + cls * 16 + k], 1u);
+        }
         if (nwarps > 1) __syncthreads(); else __syncwarp();
         flush_window_stats(P, hist, G, Cst, feas, N, tid, nthr);
     }
