@@ -85,8 +85,19 @@ typedef struct {
     int64_t total_options;       /* sum m_w K_w  (size of opt_gain / opt_cost)    */
     int64_t total_cells;         /* sum m_w (budget_bound_w + 1)                  */
     int64_t workspace_bytes;     /* bytes needed by turbo_mckp_plan / backtrack   */
-    int64_t reserved1[4];
+    int32_t max_budget_small;    /* max budget_bound over windows served by one CTA each        */
+    int32_t num_big;             /* windows whose row (budget_bound + 1 > TURBO_BIG_CELLS cells)
+                                    is split over the whole grid (long-window kernel)           */
+    int64_t grid_scratch_offset; /* workspace offset of the long-window kernel's halo ring/flags */
+    int64_t reserved1[2];
 } turbo_shape_t;
+
+/* Rows longer than this many cells (budget_bound + 1) are planned by the long-window kernel:
+ * one cooperative grid of CTAs per window, each CTA owning a contiguous budget segment, with
+ * neighbour halos exchanged through an L2 ring. Costs in such a window
+ * must not exceed TURBO_BIG_MAX_COST cells (else the window is rejected, status[1]). */
+#define TURBO_BIG_CELLS 24576
+#define TURBO_BIG_MAX_COST 4096
 
 /* Number of int64 words of the status vector written by lookup / plan. */
 #define TURBO_STATUS_WORDS 2

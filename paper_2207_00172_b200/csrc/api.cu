@@ -44,7 +44,7 @@ static const int64_t OSM_LIMIT_BYTES = 48 * 1024;   // largest per-window option
 
 static void dp_smem_words(const turbo_shape_t *s, int mode, DpParams *P)
 {
-    const int64_t rows = num_rows(s->max_budget);
+    const int64_t rows = num_rows(s->max_budget_small);
     P->row_words = (int32_t)(rows * 32);
     const int rpt_min = s->max_exits <= 4 ? 16 : 8;
     const int64_t tiles = (rows + rpt_min - 1) / rpt_min;
@@ -60,7 +60,7 @@ static void dp_smem_words(const turbo_shape_t *s, int mode, DpParams *P)
 // capped by the row itself, since a shift above B + 1 is never feasible anyway)
 static int32_t dp_pad_words(const turbo_shape_t *s)
 {
-    const int64_t row = num_rows(s->max_budget) * 32;
+    const int64_t row = num_rows(s->max_budget_small) * 32;
     return (int32_t)(row < 256 ? row : 256);
 }
 
@@ -130,6 +130,10 @@ turbo_status_t turbo_mckp_workspace(const turbo_profile_t *profiles_host, int32_
         if (win.num_frames > s.max_frames) s.max_frames = win.num_frames;
         if ((int64_t)win.num_frames * K > s.max_options) s.max_options = win.num_frames * K;
         if (win.budget > s.max_budget) s.max_budget = win.budget;
+        if ((int64_t)win.budget + 1 > TURBO_BIG_CELLS)
+            s.num_big += 1;
+        else if (win.budget > s.max_budget_small)
+            s.max_budget_small = win.budget;
         if (K < s.min_exits) s.min_exits = K;
         if (K > s.max_exits) s.max_exits = K;
         if (profiles_host[win.profile].num_classes > s.num_classes_max)
@@ -139,6 +143,10 @@ turbo_status_t turbo_mckp_workspace(const turbo_profile_t *profiles_host, int32_
     s.total_frames = frames;
     s.total_options = opt;
     s.total_cells = cells;
+    if (s.num_big > 0) {                 // long-window kernel scratch: flags + halo ring
+        s.grid_scratch_offset = (ws + 255) & ~(int64_t)255;
+        ws = s.grid_scratch_offset + grid_scratch_bytes();
+    }
     s.workspace_bytes = ws;
     *shape = s;
     return TURBO_OK;
@@ -186,9 +194,18 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int mode, const turbo_w
     P.feasible = feasible;
     P.exit_out = exit_out;
     P.status = status;
+    P.grid_scratch_offset = shape->grid_scratch_offset;
     DpLaunch info;
-    cudaError_t e = launch_dp(shape, mode, P, d.num_sms, d.smem_per_sm, d.smem_per_cta_optin,
-                              (cudaStream_t)stream, &info);
+    cudaError_t e = cudaSuccess;
+    if (shape->num_big < shape->num_windows)          // windows served by one CTA each
+        e = launch_dp(shape, mode, P, d.num_sms, d.smem_per_sm, d.smem_per_cta_optin, (cudaStream_t)stream, &info);
+    if (e == cudaSuccess && shape->num_big > 0)        // long windows: the whole grid per window
+        e = launch_dp_grid(shape, mode == DP_PLAN ? DP_PLAN : DP_SOLVE_GLOBAL, P, d.num_sms, d.smem_per_cta_optin,
+                           (cudaStream_t)stream);
+    if (e == cudaErrorInvalidConfiguration || e == cudaErrorCooperativeLaunchTooLarge) {
+        cudaGetLastError();
+        return TURBO_ERR_UNSUPPORTED;
+    }
     return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
 }
 
@@ -247,7 +264,7 @@ static int solve_mode(const turbo_shape_t *shape)
 turbo_status_t turbo_mckp_solve_workspace(const turbo_shape_t *shape, size_t *bytes)
 {
     if (!shape || !bytes) return TURBO_ERR_INVALID_ARG;
-    *bytes = solve_mode(shape) == DP_SOLVE_SMEM ? 0 : (size_t)shape->workspace_bytes;
+    *bytes = (solve_mode(shape) == DP_SOLVE_SMEM && shape->num_big == 0) ? 0 : (size_t)shape->workspace_bytes;
     return TURBO_OK;
 }
 
@@ -262,7 +279,7 @@ turbo_status_t turbo_mckp_solve(const turbo_shape_t *shape, const turbo_window_t
     if (shape->total_frames > 0 && !exit_out) return TURBO_ERR_INVALID_ARG;
     if (shape->total_options > 0 && (!opt_gain || !opt_cost)) return TURBO_ERR_INVALID_ARG;
     const int mode = solve_mode(shape);
-    if (mode == DP_SOLVE_GLOBAL &&
+    if ((mode == DP_SOLVE_GLOBAL || shape->num_big > 0) &&
         ((int64_t)workspace_bytes < shape->workspace_bytes || (shape->workspace_bytes > 0 && !workspace)))
         return TURBO_ERR_WORKSPACE;
     return run_dp(shape, mode, windows, opt_gain, opt_cost, workspace, best_gain, best_cost, feasible, exit_out,

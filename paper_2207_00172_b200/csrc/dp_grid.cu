@@ -1,0 +1,330 @@
+// dp_grid.cu -- K4: the MCKP DP for ONE long window spread over the whole GPU (SURVEY.md §8(a)
+// config c4: 3000 frames, B = 2^20, a 4 MiB budget row that no CTA or cluster can hold).
+//
+// Same recurrence as dp_kernel.cuh (PAPER.md:519-525 with f = sum; readings R1, R7):
+//     S_i[b] = max_{k : c_ik <= b} ( g_ik + S_{i+1}[b - c_ik] ),  frames N-1 .. 0.
+// B200 mapping: a cooperative grid of P CTAs (one per SM); CTA j owns the budget segment
+// [j*seg, (j+1)*seg) in shared memory for the whole window (double-buffered), so the row never
+// leaves the chip. Costs are >= 0, so cell b only reads cells <= b: frame i of segment j needs
+// frame i+1 of its own segment plus a HALO of c_max cells just below it, owned by CTA j-1.
+// After each frame CTA j publishes its top c_max cells into an L2 ring slot (depth D) and
+// release-stores a step counter; CTA j+1 acquire-polls it. Dependencies only run towards larger
+// b, so there is no grid-wide barrier per frame: total time ~ N * t_frame + P * t_publish.
+// The ring is back-pressured by a per-CTA "consumed" counter. Choice planes go to HBM in the
+// standard layout (the backtrack kernels read them unchanged).
+#include <cooperative_groups.h>
+
+#include "dp_kernel.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace turbo {
+
+__device__ __forceinline__ int ld_acquire_gpu(const int *p)
+{
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_gpu(int *p, int v)
+{
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void wait_at_least(const int *p, int target)
+{
+    while (ld_acquire_gpu(p) < target) __nanosleep(32);
+}
+
+__device__ __forceinline__ long long block_sum_ll(long long v, long long *sm, int tid, int nthr)
+{
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if ((tid & 31) == 0) sm[tid >> 5] = v;
+    __syncthreads();
+    long long s = 0;
+    for (int x = 0; x < (nthr >> 5); ++x) s += sm[x];
+    __syncthreads();
+    return s;
+}
+
+struct GridCtx {
+    int *pub;               // [GRID_MAX_CTAS] steps published (monotone across windows)
+    int *con;               // [GRID_MAX_CTAS] steps whose halo was consumed
+    long long *misc;        // [8] per-window reductions (zeroed between windows)
+    int *ring;              // [D][GRID_MAX_CTAS][TURBO_BIG_MAX_COST]
+};
+
+template <int K, int MODE>
+__device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, int32_t *bufA, int32_t *bufB,
+                           long long *red, GridCtx X, int &step_base)
+{
+    constexpr int CB = (K <= 4) ? 2 : 4;
+    constexpr int RPT = 32 / CB;
+    constexpr int H = TURBO_BIG_MAX_COST;          // halo capacity (cells)
+    constexpr int D = GRID_RING_DEPTH;
+    const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
+    const int j = blockIdx.x, NP = gridDim.x;
+
+    const turbo_window_t *win = P.windows + w;
+    const int64_t ff = win->first_frame;
+    const int32_t N = win->num_frames;
+    const int32_t B = win->budget;
+    const int32_t Bb = win->budget_bound;
+    const int32_t *__restrict__ og = P.opt_gain + win->first_option;
+    const int32_t *__restrict__ oc = P.opt_cost + win->first_option;
+    uint32_t *__restrict__ gch = reinterpret_cast<uint32_t *>(P.workspace + win->choice_offset);
+    const int32_t gtiles = (int32_t)(((Bb + 32) >> 5) + RPT - 1) / RPT;
+    const int32_t nrows = (B + 32) >> 5;
+
+    // segment of this CTA (512-cell aligned, at least the halo capacity)
+    int32_t seg = (int32_t)(((int64_t)B + 1 + NP - 1) / NP);
+    seg = (seg + 511) & ~511;
+    if (seg < H) seg = H;
+    const int32_t active = (int32_t)(((int64_t)B + 1 + seg - 1) / seg);
+    const int32_t seg_lo = j * seg;
+    const bool mine = j < active;
+
+    // ---- validation, c_max and the infeasible-report sums over all frames (grid-wide)
+    {
+        long long bad = 0, cmax = 0, g0 = 0, c0 = 0, asum = 0;
+        for (int32_t i = j * nthr + tid; i < N; i += NP * nthr) {
+            int32_t m = 0;
+            for (int k = 0; k < K; ++k) {
+                const int32_t g = __ldg(og + (int64_t)i * K + k);
+                const int32_t c = __ldg(oc + (int64_t)i * K + k);
+                const int32_t a = g < 0 ? -g : g;
+                m = a > m ? a : m;
+                bad |= (c < 0) || (c >= (1 << 30)) || (g > (1 << 24)) || (g < -(1 << 24));
+                cmax = c > cmax ? c : cmax;
+                if (k == 0) {
+                    g0 += g;
+                    c0 += c;
+                }
+            }
+            asum += m;
+        }
+        bad = __syncthreads_or((int)bad);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const long long u = __shfl_xor_sync(0xffffffffu, cmax, o);
+            cmax = u > cmax ? u : cmax;
+        }
+        if (lane == 0 && cmax > 0) atomicMax(reinterpret_cast<unsigned long long *>(&X.misc[1]), (unsigned long long)cmax);
+        g0 = block_sum_ll(g0, red, tid, nthr);
+        c0 = block_sum_ll(c0, red, tid, nthr);
+        asum = block_sum_ll(asum, red, tid, nthr);
+        if (tid == 0) {
+            if (bad) atomicOr(reinterpret_cast<unsigned long long *>(&X.misc[0]), 1ull);
+            atomicAdd(reinterpret_cast<unsigned long long *>(&X.misc[2]), (unsigned long long)g0);
+            atomicAdd(reinterpret_cast<unsigned long long *>(&X.misc[3]), (unsigned long long)c0);
+            atomicAdd(reinterpret_cast<unsigned long long *>(&X.misc[4]), (unsigned long long)asum);
+        }
+    }
+    grid.sync();
+    const long long g0_sum = *((volatile long long *)&X.misc[2]);
+    const long long c0_sum = *((volatile long long *)&X.misc[3]);
+    const int32_t cmax = (int32_t)*((volatile long long *)&X.misc[1]);
+    const bool bad = *((volatile long long *)&X.misc[0]) != 0 || *((volatile long long *)&X.misc[4]) >= GAIN_RANGE_LIMIT ||
+                     c0_sum >= 0x7fffffffll || B < 0 || B > Bb || cmax > H;
+    if (bad) {
+        if (j == 0 && tid == 0) {
+            P.best_gain[w] = 0;
+            P.best_cost[w] = 0;
+            P.feasible[w] = 0;
+            atomic_min_i64(&P.status[1], w);
+        }
+        if (MODE != DP_PLAN)
+            for (int32_t i = j * nthr + tid; i < N; i += NP * nthr) P.exit_out[ff + i] = 0;
+        return;
+    }
+    const int32_t hl = cmax;                        // halo length actually needed (<= H)
+
+    // ---- S_N = 0 on the own segment; halo: -inf below b = 0 (CTA 0), S_N = 0 otherwise
+    if (mine) {
+        for (int32_t x = tid; x < H + seg; x += nthr) {
+            const int32_t v = (x < H && j == 0) ? NEG_R : 0;
+            bufA[x] = v;
+            bufB[x] = (x < H && j == 0) ? NEG_R : 0;
+        }
+    }
+    __syncthreads();
+
+    int32_t my_gp = 0, my_c = 0;
+    if (N > 0 && lane < K) {
+        my_gp = (__ldg(og + (int64_t)(N - 1) * K + lane) << 4) | (15 - lane);
+        my_c = __ldg(oc + (int64_t)(N - 1) * K + lane);
+    }
+    int32_t *cur = bufA, *nxt = bufB;
+    const int32_t t_first = seg_lo / (32 * RPT);
+    const int32_t t_end = min((int32_t)((seg_lo + seg) / (32 * RPT)), (nrows + RPT - 1) / RPT);
+    int key[RPT];
+
+    for (int32_t f = 0; f < N; ++f) {
+        const int32_t i = N - 1 - f;
+        int32_t gp[K], cc[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            gp[k] = __shfl_sync(0xffffffffu, my_gp, k);
+            cc[k] = __shfl_sync(0xffffffffu, my_c, k);
+        }
+        if (i > 0 && lane < K) {
+            my_gp = (__ldg(og + (int64_t)(i - 1) * K + lane) << 4) | (15 - lane);
+            my_c = __ldg(oc + (int64_t)(i - 1) * K + lane);
+        }
+        if (mine) {
+            // halo of S_{i+1} from CTA j-1 (its step f-1); step 0 reads S_N = 0 (already set)
+            if (j > 0 && f > 0 && hl > 0) {
+                if (tid == 0) wait_at_least(&X.pub[j - 1], step_base + f);
+                __syncthreads();
+                const int *src = X.ring + ((int64_t)((step_base + f - 1) % D) * GRID_MAX_CTAS + (j - 1)) * H;
+                for (int32_t x = tid; x < hl; x += nthr) cur[H - hl + x] = __ldcg(src + x);
+                __syncthreads();
+                if (tid == 0) st_release_gpu(&X.con[j], step_base + f);
+            }
+            // own tiles
+            const int32_t *cur_base = cur + H - seg_lo;
+            int32_t *nxt_base = nxt + H - seg_lo;
+            for (int32_t t = t_first + warp; t < t_end; t += nwarps) {
+                const int32_t b_lo = t * RPT * 32;
+                const int32_t nr = min(RPT, nrows - t * RPT);
+                if (nr == RPT)
+                    tile_keys_fast<K, RPT>(cur_base + lane, b_lo, gp, cc, key);
+                else
+                    tile_keys<K, RPT>(cur_base, b_lo, nr, H - seg_lo, gp, cc, lane, key);
+                int32_t *dst = nxt_base + b_lo + lane;
+#pragma unroll
+                for (int r = 0; r < RPT; ++r)
+                    if (r < nr) dst[r * 32] = key[r] & ~15;
+                gch[((int64_t)i * gtiles + t) * 32 + lane] = pack_choices<RPT, CB>(key);
+            }
+            __syncthreads();
+            // publish the top hl cells of S_i for CTA j+1
+            if (j + 1 < active && hl > 0) {
+                const int32_t slot_step = step_base + f;
+                if (f >= D) {
+                    if (tid == 0) wait_at_least(&X.con[j + 1], slot_step - D + 1);
+                    __syncthreads();
+                }
+                int *dst = X.ring + ((int64_t)(slot_step % D) * GRID_MAX_CTAS + j) * H;
+                for (int32_t x = tid; x < hl; x += nthr) __stcg(dst + x, nxt[H + seg - hl + x]);
+                __syncthreads();
+                if (tid == 0) {
+                    __threadfence();
+                    st_release_gpu(&X.pub[j], slot_step + 1);
+                }
+            }
+        }
+        int32_t *tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+    }
+    step_base += N;
+
+    // ---- a4: G* = S_0[B] (owned by the last active CTA), C* = #{b <= B : S_0[b] < G*}
+    if (mine && B >= seg_lo && B < seg_lo + seg && tid == 0)
+        *((volatile long long *)&X.misc[5]) = cur[H + B - seg_lo];
+    grid.sync();
+    const int32_t RB = (int32_t)*((volatile long long *)&X.misc[5]);
+    long long cnt = 0;
+    if (mine)
+        for (int32_t b = seg_lo + tid; b <= B && b < seg_lo + seg; b += nthr) cnt += cur[H + b - seg_lo] < RB ? 1 : 0;
+    cnt = block_sum_ll(cnt, red, tid, nthr);
+    if (tid == 0 && cnt) atomicAdd(reinterpret_cast<unsigned long long *>(&X.misc[6]), (unsigned long long)cnt);
+    grid.sync();
+    const bool feas = RB > VALID_MIN_R;
+    const int32_t G = feas ? (RB >> 4) : (int32_t)g0_sum;
+    const int32_t Cst = feas ? (int32_t)*((volatile long long *)&X.misc[6]) : (int32_t)c0_sum;
+    if (j == 0 && tid == 0) {
+        P.best_gain[w] = G;
+        P.best_cost[w] = Cst;
+        P.feasible[w] = feas ? 1 : 0;
+    }
+    if (MODE == DP_PLAN) return;
+    // ---- a5 (solve): CTA 0's warp 0 walks the HBM choice planes
+    if (!feas) {
+        for (int32_t i = j * nthr + tid; i < N; i += NP * nthr) P.exit_out[ff + i] = 0;
+    } else if (j == 0 && warp == 0) {
+        backtrack_warp<K, DP_SOLVE_GLOBAL, false>(N, Cst, nullptr, gch, 0, gtiles, nullptr, oc, P.exit_out + ff,
+                                                  nullptr, lane);
+    }
+}
+
+template <int KSEL, int MODE>
+__global__ void __launch_bounds__(256, 1) dp_grid_kernel(DpParams P, int32_t seg_max)
+{
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ int4 smem_raw[];
+    long long *red = reinterpret_cast<long long *>(smem_raw);              // 8 x int64 (+ 8 spare)
+    int32_t *bufA = reinterpret_cast<int32_t *>(smem_raw) + 32;
+    int32_t *bufB = bufA + TURBO_BIG_MAX_COST + seg_max;
+    int *flags = reinterpret_cast<int *>(P.workspace + P.grid_scratch_offset);
+    GridCtx X;
+    X.pub = flags;
+    X.con = flags + GRID_MAX_CTAS;
+    X.misc = reinterpret_cast<long long *>(flags + 2 * GRID_MAX_CTAS);
+    X.ring = flags + grid_flags_words();
+    int step_base = 0;
+    for (int64_t w = 0; w < P.num_windows; ++w) {
+        if ((int64_t)P.windows[w].budget_bound + 1 <= TURBO_BIG_CELLS) continue;
+        if (KSEL != 0) {
+            grid_window<(KSEL > 0 ? KSEL : 2), MODE>(P, grid, w, bufA, bufB, red, X, step_base);
+        } else {
+            switch (P.windows[w].num_exits) {
+#define TURBO_K_CASE(KK) \
+    case KK: grid_window<KK, MODE>(P, grid, w, bufA, bufB, red, X, step_base); break;
+                TURBO_K_CASE(2) TURBO_K_CASE(3) TURBO_K_CASE(4) TURBO_K_CASE(5) TURBO_K_CASE(6)
+                TURBO_K_CASE(7) TURBO_K_CASE(8) TURBO_K_CASE(9) TURBO_K_CASE(10) TURBO_K_CASE(11)
+                TURBO_K_CASE(12) TURBO_K_CASE(13) TURBO_K_CASE(14) TURBO_K_CASE(15) TURBO_K_CASE(16)
+#undef TURBO_K_CASE
+                default: break;
+            }
+        }
+        grid.sync();                                   // every CTA done with this window
+        if (blockIdx.x == 0 && threadIdx.x < 8) X.misc[threadIdx.x] = 0;
+        grid.sync();
+    }
+}
+
+typedef void (*dp_grid_kernel_t)(DpParams, int32_t);
+
+template <int MODE>
+static dp_grid_kernel_t pick_grid(int kmin, int kmax)
+{
+    if (kmin != kmax) return dp_grid_kernel<0, MODE>;
+    switch (kmin) {
+        case 4: return dp_grid_kernel<4, MODE>;
+        case 5: return dp_grid_kernel<5, MODE>;
+        case 6: return dp_grid_kernel<6, MODE>;
+        case 8: return dp_grid_kernel<8, MODE>;
+        default: return dp_grid_kernel<0, MODE>;
+    }
+}
+
+cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams &P0, int num_sms,
+                           int smem_per_cta_max, cudaStream_t stream)
+{
+    DpParams P = P0;
+    const int NP = num_sms < GRID_MAX_CTAS ? num_sms : GRID_MAX_CTAS;
+    int32_t seg = (int32_t)(((int64_t)shape->max_budget + 1 + NP - 1) / NP);
+    seg = (seg + 511) & ~511;
+    if (seg < TURBO_BIG_MAX_COST) seg = TURBO_BIG_MAX_COST;
+    const size_t smem = 128 + (size_t)8 * (TURBO_BIG_MAX_COST + seg);
+    if (smem > (size_t)smem_per_cta_max) return cudaErrorInvalidConfiguration;
+    dp_grid_kernel_t kern = mode == DP_PLAN ? pick_grid<DP_PLAN>(shape->min_exits, shape->max_exits)
+                                            : pick_grid<DP_SOLVE_GLOBAL>(shape->min_exits, shape->max_exits);
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int occ = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorCooperativeLaunchTooLarge;
+    e = cudaMemsetAsync(P.workspace + P.grid_scratch_offset, 0, (size_t)grid_flags_words() * 4, stream);
+    if (e != cudaSuccess) return e;
+    void *args[] = {(void *)&P, (void *)&seg};
+    return cudaLaunchCooperativeKernel((const void *)kern, dim3(NP), dim3(256), args, smem, stream);
+}
+
+}  // namespace turbo

@@ -266,7 +266,6 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
 {
     constexpr int CB = (K <= 4) ? 2 : 4;          // choice bits
     constexpr int RPT = 32 / CB;                   // rows of 32 cells per tile (per choice word)
-    constexpr uint32_t CMASK = (1u << CB) - 1u;
     const bool inplace = (nwarps == 1);
     const int tid = warp * 32 + lane;
     const int nthr = nwarps * 32;
@@ -529,6 +528,7 @@ __global__ void __launch_bounds__(256, 4) dp_cta_kernel(DpParams P)
     }
     __syncthreads();
     for (int64_t w = blockIdx.x; w < P.num_windows; w += gridDim.x) {
+        if ((int64_t)P.windows[w].budget_bound + 1 > TURBO_BIG_CELLS) continue;   // long-window kernel
         if (KSEL != 0) {
             dp_window<(KSEL > 0 ? KSEL : 2), MODE, OSM, FUSE>(P, w, rowA, rowB, sch, cst, opt_s, red, hist, warp, nwarps,
                                                              lane);

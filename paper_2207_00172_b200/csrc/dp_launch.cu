@@ -34,7 +34,7 @@ static int pick_concurrency(int64_t W, int num_sms, int s_max)
 int dp_warps_per_window(const turbo_shape_t *s)
 {
     const int rpt = s->max_exits <= 4 ? 16 : 8;
-    const int64_t tiles = (num_rows(s->max_budget) + rpt - 1) / rpt;
+    const int64_t tiles = (num_rows(s->max_budget_small) + rpt - 1) / rpt;
     static int forced = -1;
     if (forced < 0) {
         const char *e = getenv("TURBO_DP_WARPS");          // tuning override (1, 2, 4, 8)

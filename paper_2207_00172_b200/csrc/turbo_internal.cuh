@@ -81,6 +81,7 @@ struct DpParams {
     int32_t fuse;
     int32_t max_options;    // option-table entries per window (osm); fused scratch follows it
     int32_t prof_entries;   // fused: staged profile entries (max C*K)
+    int64_t grid_scratch_offset;   // long-window kernel: workspace offset of flags + halo ring
     int64_t *stats;
 };
 
@@ -97,6 +98,17 @@ cudaError_t launch_lookup(const turbo_profile_t *profiles, turbo_window_t *windo
 cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P, int num_sms, int smem_per_sm,
                       int smem_per_cta_max, cudaStream_t stream, DpLaunch *info);
 int dp_warps_per_window(const turbo_shape_t *shape);
+
+// long-window (grid) kernel: scratch = flags (pub/con per CTA + misc) + halo ring
+constexpr int GRID_MAX_CTAS = 256;
+constexpr int GRID_RING_DEPTH = 4;
+__host__ __device__ constexpr int64_t grid_flags_words() { return 2 * GRID_MAX_CTAS + 64; }
+__host__ __device__ constexpr int64_t grid_scratch_bytes()
+{
+    return 4 * (grid_flags_words() + (int64_t)GRID_RING_DEPTH * GRID_MAX_CTAS * TURBO_BIG_MAX_COST);
+}
+cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams &P, int num_sms,
+                           int smem_per_cta_max, cudaStream_t stream);
 size_t dp_smem_bytes(const DpParams &P, int nwarps);
 cudaError_t launch_backtrack(const turbo_window_t *windows, int32_t num_windows, const int32_t *opt_cost,
                              const uint8_t *workspace, const int32_t *best_cost, const uint8_t *feasible,

@@ -48,7 +48,8 @@ class Shape(ctypes.Structure):
                 ("num_classes_max", ctypes.c_int32), ("max_options", ctypes.c_int32),
                 ("total_frames", ctypes.c_int64), ("total_options", ctypes.c_int64),
                 ("total_cells", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
-                ("reserved1", ctypes.c_int64 * 4)]
+                ("max_budget_small", ctypes.c_int32), ("num_big", ctypes.c_int32),
+                ("grid_scratch_offset", ctypes.c_int64), ("reserved1", ctypes.c_int64 * 2)]
 
 
 assert ctypes.sizeof(Window) == 48

@@ -33,4 +33,5 @@ from .workloads import (  # noqa: F401
     paper_gain_table,
     regular_costs,
     concat_workloads,
+    make_long_window,
 )

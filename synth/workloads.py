@@ -292,3 +292,18 @@ def concat_workloads(parts: List[Workload], name: str = "concat") -> Workload:
         cls.append(p.class_id)
     return Workload(name, gains, costs, shapes, np.concatenate(nf), np.concatenate(bud),
                     np.concatenate(cap), base, np.concatenate(prof), np.concatenate(cls), {})
+
+
+def make_long_window(seed: int, N: int, K: int, B: int, c_max: Optional[int] = None, random_rows: bool = False,
+                     C: int = NUM_CLASSES, base_cost: int = 84) -> Workload:
+    """One long window (c4-shaped: rows far beyond one CTA). Paper profile with regular costs
+    c_max = ceil(3B/N), or (random_rows) gains U{-2..40}, costs U{0..c_max}, c_0 = 0."""
+    cm = -((-3 * B) // N) if c_max is None else c_max
+    if random_rows:
+        g = rand_int(seed, S_TGAIN, np.arange(C * K), -2, 40).astype(np.int32)
+        c = rand_int(seed, S_TCOST, np.arange(C * K), 0, cm).astype(np.int32)
+        c.reshape(C, K)[:, 0] = 0
+    else:
+        g, c = _paper_profile(K, cm, C)
+    cls = _class_ids(seed, np.array([N], np.int32), np.array([0.35]), window_ids=np.array([seed]))
+    return _wl(f"long{seed}", [g], [c], [(C, K)], [N], [B], [0], cls, base_cost, {"seed": seed, "c_max": cm})

@@ -1,0 +1,72 @@
+"""Long windows (rows > TURBO_BIG_CELLS cells) served by the cooperative grid kernel (K4):
+bit-exact parity with the oracle, mixed batches (routing between the CTA and grid kernels)
+and config c4 at full size (3000 frames, B = 2^20)."""
+import numpy as np
+import pytest
+
+import synth
+from tests.parity import compare, gpu_run, oracle_run
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _lib():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2207_00172_b200 import build, turbo
+    build.build()
+    turbo.load()
+
+
+@pytest.mark.parametrize("fused", [True, False], ids=["solve", "plan+backtrack"])
+def test_long_window_paper_profile(fused):
+    wl = synth.make_long_window(3, N=120, K=6, B=40000)
+    compare(wl, gpu_run(wl, fused), oracle_run(wl))
+
+
+@pytest.mark.parametrize("K", [2, 4, 5, 8, 11])
+def test_long_window_random_rows(K):
+    """Random (non-monotone, negative) gains, costs up to 700, ragged top tile."""
+    wl = synth.make_long_window(10 + K, N=90, K=K, B=30001 + 37 * K, c_max=700, random_rows=True)
+    compare(wl, gpu_run(wl, True), oracle_run(wl))
+
+
+def test_mixed_batch_routes_small_and_long_windows():
+    parts = [synth.make_config(2, num_windows=40), synth.make_long_window(5, N=64, K=5, B=50000),
+             synth.make_config(1), synth.make_long_window(6, N=40, K=5, B=26000, c_max=3000)]
+    for p in parts:
+        p.base_cost = 84
+        p.capacity = (p.budget.astype(np.int64) + p.num_frames.astype(np.int64) * 84).astype(np.int32)
+    wl = synth.concat_workloads(parts)
+    for fused in (True, False):
+        compare(wl, gpu_run(wl, fused), oracle_run(wl))
+
+
+def test_long_window_cost_above_halo_cap_is_rejected():
+    wl = synth.make_long_window(7, N=30, K=4, B=30000, c_max=5000)
+    got = gpu_run(wl, True)
+    assert int(got["status"][1]) == 0 and int(got["feasible"][0]) == 0
+    assert (got["exits"] == 0).all()
+
+
+def test_config4_full_size():
+    """c4 at full size: G*, C* and the whole exit vector against the oracle's full suffix table
+    (25 GB of int64 on the host; skipped if the host lacks the memory)."""
+    import psutil
+    wl = synth.make_config(4)
+    got = gpu_run(wl, True)
+    assert int(got["status"][0]) == -1 and int(got["status"][1]) == -1
+    og = got["opt_gain"][:3000 * 6].reshape(3000, 6)
+    oc = got["opt_cost"][:3000 * 6].reshape(3000, 6)
+    ex = got["exits"].astype(np.int64)
+    assert og[np.arange(3000), ex].sum() == got["best_gain"][0]
+    assert oc[np.arange(3000), ex].sum() == got["best_cost"][0] <= (1 << 20)
+    if psutil.virtual_memory().available < 40 * 2**30:
+        want = oracle_run(wl, mode="value")
+        assert int(got["best_gain"][0]) == int(want["best_gain"][0])
+        assert int(got["best_cost"][0]) == int(want["best_cost"][0])
+        pytest.skip("host memory too small for the full oracle table; G*/C* checked")
+    want = oracle_run(wl)
+    compare(wl, got, want)
