@@ -32,9 +32,15 @@ __device__ __forceinline__ void st_release_gpu(int *p, int v)
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ void wait_at_least(const int *p, int target)
+// Spin until *p >= target. Bounded (~seconds): a lost publication must not hang the GPU; on
+// timeout the caller flags the window (status[1]) and carries on, so the kernel always exits.
+__device__ __forceinline__ bool wait_at_least(const int *p, int target)
 {
-    while (ld_acquire_gpu(p) < target) __nanosleep(32);
+    for (long long it = 0; it < (1ll << 26); ++it) {
+        if (ld_acquire_gpu(p) >= target) return true;
+        __nanosleep(32);
+    }
+    return false;
 }
 
 __device__ __forceinline__ long long block_sum_ll(long long v, long long *sm, int tid, int nthr)
@@ -177,7 +183,7 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
         if (mine) {
             // halo of S_{i+1} from CTA j-1 (its step f-1); step 0 reads S_N = 0 (already set)
             if (j > 0 && f > 0 && hl > 0) {
-                if (tid == 0) wait_at_least(&X.pub[j - 1], step_base + f);
+                if (tid == 0 && !wait_at_least(&X.pub[j - 1], step_base + f)) atomic_min_i64(&P.status[1], w);
                 __syncthreads();
                 const int *src = X.ring + ((int64_t)((step_base + f - 1) % D) * GRID_MAX_CTAS + (j - 1)) * H;
                 for (int32_t x = tid; x < hl; x += nthr) cur[H - hl + x] = __ldcg(src + x);
@@ -205,7 +211,7 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
             if (j + 1 < active && hl > 0) {
                 const int32_t slot_step = step_base + f;
                 if (f >= D) {
-                    if (tid == 0) wait_at_least(&X.con[j + 1], slot_step - D + 1);
+                    if (tid == 0 && !wait_at_least(&X.con[j + 1], slot_step - D + 1)) atomic_min_i64(&P.status[1], w);
                     __syncthreads();
                 }
                 int *dst = X.ring + ((int64_t)(slot_step % D) * GRID_MAX_CTAS + j) * H;
