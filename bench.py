@@ -36,6 +36,7 @@ WORKLOADS = {
     "c1": dict(config=1, per_gpu=1, desc="1 window x 30 frames, K=4, B=120"),
     "c2": dict(config=2, per_gpu=1024, desc="1024 streams x 1 s windows at 30 fps (N=30), K=5, B=1000 per GPU"),
     "c3": dict(config=3, per_gpu=8192, desc="8192 windows x 300 frames, K=8, B=4096 per GPU (c3 = 65536 over 8 GPUs)"),
+    "c4": dict(config=4, per_gpu=1, desc="single long window: 3000 frames, K=6, B=2^20 (grid-spanning row; replicas)"),
     "c5": dict(config=5, per_gpu=2048, desc="mixed sweep: K 2-16, B 64-16384, N 30-300, skewed classes; 2048 windows per GPU"),
 }
 
@@ -170,6 +171,12 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- GPU leg
+TURBO_BIG_CELLS = 24576          # include/turbo.h: rows longer than this use the grid kernel
+
+
+def _has_long_windows(wl) -> bool:
+    return bool((wl.budget.astype(np.int64) + 1 > TURBO_BIG_CELLS).any())
+
 def run_turbo(args):
     import torch
     ws, rank, local = dist_env()
@@ -190,6 +197,8 @@ def run_turbo(args):
     name = args.workload
     wl = make_workload(name, rank)
     path = args.path
+    if path == "auto":      # one fused launch unless long windows need the grid kernel
+        path = "solve" if _has_long_windows(wl) else "schedule"
     b = turbo.batch_from_workload(wl, device=dev, with_plan_workspace=(path == "plan"))
     stream = torch.cuda.current_stream(dev)
     fused = path == "solve"
@@ -398,8 +407,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["turbo", "reference"], default="turbo")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
-    ap.add_argument("--path", choices=["schedule", "solve", "plan"], default="schedule",
-                    help="schedule: one fused a1..a6 launch; solve: lookup, solve, stats; plan: 4 launches")
+    ap.add_argument("--path", choices=["auto", "schedule", "solve", "plan"], default="auto",
+                    help="auto: schedule unless long windows; schedule: one fused a1..a6 launch; solve: lookup, "
+                         "solve, stats; plan: 4 launches")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()

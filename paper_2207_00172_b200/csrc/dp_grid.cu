@@ -181,19 +181,9 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
             my_c = __ldg(oc + (int64_t)(i - 1) * K + lane);
         }
         if (mine) {
-            // halo of S_{i+1} from CTA j-1 (its step f-1); step 0 reads S_N = 0 (already set)
-            if (j > 0 && f > 0 && hl > 0) {
-                if (tid == 0 && !wait_at_least(&X.pub[j - 1], step_base + f)) atomic_min_i64(&P.status[1], w);
-                __syncthreads();
-                const int *src = X.ring + ((int64_t)((step_base + f - 1) % D) * GRID_MAX_CTAS + (j - 1)) * H;
-                for (int32_t x = tid; x < hl; x += nthr) cur[H - hl + x] = __ldcg(src + x);
-                __syncthreads();
-                if (tid == 0) st_release_gpu(&X.con[j], step_base + f);
-            }
-            // own tiles
             const int32_t *cur_base = cur + H - seg_lo;
             int32_t *nxt_base = nxt + H - seg_lo;
-            for (int32_t t = t_first + warp; t < t_end; t += nwarps) {
+            auto do_tile = [&](int32_t t) {
                 const int32_t b_lo = t * RPT * 32;
                 const int32_t nr = min(RPT, nrows - t * RPT);
                 if (nr == RPT)
@@ -205,23 +195,59 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
                 for (int r = 0; r < RPT; ++r)
                     if (r < nr) dst[r * 32] = key[r] & ~15;
                 gch[((int64_t)i * gtiles + t) * 32 + lane] = pack_choices<RPT, CB>(key);
-            }
-            __syncthreads();
-            // publish the top hl cells of S_i for CTA j+1
-            if (j + 1 < active && hl > 0) {
+            };
+            // halo of S_{i+1} from CTA j-1 (its step f-1); step 0 reads S_N = 0 (already set).
+            // Executed by one warp (the leader lane polls).
+            const bool need_halo = (j > 0 && f > 0 && hl > 0);
+            auto fetch_halo = [&]() {
+                if (lane == 0 && !wait_at_least(&X.pub[j - 1], step_base + f)) atomic_min_i64(&P.status[1], w);
+                __syncwarp();
+                const int *src = X.ring + ((int64_t)((step_base + f - 1) % D) * GRID_MAX_CTAS + (j - 1)) * H;
+                for (int32_t x = lane; x < hl; x += 32) cur[H - hl + x] = __ldcg(src + x);
+                __syncwarp();
+                if (lane == 0) st_release_gpu(&X.con[j], step_base + f);
+            };
+            // publish the top hl cells of S_i for CTA j+1 (one warp; ring slot back-pressured)
+            const bool publish = (j + 1 < active && hl > 0);
+            auto do_publish = [&]() {
                 const int32_t slot_step = step_base + f;
-                if (f >= D) {
-                    if (tid == 0 && !wait_at_least(&X.con[j + 1], slot_step - D + 1)) atomic_min_i64(&P.status[1], w);
-                    __syncthreads();
-                }
+                if (f >= D && lane == 0 && !wait_at_least(&X.con[j + 1], slot_step - D + 1))
+                    atomic_min_i64(&P.status[1], w);
+                __syncwarp();
                 int *dst = X.ring + ((int64_t)(slot_step % D) * GRID_MAX_CTAS + j) * H;
-                for (int32_t x = tid; x < hl; x += nthr) __stcg(dst + x, nxt[H + seg - hl + x]);
-                __syncthreads();
-                if (tid == 0) {
+                for (int32_t x = lane; x < hl; x += 32) __stcg(dst + x, nxt[H + seg - hl + x]);
+                __syncwarp();
+                if (lane == 0) {
                     __threadfence();
                     st_release_gpu(&X.pub[j], slot_step + 1);
                 }
+            };
+            const int32_t n_edge = (hl + 32 * RPT - 1) / (32 * RPT);   // tiles within hl of an edge
+            const int32_t bot_end = min(t_end, t_first + n_edge);        // tiles that read the halo
+            const int32_t top_lo = t_end - n_edge;                       // tiles holding published cells
+            if (nwarps >= 3 && top_lo >= bot_end) {
+                // 1) top tiles first, 2) warp 0 publishes them while warp 1 fetches the halo and the
+                // others compute the middle, 3) bottom tiles once the halo is in: the exchange
+                // latency hides behind the middle of the segment.
+                for (int32_t t = t_end - 1 - warp; t >= top_lo; t -= nwarps) do_tile(t);
+                __syncthreads();
+                if (warp == 0) {
+                    if (publish) do_publish();
+                } else if (warp == 1) {
+                    if (need_halo) fetch_halo();
+                } else {
+                    for (int32_t t = top_lo - 1 - (warp - 2); t >= bot_end; t -= nwarps - 2) do_tile(t);
+                }
+                __syncthreads();
+                for (int32_t t = bot_end - 1 - warp; t >= t_first; t -= nwarps) do_tile(t);
+            } else {
+                if (need_halo && warp == 0) fetch_halo();
+                __syncthreads();
+                for (int32_t t = t_first + warp; t < t_end; t += nwarps) do_tile(t);
+                __syncthreads();
+                if (publish && warp == 0) do_publish();
             }
+            __syncthreads();                                   // S_i complete before the swap
         }
         int32_t *tmp = cur;
         cur = nxt;
@@ -259,7 +285,7 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
 }
 
 template <int KSEL, int MODE>
-__global__ void __launch_bounds__(256, 1) dp_grid_kernel(DpParams P, int32_t seg_max)
+__global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg_max)
 {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ int4 smem_raw[];
@@ -295,6 +321,7 @@ __global__ void __launch_bounds__(256, 1) dp_grid_kernel(DpParams P, int32_t seg
 }
 
 typedef void (*dp_grid_kernel_t)(DpParams, int32_t);
+static const int GRID_THREADS = 512;
 
 template <int MODE>
 static dp_grid_kernel_t pick_grid(int kmin, int kmax)
@@ -324,13 +351,13 @@ cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams 
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, GRID_THREADS, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorCooperativeLaunchTooLarge;
     e = cudaMemsetAsync(P.workspace + P.grid_scratch_offset, 0, (size_t)grid_flags_words() * 4, stream);
     if (e != cudaSuccess) return e;
     void *args[] = {(void *)&P, (void *)&seg};
-    return cudaLaunchCooperativeKernel((const void *)kern, dim3(NP), dim3(256), args, smem, stream);
+    return cudaLaunchCooperativeKernel((const void *)kern, dim3(NP), dim3(GRID_THREADS), args, smem, stream);
 }
 
 }  // namespace turbo
