@@ -43,6 +43,16 @@ __device__ __forceinline__ bool wait_at_least(const int *p, int target)
     return false;
 }
 
+__device__ __forceinline__ void named_sync(int id, int n)
+{
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__device__ __forceinline__ void named_arrive(int id, int n)
+{
+    asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
 __device__ __forceinline__ long long block_sum_ll(long long v, long long *sm, int tid, int nthr)
 {
 #pragma unroll
@@ -217,42 +227,55 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
                 int *dst = X.ring + ((int64_t)(slot_step % D) * GRID_MAX_CTAS + j) * H;
                 for (int32_t x = lane; x < hl; x += 32) __stcg(dst + x, nxt[H + seg - hl + x]);
                 __syncwarp();
-                if (lane == 0) {
-                    __threadfence();
-                    st_release_gpu(&X.pub[j], slot_step + 1);
-                }
+                if (lane == 0) st_release_gpu(&X.pub[j], slot_step + 1);   // orders the warp's ring stores
             };
             const int32_t n_edge = (hl + 32 * RPT - 1) / (32 * RPT);   // tiles within hl of an edge
             const int32_t bot_end = min(t_end, t_first + n_edge);        // tiles that read the halo
             const int32_t top_lo = t_end - n_edge;                       // tiles holding published cells
-            if (nwarps >= 3 && top_lo >= bot_end) {
-                // 1) top tiles first, 2) warp 0 publishes them while warp 1 fetches the halo and the
-                // others compute the middle, 3) bottom tiles once the halo is in: the exchange
-                // latency hides behind the middle of the segment.
-                for (int32_t t = t_end - 1 - warp; t >= top_lo; t -= nwarps) do_tile(t);
-                __syncthreads();
-                if (warp == 0) {
-                    if (publish) do_publish();
-                } else if (warp == 1) {
-                    if (need_halo) fetch_halo();
-                } else {
-                    for (int32_t t = top_lo - 1 - (warp - 2); t >= bot_end; t -= nwarps - 2) do_tile(t);
+            const bool split = top_lo >= bot_end;                        // top tiles never need the halo
+            // Warp specialisation: warps 0..C-1 compute tiles, warp C (the last) exchanges halos.
+            // Named barriers (ids by step parity; 0 is __syncthreads): TOP = compute warps have
+            // written the published cells (arrive) -> comm warp publishes (sync); HALO = comm warp
+            // has fetched the halo (arrive) -> compute warps may do the bottom tiles (sync);
+            // STEP = compute warps only, S_i complete before the buffers swap.
+            const int C = nwarps - 1;
+            const int par = f & 1;
+            const int bar_top = 1 + par, bar_halo = 3 + par, bar_step = 5;
+            if (warp < C) {
+                const int32_t n_pre = split ? t_end - bot_end : 0;      // top first, then the middle
+                bool arrived = false;
+                if (split && n_edge <= warp) {
+                    named_arrive(bar_top, nthr);
+                    arrived = true;
                 }
-                __syncthreads();
-                for (int32_t t = bot_end - 1 - warp; t >= t_first; t -= nwarps) do_tile(t);
+                for (int32_t idx = warp; idx < n_pre; idx += C) {
+                    do_tile(t_end - 1 - idx);
+                    if (!arrived && idx + C >= n_edge) {
+                        __threadfence_block();
+                        named_arrive(bar_top, nthr);
+                        arrived = true;
+                    }
+                }
+                named_sync(bar_halo, nthr);
+                for (int32_t t = (split ? bot_end : t_end) - 1 - warp; t >= t_first; t -= C) do_tile(t);
+                if (!arrived) {
+                    __threadfence_block();
+                    named_arrive(bar_top, nthr);
+                }
+                named_sync(bar_step, C * 32);
             } else {
-                if (need_halo && warp == 0) fetch_halo();
-                __syncthreads();
-                for (int32_t t = t_first + warp; t < t_end; t += nwarps) do_tile(t);
-                __syncthreads();
-                if (publish && warp == 0) do_publish();
+                if (need_halo) fetch_halo();
+                __threadfence_block();
+                named_arrive(bar_halo, nthr);
+                named_sync(bar_top, nthr);
+                if (publish) do_publish();
             }
-            __syncthreads();                                   // S_i complete before the swap
         }
         int32_t *tmp = cur;
         cur = nxt;
         nxt = tmp;
     }
+    __syncthreads();                                   // compute and comm warps leave the frame loop
     step_base += N;
 
     // ---- a4: G* = S_0[B] (owned by the last active CTA), C* = #{b <= B : S_0[b] < G*}
