@@ -14,6 +14,8 @@
 // standard layout (the backtrack kernels read them unchanged).
 #include <cooperative_groups.h>
 
+#include <mutex>
+
 #include "dp_kernel.cuh"
 
 namespace cg = cooperative_groups;
@@ -25,6 +27,23 @@ __device__ __forceinline__ int ld_acquire_gpu(const int *p)
     int v;
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long *p)
+{
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned long long v)
+{
+    asm volatile("st.relaxed.gpu.global.b64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void st_relaxed_u32(int *p, int v)
+{
+    asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ void st_release_gpu(int *p, int v)
@@ -70,7 +89,7 @@ struct GridCtx {
     int *pub;               // [GRID_MAX_CTAS] steps published (monotone across windows)
     int *con;               // [GRID_MAX_CTAS] steps whose halo was consumed
     long long *misc;        // [8] per-window reductions (zeroed between windows)
-    int *ring;              // [D][GRID_MAX_CTAS][TURBO_BIG_MAX_COST]
+    unsigned long long *ring;   // [D][GRID_MAX_CTAS][TURBO_BIG_MAX_COST] of {value, step tag}
 };
 
 template <int K, int MODE>
@@ -209,13 +228,30 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
             // halo of S_{i+1} from CTA j-1 (its step f-1); step 0 reads S_N = 0 (already set).
             // Executed by one warp (the leader lane polls).
             const bool need_halo = (j > 0 && f > 0 && hl > 0);
+            // Low-latency protocol: every ring element is one 64-bit word {value, step tag}, stored
+            // and polled with relaxed gpu-scope accesses -- the tag proves the value is current, so
+            // no fence and no separate flag sit on the exchange path.
             auto fetch_halo = [&]() {
-                if (lane == 0 && !wait_at_least(&X.pub[j - 1], step_base + f)) atomic_min_i64(&P.status[1], w);
-                __syncwarp();
-                const int *src = X.ring + ((int64_t)((step_base + f - 1) % D) * GRID_MAX_CTAS + (j - 1)) * H;
-                for (int32_t x = lane; x < hl; x += 32) cur[H - hl + x] = __ldcg(src + x);
-                __syncwarp();
-                if (lane == 0) st_release_gpu(&X.con[j], step_base + f);
+                const uint32_t tag = (uint32_t)(step_base + f);          // j-1's step f-1 publishes tag sb+f
+                const unsigned long long *src =
+                    X.ring + ((int64_t)((step_base + f - 1) % D) * GRID_MAX_CTAS + (j - 1)) * H;
+                bool ok = true;
+                for (int32_t x = lane; x < hl; x += 32) {
+                    unsigned long long v = ld_relaxed_u64(src + x);
+                    for (long long it = 0; (uint32_t)(v >> 32) != tag; ++it) {
+                        if (it > (1ll << 24)) {
+                            ok = false;
+                            break;
+                        }
+                        __nanosleep(20);
+                        v = ld_relaxed_u64(src + x);
+                    }
+                    cur[H - hl + x] = (int32_t)(uint32_t)v;
+                }
+                if (!__all_sync(0xffffffffu, ok) && lane == 0) atomic_min_i64(&P.status[1], w);
+            };
+            auto release_halo_slot = [&]() {                               // back-pressure only
+                if (lane == 0) st_relaxed_u32(&X.con[j], step_base + f);
             };
             // publish the top hl cells of S_i for CTA j+1 (one warp; ring slot back-pressured)
             const bool publish = (j + 1 < active && hl > 0);
@@ -224,10 +260,10 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
                 if (f >= D && lane == 0 && !wait_at_least(&X.con[j + 1], slot_step - D + 1))
                     atomic_min_i64(&P.status[1], w);
                 __syncwarp();
-                int *dst = X.ring + ((int64_t)(slot_step % D) * GRID_MAX_CTAS + j) * H;
-                for (int32_t x = lane; x < hl; x += 32) __stcg(dst + x, nxt[H + seg - hl + x]);
-                __syncwarp();
-                if (lane == 0) st_release_gpu(&X.pub[j], slot_step + 1);   // orders the warp's ring stores
+                unsigned long long *dst = X.ring + ((int64_t)(slot_step % D) * GRID_MAX_CTAS + j) * H;
+                const unsigned long long tag = (unsigned long long)(uint32_t)(slot_step + 1) << 32;
+                for (int32_t x = lane; x < hl; x += 32)
+                    st_relaxed_u64(dst + x, tag | (uint32_t)nxt[H + seg - hl + x]);
             };
             const int32_t n_edge = (hl + 32 * RPT - 1) / (32 * RPT);   // tiles within hl of an edge
             const int32_t bot_end = min(t_end, t_first + n_edge);        // tiles that read the halo
@@ -267,6 +303,7 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
                 if (need_halo) fetch_halo();
                 __threadfence_block();
                 named_arrive(bar_halo, nthr);
+                if (need_halo) release_halo_slot();
                 named_sync(bar_top, nthr);
                 if (publish) do_publish();
             }
@@ -308,7 +345,7 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
 }
 
 template <int KSEL, int MODE>
-__global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg_max)
+__global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg_max, int32_t tag_base)
 {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ int4 smem_raw[];
@@ -320,8 +357,8 @@ __global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg
     X.pub = flags;
     X.con = flags + GRID_MAX_CTAS;
     X.misc = reinterpret_cast<long long *>(flags + 2 * GRID_MAX_CTAS);
-    X.ring = flags + grid_flags_words();
-    int step_base = 0;
+    X.ring = reinterpret_cast<unsigned long long *>(flags + grid_flags_words());
+    int step_base = tag_base;          // ring tags of this launch never repeat an earlier launch's
     for (int64_t w = 0; w < P.num_windows; ++w) {
         if ((int64_t)P.windows[w].budget_bound + 1 <= TURBO_BIG_CELLS) continue;
         if (KSEL != 0) {
@@ -343,7 +380,7 @@ __global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg
     }
 }
 
-typedef void (*dp_grid_kernel_t)(DpParams, int32_t);
+typedef void (*dp_grid_kernel_t)(DpParams, int32_t, int32_t);
 static const int GRID_THREADS = 512;
 
 template <int MODE>
@@ -379,7 +416,24 @@ cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams 
     if (occ < 1) return cudaErrorCooperativeLaunchTooLarge;
     e = cudaMemsetAsync(P.workspace + P.grid_scratch_offset, 0, (size_t)grid_flags_words() * 4, stream);
     if (e != cudaSuccess) return e;
-    void *args[] = {(void *)&P, (void *)&seg};
+    // ring tags: a per-process epoch advanced past every step this launch can take, so a stale
+    // ring word from an earlier launch can never carry a matching tag (the ring is cleared when
+    // the epoch wraps)
+    static std::mutex mu;
+    int32_t tag_base;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        static int64_t epoch = 1;
+        const int64_t span = (int64_t)shape->num_big * shape->max_frames + 2;
+        if (epoch + span >= (1ll << 30)) {
+            e = cudaMemsetAsync(P.workspace + P.grid_scratch_offset, 0, (size_t)grid_scratch_bytes(), stream);
+            if (e != cudaSuccess) return e;
+            epoch = 1;
+        }
+        tag_base = (int32_t)epoch;
+        epoch += span;
+    }
+    void *args[] = {(void *)&P, (void *)&seg, (void *)&tag_base};
     return cudaLaunchCooperativeKernel((const void *)kern, dim3(NP), dim3(GRID_THREADS), args, smem, stream);
 }
 

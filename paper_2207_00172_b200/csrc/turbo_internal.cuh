@@ -105,7 +105,7 @@ constexpr int GRID_RING_DEPTH = 4;
 __host__ __device__ constexpr int64_t grid_flags_words() { return 2 * GRID_MAX_CTAS + 64; }
 __host__ __device__ constexpr int64_t grid_scratch_bytes()
 {
-    return 4 * (grid_flags_words() + (int64_t)GRID_RING_DEPTH * GRID_MAX_CTAS * TURBO_BIG_MAX_COST);
+    return 4 * grid_flags_words() + 8 * (int64_t)GRID_RING_DEPTH * GRID_MAX_CTAS * TURBO_BIG_MAX_COST;
 }
 cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams &P, int num_sms,
                            int smem_per_cta_max, cudaStream_t stream);
