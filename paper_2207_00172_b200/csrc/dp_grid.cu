@@ -236,17 +236,27 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
                 const unsigned long long *src =
                     X.ring + ((int64_t)((step_base + f - 1) % D) * GRID_MAX_CTAS + (j - 1)) * H;
                 bool ok = true;
-                for (int32_t x = lane; x < hl; x += 32) {
-                    unsigned long long v = ld_relaxed_u64(src + x);
-                    for (long long it = 0; (uint32_t)(v >> 32) != tag; ++it) {
-                        if (it > (1ll << 24)) {
-                            ok = false;
-                            break;
-                        }
-                        __nanosleep(20);
-                        v = ld_relaxed_u64(src + x);
+                for (int32_t x0 = 0; x0 < hl; x0 += 32 * 8) {          // 8 independent loads in flight
+                    unsigned long long v[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int32_t x = x0 + u * 32 + lane;
+                        v[u] = x < hl ? ld_relaxed_u64(src + x) : 0ull;
                     }
-                    cur[H - hl + x] = (int32_t)(uint32_t)v;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        const int32_t x = x0 + u * 32 + lane;
+                        if (x >= hl) continue;
+                        for (long long it = 0; (uint32_t)(v[u] >> 32) != tag; ++it) {   // rarely taken
+                            if (it > (1ll << 24)) {
+                                ok = false;
+                                break;
+                            }
+                            __nanosleep(20);
+                            v[u] = ld_relaxed_u64(src + x);
+                        }
+                        cur[H - hl + x] = (int32_t)(uint32_t)v[u];
+                    }
                 }
                 if (!__all_sync(0xffffffffu, ok) && lane == 0) atomic_min_i64(&P.status[1], w);
             };
