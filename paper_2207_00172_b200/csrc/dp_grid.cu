@@ -14,6 +14,7 @@
 // standard layout (the backtrack kernels read them unchanged).
 #include <cooperative_groups.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "dp_kernel.cuh"
@@ -44,6 +45,60 @@ __device__ __forceinline__ void st_relaxed_u64(unsigned long long *p, unsigned l
 __device__ __forceinline__ void st_relaxed_u32(int *p, int v)
 {
     asm volatile("st.relaxed.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t smem_addr(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *mbar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(mbar)), "r"(count) : "memory");
+}
+
+// TMA 1-D bulk copy global -> shared, completion signalled on the mbarrier (expect_tx bytes)
+__device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t bytes, uint64_t *mbar)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(mbar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_addr(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_addr(mbar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t phase)
+{
+    asm volatile(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+            smem_addr(mbar)),
+        "r"(phase)
+        : "memory");
+}
+
+// TMA 1-D bulk copy shared -> global (bulk async-group)
+__device__ __forceinline__ void tma_store_1d(void *dst, const void *src, uint32_t bytes)
+{
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_addr(src)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_store_wait_read()
+{
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void tma_store_wait_all()
+{
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async()
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
 __device__ __forceinline__ void st_release_gpu(int *p, int v)
@@ -94,7 +149,8 @@ struct GridCtx {
 
 template <int K, int MODE>
 __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, int32_t *bufA, int32_t *bufB,
-                           long long *red, GridCtx X, int &step_base)
+                           long long *red, GridCtx X, int &step_base, unsigned long long *stage_in,
+                           unsigned long long *stage_out, uint64_t *mbar, uint32_t &mbar_phase)
 {
     constexpr int CB = (K <= 4) ? 2 : 4;
     constexpr int RPT = 32 / CB;
@@ -227,53 +283,53 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
             };
             // halo of S_{i+1} from CTA j-1 (its step f-1); step 0 reads S_N = 0 (already set).
             // Executed by one warp (the leader lane polls).
-            const bool need_halo = (j > 0 && f > 0 && hl > 0);
-            // Low-latency protocol: every ring element is one 64-bit word {value, step tag}, stored
-            // and polled with relaxed gpu-scope accesses -- the tag proves the value is current, so
-            // no fence and no separate flag sit on the exchange path.
+            const bool need_halo = (j > 0 && f > 0 && hl > 0) && !(P.debug & 1);
+            // Halo exchange through the L2 ring with the Tensor Memory Accelerator: every ring element
+            // is one 64-bit word {value, step tag}. The publisher packs its top cells into a smem
+            // stage and issues ONE bulk store (cp.async.bulk global <- shared); the consumer issues
+            // ONE bulk load into its own stage (mbarrier completion) and checks the tags -- a stale
+            // tag (publication still in flight) just re-issues the copy. No fence, no flag word.
+            const int32_t hl8 = (hl + 1) & ~1;                         // 16-byte multiple of 8-B words
             auto fetch_halo = [&]() {
                 const uint32_t tag = (uint32_t)(step_base + f);          // j-1's step f-1 publishes tag sb+f
                 const unsigned long long *src =
                     X.ring + ((int64_t)((step_base + f - 1) % D) * GRID_MAX_CTAS + (j - 1)) * H;
-                bool ok = true;
-                for (int32_t x0 = 0; x0 < hl; x0 += 32 * 8) {          // 8 independent loads in flight
-                    unsigned long long v[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int32_t x = x0 + u * 32 + lane;
-                        v[u] = x < hl ? ld_relaxed_u64(src + x) : 0ull;
+                bool ok = false;
+                for (int attempt = 0; attempt < (1 << 22) && !ok; ++attempt) {
+                    if (lane == 0) {
+                        tma_load_1d(stage_in, src, hl8 * 8, mbar);
+                        mbar_wait(mbar, mbar_phase);
                     }
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        const int32_t x = x0 + u * 32 + lane;
-                        if (x >= hl) continue;
-                        for (long long it = 0; (uint32_t)(v[u] >> 32) != tag; ++it) {   // rarely taken
-                            if (it > (1ll << 24)) {
-                                ok = false;
-                                break;
-                            }
-                            __nanosleep(20);
-                            v[u] = ld_relaxed_u64(src + x);
-                        }
-                        cur[H - hl + x] = (int32_t)(uint32_t)v[u];
-                    }
+                    mbar_phase ^= 1u;
+                    __syncwarp();
+                    bool mine_ok = true;
+                    for (int32_t x = lane; x < hl8; x += 32) mine_ok &= (uint32_t)(stage_in[x] >> 32) == tag;
+                    ok = __all_sync(0xffffffffu, mine_ok);
+                    if (!ok) __nanosleep(64);
                 }
-                if (!__all_sync(0xffffffffu, ok) && lane == 0) atomic_min_i64(&P.status[1], w);
+                if (!ok && lane == 0) atomic_min_i64(&P.status[1], w);
+                for (int32_t x = lane; x < hl8; x += 32) cur[H - hl8 + x] = (int32_t)(uint32_t)stage_in[x];
             };
             auto release_halo_slot = [&]() {                               // back-pressure only
                 if (lane == 0) st_relaxed_u32(&X.con[j], step_base + f);
             };
-            // publish the top hl cells of S_i for CTA j+1 (one warp; ring slot back-pressured)
-            const bool publish = (j + 1 < active && hl > 0);
+            // publish the top hl8 cells of S_i for CTA j+1 (ring slot back-pressured)
+            const bool publish = (j + 1 < active && hl > 0) && !(P.debug & 1);
             auto do_publish = [&]() {
                 const int32_t slot_step = step_base + f;
-                if (f >= D && lane == 0 && !wait_at_least(&X.con[j + 1], slot_step - D + 1))
-                    atomic_min_i64(&P.status[1], w);
+                if (lane == 0) {
+                    if (f >= D && !wait_at_least(&X.con[j + 1], slot_step - D + 1)) atomic_min_i64(&P.status[1], w);
+                    tma_store_wait_read();                                 // previous store has read the stage
+                }
                 __syncwarp();
-                unsigned long long *dst = X.ring + ((int64_t)(slot_step % D) * GRID_MAX_CTAS + j) * H;
                 const unsigned long long tag = (unsigned long long)(uint32_t)(slot_step + 1) << 32;
-                for (int32_t x = lane; x < hl; x += 32)
-                    st_relaxed_u64(dst + x, tag | (uint32_t)nxt[H + seg - hl + x]);
+                for (int32_t x = lane; x < hl8; x += 32) stage_out[x] = tag | (uint32_t)nxt[H + seg - hl8 + x];
+                fence_proxy_async();                                       // generic smem writes -> TMA
+                __syncwarp();
+                if (lane == 0) {
+                    unsigned long long *dst = X.ring + ((int64_t)(slot_step % D) * GRID_MAX_CTAS + j) * H;
+                    tma_store_1d(dst, stage_out, hl8 * 8);
+                }
             };
             const int32_t n_edge = (hl + 32 * RPT - 1) / (32 * RPT);   // tiles within hl of an edge
             const int32_t bot_end = min(t_end, t_first + n_edge);        // tiles that read the halo
@@ -322,6 +378,7 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
         cur = nxt;
         nxt = tmp;
     }
+    if (warp == nwarps - 1 && lane == 0) tma_store_wait_all();   // last publication has left smem
     __syncthreads();                                   // compute and comm warps leave the frame loop
     step_base += N;
 
@@ -362,6 +419,12 @@ __global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg
     long long *red = reinterpret_cast<long long *>(smem_raw);              // 8 x int64 (+ 8 spare)
     int32_t *bufA = reinterpret_cast<int32_t *>(smem_raw) + 32;
     int32_t *bufB = bufA + TURBO_BIG_MAX_COST + seg_max;
+    unsigned long long *stage_in = reinterpret_cast<unsigned long long *>(bufB + TURBO_BIG_MAX_COST + seg_max);
+    unsigned long long *stage_out = stage_in + TURBO_BIG_MAX_COST;
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(stage_out + TURBO_BIG_MAX_COST);
+    uint32_t mbar_phase = 0;
+    if (threadIdx.x == 0) mbar_init(mbar, 1);
+    __syncthreads();
     int *flags = reinterpret_cast<int *>(P.workspace + P.grid_scratch_offset);
     GridCtx X;
     X.pub = flags;
@@ -372,11 +435,13 @@ __global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg
     for (int64_t w = 0; w < P.num_windows; ++w) {
         if ((int64_t)P.windows[w].budget_bound + 1 <= TURBO_BIG_CELLS) continue;
         if (KSEL != 0) {
-            grid_window<(KSEL > 0 ? KSEL : 2), MODE>(P, grid, w, bufA, bufB, red, X, step_base);
+            grid_window<(KSEL > 0 ? KSEL : 2), MODE>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar,
+                                                     mbar_phase);
         } else {
             switch (P.windows[w].num_exits) {
 #define TURBO_K_CASE(KK) \
-    case KK: grid_window<KK, MODE>(P, grid, w, bufA, bufB, red, X, step_base); break;
+    case KK: grid_window<KK, MODE>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar, mbar_phase); \
+        break;
                 TURBO_K_CASE(2) TURBO_K_CASE(3) TURBO_K_CASE(4) TURBO_K_CASE(5) TURBO_K_CASE(6)
                 TURBO_K_CASE(7) TURBO_K_CASE(8) TURBO_K_CASE(9) TURBO_K_CASE(10) TURBO_K_CASE(11)
                 TURBO_K_CASE(12) TURBO_K_CASE(13) TURBO_K_CASE(14) TURBO_K_CASE(15) TURBO_K_CASE(16)
@@ -414,7 +479,7 @@ cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams 
     int32_t seg = (int32_t)(((int64_t)shape->max_budget + 1 + NP - 1) / NP);
     seg = (seg + 511) & ~511;
     if (seg < TURBO_BIG_MAX_COST) seg = TURBO_BIG_MAX_COST;
-    const size_t smem = 128 + (size_t)8 * (TURBO_BIG_MAX_COST + seg);
+    const size_t smem = 128 + (size_t)8 * (TURBO_BIG_MAX_COST + seg) + (size_t)16 * TURBO_BIG_MAX_COST + 16;
     if (smem > (size_t)smem_per_cta_max) return cudaErrorInvalidConfiguration;
     dp_grid_kernel_t kern = mode == DP_PLAN ? pick_grid<DP_PLAN>(shape->min_exits, shape->max_exits)
                                             : pick_grid<DP_SOLVE_GLOBAL>(shape->min_exits, shape->max_exits);
@@ -442,6 +507,10 @@ cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams 
         }
         tag_base = (int32_t)epoch;
         epoch += span;
+    }
+    {
+        const char *dbg = getenv("TURBO_GRID_DEBUG");      // 1: no halo exchange (timing only)
+        P.debug = dbg ? atoi(dbg) : 0;
     }
     void *args[] = {(void *)&P, (void *)&seg, (void *)&tag_base};
     return cudaLaunchCooperativeKernel((const void *)kern, dim3(NP), dim3(GRID_THREADS), args, smem, stream);

@@ -82,6 +82,7 @@ struct DpParams {
     int32_t max_options;    // option-table entries per window (osm); fused scratch follows it
     int32_t prof_entries;   // fused: staged profile entries (max C*K)
     int64_t grid_scratch_offset;   // long-window kernel: workspace offset of flags + halo ring
+    int32_t debug;                 // long-window kernel tuning switches (TURBO_GRID_DEBUG)
     int64_t *stats;
 };
 
