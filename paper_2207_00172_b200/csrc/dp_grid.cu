@@ -366,12 +366,14 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
                 }
                 named_sync(bar_step, C * 32);
             } else {
+                // publish S_i's top first (the neighbour's critical path), then fetch our halo --
+                // it was published a step ago, so it is normally already in L2
+                named_sync(bar_top, nthr);
+                if (publish) do_publish();
                 if (need_halo) fetch_halo();
                 __threadfence_block();
                 named_arrive(bar_halo, nthr);
                 if (need_halo) release_halo_slot();
-                named_sync(bar_top, nthr);
-                if (publish) do_publish();
             }
         }
         int32_t *tmp = cur;
