@@ -110,7 +110,7 @@ __device__ __forceinline__ void st_release_gpu(int *p, int v)
 // timeout the caller flags the window (status[1]) and carries on, so the kernel always exits.
 __device__ __forceinline__ bool wait_at_least(const int *p, int target)
 {
-    for (long long it = 0; it < (1ll << 26); ++it) {
+    for (long long it = 0; it < (1ll << 22); ++it) {
         if (ld_acquire_gpu(p) >= target) return true;
         __nanosleep(32);
     }
@@ -295,7 +295,7 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
                 const unsigned long long *src =
                     X.ring + ((int64_t)((step_base + f - 1) % D) * GRID_MAX_CTAS + (j - 1)) * H;
                 bool ok = false;
-                for (int attempt = 0; attempt < (1 << 22) && !ok; ++attempt) {
+                for (int attempt = 0; attempt < (1 << 16) && !ok; ++attempt) {
                     if (lane == 0) {
                         tma_load_1d(stage_in, src, hl8 * 8, mbar);
                         mbar_wait(mbar, mbar_phase);
@@ -365,7 +365,7 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
                     named_arrive(bar_top, nthr);
                 }
                 named_sync(bar_step, C * 32);
-            } else {
+            } else if (split) {
                 // publish S_i's top first (the neighbour's critical path), then fetch our halo --
                 // it was published a step ago, so it is normally already in L2
                 named_sync(bar_top, nthr);
@@ -374,6 +374,14 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
                 __threadfence_block();
                 named_arrive(bar_halo, nthr);
                 if (need_halo) release_halo_slot();
+            } else {
+                // short segment: every tile may read the halo, so it must come first
+                if (need_halo) fetch_halo();
+                __threadfence_block();
+                named_arrive(bar_halo, nthr);
+                if (need_halo) release_halo_slot();
+                named_sync(bar_top, nthr);
+                if (publish) do_publish();
             }
         }
         int32_t *tmp = cur;
