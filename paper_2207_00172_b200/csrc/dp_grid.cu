@@ -290,16 +290,17 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
             // ONE bulk load into its own stage (mbarrier completion) and checks the tags -- a stale
             // tag (publication still in flight) just re-issues the copy. No fence, no flag word.
             const int32_t hl8 = (hl + 1) & ~1;                         // 16-byte multiple of 8-B words
-            auto fetch_halo = [&]() {
+            const unsigned long long *halo_src =
+                X.ring + ((int64_t)((step_base + f - 1) % D) * GRID_MAX_CTAS + (j - 1)) * H;
+            auto issue_halo = [&]() {                                 // async: TMA load of the slot
+                if (lane == 0) tma_load_1d(stage_in, halo_src, hl8 * 8, mbar);
+            };
+            auto fetch_halo = [&](bool issued) {
                 const uint32_t tag = (uint32_t)(step_base + f);          // j-1's step f-1 publishes tag sb+f
-                const unsigned long long *src =
-                    X.ring + ((int64_t)((step_base + f - 1) % D) * GRID_MAX_CTAS + (j - 1)) * H;
                 bool ok = false;
                 for (int attempt = 0; attempt < (1 << 16) && !ok; ++attempt) {
-                    if (lane == 0) {
-                        tma_load_1d(stage_in, src, hl8 * 8, mbar);
-                        mbar_wait(mbar, mbar_phase);
-                    }
+                    if (!issued || attempt > 0) issue_halo();
+                    if (lane == 0) mbar_wait(mbar, mbar_phase);
                     mbar_phase ^= 1u;
                     __syncwarp();
                     bool mine_ok = true;
@@ -366,17 +367,18 @@ __device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, 
                 }
                 named_sync(bar_step, C * 32);
             } else if (split) {
-                // publish S_i's top first (the neighbour's critical path), then fetch our halo --
-                // it was published a step ago, so it is normally already in L2
+                // the halo (published a step ago, normally already in L2) is requested at once and
+                // lands while we wait for our top tiles and publish them
+                if (need_halo) issue_halo();
                 named_sync(bar_top, nthr);
                 if (publish) do_publish();
-                if (need_halo) fetch_halo();
+                if (need_halo) fetch_halo(true);
                 __threadfence_block();
                 named_arrive(bar_halo, nthr);
                 if (need_halo) release_halo_slot();
             } else {
                 // short segment: every tile may read the halo, so it must come first
-                if (need_halo) fetch_halo();
+                if (need_halo) fetch_halo(false);
                 __threadfence_block();
                 named_arrive(bar_halo, nthr);
                 if (need_halo) release_halo_slot();
