@@ -90,7 +90,23 @@ typedef struct {
                                     is split over the whole grid (long-window kernel)           */
     int64_t grid_scratch_offset; /* workspace offset of the long-window kernel's halo ring/flags */
     int64_t reserved1[2];
+    /* per row-size class (TURBO_NUM_CLASSES, see below): windows of one class are planned by one
+     * launch shaped for them (warps per window, shared memory, residency) */
+    int32_t cls_count[4];
+    int32_t cls_max_budget[4];
+    int32_t cls_max_frames[4];
+    int32_t cls_max_options[4];
+    int32_t cls_min_exits[4];
+    int32_t cls_max_exits[4];
 } turbo_shape_t;
+
+/* Row-size classes of windows served by one CTA each: class c holds the windows with
+ * budget_bound + 1 <= TURBO_CLASS_CELLS_c cells (and above the previous bound). */
+#define TURBO_NUM_CLASSES 4
+#define TURBO_CLASS_CELLS_0 256
+#define TURBO_CLASS_CELLS_1 1024
+#define TURBO_CLASS_CELLS_2 4608
+#define TURBO_CLASS_CELLS_3 24576
 
 /* Rows longer than this many cells (budget_bound + 1) are planned by the long-window kernel:
  * one cooperative grid of CTAs per window, each CTA owning a contiguous budget segment, with

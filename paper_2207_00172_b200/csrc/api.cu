@@ -111,6 +111,10 @@ turbo_status_t turbo_mckp_workspace(const turbo_profile_t *profiles_host, int32_
     s.num_profiles = num_profiles;
     s.min_exits = MAX_EXITS;
     s.max_exits = 2;
+    for (int c = 0; c < TURBO_NUM_CLASSES; ++c) {
+        s.cls_min_exits[c] = MAX_EXITS;
+        s.cls_max_exits[c] = 2;
+    }
     int64_t opt = 0, ws = 0, frames = 0, cells = 0;
     for (int32_t w = 0; w < num_windows; ++w) {
         turbo_window_t &win = windows_host[w];
@@ -130,10 +134,18 @@ turbo_status_t turbo_mckp_workspace(const turbo_profile_t *profiles_host, int32_
         if (win.num_frames > s.max_frames) s.max_frames = win.num_frames;
         if ((int64_t)win.num_frames * K > s.max_options) s.max_options = win.num_frames * K;
         if (win.budget > s.max_budget) s.max_budget = win.budget;
-        if ((int64_t)win.budget + 1 > TURBO_BIG_CELLS)
+        const int rc = row_class((int64_t)win.budget + 1);
+        if (rc >= TURBO_NUM_CLASSES) {
             s.num_big += 1;
-        else if (win.budget > s.max_budget_small)
-            s.max_budget_small = win.budget;
+        } else {
+            if (win.budget > s.max_budget_small) s.max_budget_small = win.budget;
+            s.cls_count[rc] += 1;
+            if (win.budget > s.cls_max_budget[rc]) s.cls_max_budget[rc] = win.budget;
+            if (win.num_frames > s.cls_max_frames[rc]) s.cls_max_frames[rc] = win.num_frames;
+            if (win.num_frames * K > s.cls_max_options[rc]) s.cls_max_options[rc] = win.num_frames * K;
+            if (K < s.cls_min_exits[rc]) s.cls_min_exits[rc] = K;
+            if (K > s.cls_max_exits[rc]) s.cls_max_exits[rc] = K;
+        }
         if (K < s.min_exits) s.min_exits = K;
         if (K > s.max_exits) s.max_exits = K;
         if (profiles_host[win.profile].num_classes > s.num_classes_max)
@@ -171,19 +183,106 @@ turbo_status_t turbo_profile_lookup(const turbo_shape_t *shape, const turbo_prof
     return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
 }
 
-static turbo_status_t run_dp(const turbo_shape_t *shape, int mode, const turbo_window_t *windows,
-                             const int32_t *opt_gain, const int32_t *opt_cost, void *workspace,
-                             int32_t *best_gain, int32_t *best_cost, uint8_t *feasible, uint8_t *exit_out,
-                             int64_t *status, turbo_stream_t stream)
+// Launch shape of one row-size class: windows outside the class are skipped by the kernel.
+static turbo_shape_t class_shape(const turbo_shape_t *s, int c)
+{
+    turbo_shape_t t = *s;
+    t.max_budget_small = s->cls_max_budget[c];
+    t.max_budget = s->cls_max_budget[c];
+    t.max_frames = s->cls_max_frames[c];
+    t.max_options = s->cls_max_options[c];
+    t.min_exits = s->cls_min_exits[c];
+    t.max_exits = s->cls_max_exits[c];
+    t.num_big = 0;
+    return t;
+}
+
+enum { RUN_PLAN = 0, RUN_SOLVE = 1, RUN_SCHEDULE = 2 };
+
+// Fused-solve variant of one class: choice planes in shared memory when they fit under
+// smem_choice_limit per CTA (or, when forced by the debug hook, under the per-CTA maximum).
+static int solve_mode(const turbo_shape_t *cs)
+{
+    if ((g_variant & 3) == 2) return DP_SOLVE_GLOBAL;
+    DpParams P;
+    std::memset(&P, 0, sizeof(P));
+    dp_smem_words(cs, DP_SOLVE_SMEM, &P);
+    P.pad_words = dp_pad_words(cs);
+    const int64_t bytes = (int64_t)dp_smem_bytes(P, dp_warps_per_window(cs));
+    if ((g_variant & 3) == 1) {
+        DeviceInfo d;
+        if (device_info(&d) == cudaSuccess && bytes <= (int64_t)d.smem_per_cta_optin) return DP_SOLVE_SMEM;
+        return DP_SOLVE_GLOBAL;
+    }
+    return bytes <= (int64_t)smem_choice_limit ? DP_SOLVE_SMEM : DP_SOLVE_GLOBAL;
+}
+
+// Does a fused solve / schedule of this batch write any choice plane to HBM?
+static bool solve_needs_workspace(const turbo_shape_t *s)
+{
+    if (s->num_big > 0) return true;
+    for (int c = 0; c < TURBO_NUM_CLASSES; ++c) {
+        if (!s->cls_count[c]) continue;
+        const turbo_shape_t cs = class_shape(s, c);
+        if (solve_mode(&cs) == DP_SOLVE_GLOBAL) return true;
+    }
+    return false;
+}
+
+// One launch per non-empty row-size class (then the grid kernel for long windows).
+static turbo_status_t run_dp(const turbo_shape_t *shape, int kind, const DpParams &base, turbo_stream_t stream)
 {
     DeviceInfo d;
     if (device_info(&d) != cudaSuccess) return TURBO_ERR_CUDA;
+    if (kind == RUN_SCHEDULE && shape->num_big > 0) return TURBO_ERR_UNSUPPORTED;
+    DpParams Ps[TURBO_NUM_CLASSES];
+    turbo_shape_t shapes[TURBO_NUM_CLASSES];
+    int modes[TURBO_NUM_CLASSES];
+    for (int c = 0; c < TURBO_NUM_CLASSES; ++c) {          // validate every class before launching
+        if (!shape->cls_count[c]) continue;
+        shapes[c] = class_shape(shape, c);
+        modes[c] = kind == RUN_PLAN ? DP_PLAN : solve_mode(&shapes[c]);
+        DpParams &P = Ps[c];
+        P = base;
+        dp_smem_words(&shapes[c], modes[c], &P);
+        P.warp_words = 0;
+        P.pad_words = dp_pad_words(&shapes[c]);
+        if (kind == RUN_SCHEDULE) {
+            if (!P.osm) return TURBO_ERR_UNSUPPORTED;      // option table must be staged in smem
+            // fused scratch after the option table: profile (C*K int2), class ids and exits (N B each)
+            P.prof_entries = shapes[c].num_classes_max * shapes[c].max_exits;
+            P.cst_words += 2 * P.prof_entries + 2 * ((shapes[c].max_frames + 3) / 4);
+        }
+        P.cls = c;
+        P.cls_count = shape->cls_count[c];
+        if (dp_smem_bytes(P, dp_warps_per_window(&shapes[c])) > (size_t)d.smem_per_cta_optin)
+            return TURBO_ERR_UNSUPPORTED;
+    }
+    DpLaunch info;
+    cudaError_t e = cudaSuccess;
+    for (int c = 0; c < TURBO_NUM_CLASSES && e == cudaSuccess; ++c)
+        if (shape->cls_count[c])
+            e = launch_dp(&shapes[c], modes[c], Ps[c], d.num_sms, d.smem_per_sm, d.smem_per_cta_optin,
+                          (cudaStream_t)stream, &info);
+    if (e == cudaSuccess && shape->num_big > 0) {          // long windows: the whole grid per window
+        DpParams P = base;
+        P.grid_scratch_offset = shape->grid_scratch_offset;
+        e = launch_dp_grid(shape, kind == RUN_PLAN ? DP_PLAN : DP_SOLVE_GLOBAL, P, d.num_sms, d.smem_per_cta_optin,
+                           (cudaStream_t)stream);
+    }
+    if (e == cudaErrorInvalidConfiguration || e == cudaErrorCooperativeLaunchTooLarge) {
+        cudaGetLastError();
+        return TURBO_ERR_UNSUPPORTED;
+    }
+    return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
+}
+
+static DpParams base_params(const turbo_shape_t *shape, const turbo_window_t *windows, const int32_t *opt_gain,
+                            const int32_t *opt_cost, void *workspace, int32_t *best_gain, int32_t *best_cost,
+                            uint8_t *feasible, uint8_t *exit_out, int64_t *status)
+{
     DpParams P;
     std::memset(&P, 0, sizeof(P));
-    dp_smem_words(shape, mode, &P);
-    P.warp_words = 0;
-    P.pad_words = dp_pad_words(shape);
-    if (dp_smem_bytes(P, dp_warps_per_window(shape)) > (size_t)d.smem_per_cta_optin) return TURBO_ERR_UNSUPPORTED;
     P.windows = windows;
     P.num_windows = shape->num_windows;
     P.opt_gain = opt_gain;
@@ -195,18 +294,8 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int mode, const turbo_w
     P.exit_out = exit_out;
     P.status = status;
     P.grid_scratch_offset = shape->grid_scratch_offset;
-    DpLaunch info;
-    cudaError_t e = cudaSuccess;
-    if (shape->num_big < shape->num_windows)          // windows served by one CTA each
-        e = launch_dp(shape, mode, P, d.num_sms, d.smem_per_sm, d.smem_per_cta_optin, (cudaStream_t)stream, &info);
-    if (e == cudaSuccess && shape->num_big > 0)        // long windows: the whole grid per window
-        e = launch_dp_grid(shape, mode == DP_PLAN ? DP_PLAN : DP_SOLVE_GLOBAL, P, d.num_sms, d.smem_per_cta_optin,
-                           (cudaStream_t)stream);
-    if (e == cudaErrorInvalidConfiguration || e == cudaErrorCooperativeLaunchTooLarge) {
-        cudaGetLastError();
-        return TURBO_ERR_UNSUPPORTED;
-    }
-    return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
+    P.cls = -1;
+    return P;
 }
 
 turbo_status_t turbo_mckp_plan(const turbo_shape_t *shape, const turbo_window_t *windows, const int32_t *opt_gain,
@@ -220,8 +309,10 @@ turbo_status_t turbo_mckp_plan(const turbo_shape_t *shape, const turbo_window_t 
     if (shape->total_options > 0 && (!opt_gain || !opt_cost)) return TURBO_ERR_INVALID_ARG;
     if ((int64_t)workspace_bytes < shape->workspace_bytes || (shape->workspace_bytes > 0 && !workspace))
         return TURBO_ERR_WORKSPACE;
-    return run_dp(shape, DP_PLAN, windows, opt_gain, opt_cost, workspace, best_gain, best_cost, feasible, nullptr,
-                  status, stream);
+    return run_dp(shape, RUN_PLAN,
+                  base_params(shape, windows, opt_gain, opt_cost, workspace, best_gain, best_cost, feasible, nullptr,
+                              status),
+                  stream);
 }
 
 turbo_status_t turbo_backtrack(const turbo_shape_t *shape, const turbo_window_t *windows, const int32_t *opt_cost,
@@ -243,28 +334,10 @@ turbo_status_t turbo_backtrack(const turbo_shape_t *shape, const turbo_window_t 
     return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
 }
 
-// Fused-solve variant: choice planes in shared memory when one warp's planes fit under
-// smem_choice_limit (or, when forced by the debug hook, under the per-CTA maximum).
-static int solve_mode(const turbo_shape_t *shape)
-{
-    if ((g_variant & 3) == 2) return DP_SOLVE_GLOBAL;
-    DpParams P;
-    std::memset(&P, 0, sizeof(P));
-    dp_smem_words(shape, DP_SOLVE_SMEM, &P);
-    P.pad_words = dp_pad_words(shape);
-    const int64_t bytes = (int64_t)dp_smem_bytes(P, dp_warps_per_window(shape));
-    if ((g_variant & 3) == 1) {
-        DeviceInfo d;
-        if (device_info(&d) == cudaSuccess && bytes <= (int64_t)d.smem_per_cta_optin) return DP_SOLVE_SMEM;
-        return DP_SOLVE_GLOBAL;
-    }
-    return bytes <= (int64_t)smem_choice_limit ? DP_SOLVE_SMEM : DP_SOLVE_GLOBAL;
-}
-
 turbo_status_t turbo_mckp_solve_workspace(const turbo_shape_t *shape, size_t *bytes)
 {
     if (!shape || !bytes) return TURBO_ERR_INVALID_ARG;
-    *bytes = (solve_mode(shape) == DP_SOLVE_SMEM && shape->num_big == 0) ? 0 : (size_t)shape->workspace_bytes;
+    *bytes = solve_needs_workspace(shape) ? (size_t)shape->workspace_bytes : 0;
     return TURBO_OK;
 }
 
@@ -278,12 +351,13 @@ turbo_status_t turbo_mckp_solve(const turbo_shape_t *shape, const turbo_window_t
     if (!windows || !best_gain || !best_cost || !feasible || !status) return TURBO_ERR_INVALID_ARG;
     if (shape->total_frames > 0 && !exit_out) return TURBO_ERR_INVALID_ARG;
     if (shape->total_options > 0 && (!opt_gain || !opt_cost)) return TURBO_ERR_INVALID_ARG;
-    const int mode = solve_mode(shape);
-    if ((mode == DP_SOLVE_GLOBAL || shape->num_big > 0) &&
+    if (solve_needs_workspace(shape) &&
         ((int64_t)workspace_bytes < shape->workspace_bytes || (shape->workspace_bytes > 0 && !workspace)))
         return TURBO_ERR_WORKSPACE;
-    return run_dp(shape, mode, windows, opt_gain, opt_cost, workspace, best_gain, best_cost, feasible, exit_out,
-                  status, stream);
+    return run_dp(shape, RUN_SOLVE,
+                  base_params(shape, windows, opt_gain, opt_cost, workspace, best_gain, best_cost, feasible, exit_out,
+                              status),
+                  stream);
 }
 
 turbo_status_t turbo_schedule(const turbo_shape_t *shape, const turbo_profile_t *profiles, turbo_window_t *windows,
@@ -296,40 +370,19 @@ turbo_status_t turbo_schedule(const turbo_shape_t *shape, const turbo_profile_t 
     if (!profiles || !windows || !best_gain || !best_cost || !feasible || !stats || !status || base_cost < 0)
         return TURBO_ERR_INVALID_ARG;
     if (shape->total_frames > 0 && (!class_id || !exit_out)) return TURBO_ERR_INVALID_ARG;
-    const int mode = solve_mode(shape);
-    if (mode == DP_SOLVE_GLOBAL &&
+    if (solve_needs_workspace(shape) &&
         ((int64_t)workspace_bytes < shape->workspace_bytes || (shape->workspace_bytes > 0 && !workspace)))
         return TURBO_ERR_WORKSPACE;
-    DeviceInfo d;
-    if (device_info(&d) != cudaSuccess) return TURBO_ERR_CUDA;
-    DpParams P;
-    std::memset(&P, 0, sizeof(P));
-    dp_smem_words(shape, mode, &P);
-    if (!P.osm) return TURBO_ERR_UNSUPPORTED;         // option table must be staged in smem
-    // fused scratch after the option table: the profile (C*K int2) and the class ids (N bytes)
-    P.prof_entries = shape->num_classes_max * shape->max_exits;
-    P.cst_words += 2 * P.prof_entries + 2 * ((shape->max_frames + 3) / 4);   // + class ids + exits
-    P.pad_words = dp_pad_words(shape);
-    if (dp_smem_bytes(P, dp_warps_per_window(shape)) > (size_t)d.smem_per_cta_optin) return TURBO_ERR_UNSUPPORTED;
-    P.windows = windows;
+    DpParams P = base_params(shape, windows, nullptr, nullptr, workspace, best_gain, best_cost, feasible, exit_out,
+                             status);
     P.windows_rw = windows;
-    P.num_windows = shape->num_windows;
-    P.workspace = reinterpret_cast<uint8_t *>(workspace);
-    P.best_gain = best_gain;
-    P.best_cost = best_cost;
-    P.feasible = feasible;
-    P.exit_out = exit_out;
-    P.status = status;
     P.profiles = profiles;
     P.class_id = class_id;
     P.capacity = capacity;
     P.base_cost = base_cost;
     P.fuse = 1;
     P.stats = stats;
-    DpLaunch info;
-    cudaError_t e = launch_dp(shape, mode, P, d.num_sms, d.smem_per_sm, d.smem_per_cta_optin, (cudaStream_t)stream,
-                              &info);
-    return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
+    return run_dp(shape, RUN_SCHEDULE, P, stream);
 }
 
 turbo_status_t turbo_stats(const turbo_shape_t *shape, const turbo_window_t *windows, const uint8_t *class_id,

@@ -528,7 +528,8 @@ __global__ void __launch_bounds__(256, 4) dp_cta_kernel(DpParams P)
     }
     __syncthreads();
     for (int64_t w = blockIdx.x; w < P.num_windows; w += gridDim.x) {
-        if ((int64_t)P.windows[w].budget_bound + 1 > TURBO_BIG_CELLS) continue;   // long-window kernel
+        const int rc = row_class((int64_t)P.windows[w].budget_bound + 1);
+        if (rc >= TURBO_NUM_CLASSES || (P.cls >= 0 && rc != P.cls)) continue;   // other launch serves it
         if (KSEL != 0) {
             dp_window<(KSEL > 0 ? KSEL : 2), MODE, OSM, FUSE>(P, w, rowA, rowB, sch, cst, opt_s, red, hist, warp, nwarps,
                                                              lane);

@@ -115,7 +115,8 @@ cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P0, 
     static std::map<std::tuple<int, const void *, int, size_t, int64_t>, size_t> cache;
     int dev = 0;
     cudaGetDevice(&dev);
-    const auto ckey = std::make_tuple(dev, (const void *)kern, G, need, W);
+    const int64_t Wc = P.cls_count > 0 ? P.cls_count : W;   // windows this launch plans
+    const auto ckey = std::make_tuple(dev, (const void *)kern, G, need, Wc);
     size_t smem = need;
     bool cached = false;
     {
@@ -132,7 +133,7 @@ cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P0, 
         if (e != cudaSuccess) return e;
         if (s_max < 1) return cudaErrorInvalidConfiguration;
     }
-    const int s = cached ? 0 : pick_concurrency(W, num_sms, s_max);
+    const int s = cached ? 0 : pick_concurrency(Wc, num_sms, s_max);
     // pad the dynamic smem so that exactly s CTAs fit per SM (occupancy as a knob)
     if (!cached && s < s_max) {
         size_t hi = dyn_max, lo = need;                       // largest smem with occupancy >= s

@@ -27,6 +27,13 @@ constexpr int MAX_EXITS = 16;
 __host__ __device__ __forceinline__ int choice_bits(int K) { return K <= 4 ? 2 : 4; }
 // rows of 32 cells per choice word (= per tile): 16 for 2-bit, 8 for 4-bit choices
 __host__ __device__ __forceinline__ int rows_per_tile(int K) { return 32 / choice_bits(K); }
+// row-size class of a window with `cells` = budget_bound + 1 (TURBO_NUM_CLASSES = long window)
+__host__ __device__ __forceinline__ int row_class(int64_t cells)
+{
+    return cells <= TURBO_CLASS_CELLS_0 ? 0 : cells <= TURBO_CLASS_CELLS_1 ? 1 : cells <= TURBO_CLASS_CELLS_2 ? 2
+         : cells <= TURBO_CLASS_CELLS_3 ? 3 : TURBO_NUM_CLASSES;
+}
+
 __host__ __device__ __forceinline__ int64_t num_rows(int64_t B) { return (B + 1 + 31) / 32; }
 __host__ __device__ __forceinline__ int64_t num_tiles(int64_t B, int K) {
     int64_t rpt = rows_per_tile(K);
@@ -83,6 +90,8 @@ struct DpParams {
     int32_t prof_entries;   // fused: staged profile entries (max C*K)
     int64_t grid_scratch_offset;   // long-window kernel: workspace offset of flags + halo ring
     int32_t debug;                 // long-window kernel tuning switches (TURBO_GRID_DEBUG)
+    int32_t cls;                   // row-size class served by this launch (-1: every window)
+    int32_t cls_count;             // windows in that class (residency / wave planning)
     int64_t *stats;
 };
 

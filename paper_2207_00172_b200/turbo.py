@@ -49,7 +49,10 @@ class Shape(ctypes.Structure):
                 ("total_frames", ctypes.c_int64), ("total_options", ctypes.c_int64),
                 ("total_cells", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
                 ("max_budget_small", ctypes.c_int32), ("num_big", ctypes.c_int32),
-                ("grid_scratch_offset", ctypes.c_int64), ("reserved1", ctypes.c_int64 * 2)]
+                ("grid_scratch_offset", ctypes.c_int64), ("reserved1", ctypes.c_int64 * 2),
+                ("cls_count", ctypes.c_int32 * 4), ("cls_max_budget", ctypes.c_int32 * 4),
+                ("cls_max_frames", ctypes.c_int32 * 4), ("cls_max_options", ctypes.c_int32 * 4),
+                ("cls_min_exits", ctypes.c_int32 * 4), ("cls_max_exits", ctypes.c_int32 * 4)]
 
 
 assert ctypes.sizeof(Window) == 48

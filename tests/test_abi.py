@@ -43,7 +43,7 @@ def test_abi_version_and_strings(tb):
 def test_struct_sizes(tb):
     assert ctypes.sizeof(tb.Window) == 48
     assert ctypes.sizeof(tb.Profile) == 24
-    assert ctypes.sizeof(tb.Shape) == 96
+    assert ctypes.sizeof(tb.Shape) == 192
 
 
 def _profiles(tb, Ks, C=10):
