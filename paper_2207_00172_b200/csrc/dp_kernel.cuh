@@ -506,7 +506,9 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
 // [choice planes (solve smem)]. The pads (pad_words of -inf below each row buffer) are written
 // once and never overwritten.
 template <int KSEL, int MODE, bool OSM, bool FUSE>
-__global__ void __launch_bounds__(256, 4) dp_cta_kernel(DpParams P)
+// Register budget: 64 for fixed-K kernels (4 CTAs x 256 threads or 2 x 512 per SM); the
+// mixed-K kernel inlines every K and gets 128 to avoid spilling its hot loop.
+__global__ void __launch_bounds__(512, (KSEL == 0) ? 1 : 2) dp_cta_kernel(DpParams P)
 {
     extern __shared__ int4 smem_raw[];
     const int lane = threadIdx.x & 31;

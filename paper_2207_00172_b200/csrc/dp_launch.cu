@@ -40,8 +40,9 @@ int dp_warps_per_window(const turbo_shape_t *s)
         const char *e = getenv("TURBO_DP_WARPS");          // tuning override (1, 2, 4, 8)
         forced = e ? atoi(e) : 0;
     }
-    if (forced > 0 && tiles > 1) return forced > 8 ? 8 : forced;
+    if (forced > 0 && tiles > 1) return forced > 16 ? 16 : forced;
     if (tiles <= 1) return 1;
+    if (tiles >= 32) return 16;      // long rows: more warps per SM to hide LDS/barrier latency
     return tiles >= 8 ? 8 : (int)tiles;
 }
 
