@@ -51,7 +51,12 @@ static void dp_smem_words(const turbo_shape_t *s, int mode, DpParams *P)
     const int64_t chs = mode == DP_SOLVE_SMEM ? (int64_t)s->max_frames * tiles * 32 : 0;
     P->chs_words = (int32_t)(chs > INT32_MAX ? INT32_MAX : chs);
     const int64_t opts = s->max_options;
-    P->osm = (opts * 8 <= OSM_LIMIT_BYTES && !(g_variant & 4)) ? 1 : 0;
+    // stage the option table only when it is small next to the row(s) it feeds: for short rows
+    // the table would dominate shared memory and cap residency; those windows broadcast options
+    // from registers (shuffles) instead
+    const int64_t row_bytes = (int64_t)P->row_words * 4 * (dp_warps_per_window(s) > 1 ? 2 : 1);
+    P->osm = (opts * 8 <= OSM_LIMIT_BYTES && opts * 8 <= (row_bytes > 4096 ? row_bytes : 4096) &&
+              !(g_variant & 4)) ? 1 : 0;
     P->cst_words = P->osm ? (int32_t)(2 * opts) : (mode == DP_PLAN ? 0 : (int32_t)((int64_t)s->max_frames * s->max_exits));
     P->max_options = (int32_t)opts;
 }
@@ -247,8 +252,7 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int kind, const DpParam
         dp_smem_words(&shapes[c], modes[c], &P);
         P.warp_words = 0;
         P.pad_words = dp_pad_words(&shapes[c]);
-        if (kind == RUN_SCHEDULE) {
-            if (!P.osm) return TURBO_ERR_UNSUPPORTED;      // option table must be staged in smem
+        if (kind == RUN_SCHEDULE && P.osm) {
             // fused scratch after the option table: profile (C*K int2), class ids and exits (N B each)
             P.prof_entries = shapes[c].num_classes_max * shapes[c].max_exits;
             P.cst_words += 2 * P.prof_entries + 2 * ((shapes[c].max_frames + 3) / 4);

@@ -148,7 +148,7 @@ struct GridCtx {
 };
 
 template <int K, int MODE>
-__device__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, int32_t *bufA, int32_t *bufB,
+__device__ __noinline__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, int32_t *bufA, int32_t *bufB,
                            long long *red, GridCtx X, int &step_base, unsigned long long *stage_in,
                            unsigned long long *stage_out, uint64_t *mbar, uint32_t &mbar_phase)
 {

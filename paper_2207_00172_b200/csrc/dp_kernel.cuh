@@ -280,6 +280,28 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
 
     const int32_t *__restrict__ og = P.opt_gain + fo;
     const int32_t *__restrict__ oc = P.opt_cost + fo;
+    // option (g, c) of frame i, exit k straight from global memory: the option table (lookup
+    // path) or, fused, the profile row of the frame's class (a zero row for a class >= C)
+    const turbo_profile_t *prof = FUSE ? P.profiles + win->profile : nullptr;
+    auto load_opt = [&](int32_t i, int32_t k, int32_t &g, int32_t &c) {
+        if (FUSE) {
+            const int32_t cls = P.class_id[ff + i];
+            if (cls < prof->num_classes) {
+                g = __ldg(prof->gain + cls * K + k);
+                c = __ldg(prof->cost + cls * K + k);
+            } else {
+                g = 0;
+                c = 0;
+            }
+        } else {
+            g = __ldg(og + (int64_t)i * K + k);
+            c = __ldg(oc + (int64_t)i * K + k);
+        }
+    };
+    auto class_of = [&](int32_t i) -> uint32_t {               // fused statistics only
+        return OSM ? reinterpret_cast<const uint8_t *>(opt_s + P.max_options + P.prof_entries)[i]
+                   : (uint32_t)P.class_id[ff + i];
+    };
 
     if (FUSE) {
         // a1 (reading R3): B_w = max(0, capacity_w - m_w * u0)
@@ -349,9 +371,10 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
                     g = v.x >> 4;
                     c = v.y;
                 } else {
-                    g = __ldg(og + (int64_t)i * K + k);
-                    c = __ldg(oc + (int64_t)i * K + k);
+                    load_opt(i, k, g, c);
                     bad |= (c < 0) || (c >= (1 << 30)) || (g > (1 << 24)) || (g < -(1 << 24));
+                    if (FUSE && k == 0 && (int32_t)P.class_id[ff + i] >= prof->num_classes)
+                        atomic_min_i64(&P.status[0], ff + i);
                 }
                 const int32_t a = g < 0 ? -g : g;
                 m = a > m ? a : m;
@@ -390,8 +413,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
         if (FUSE) {
             if (tid == 0)
                 for (int32_t i = 0; i < N; ++i) {
-                    const uint32_t cls =
-                        reinterpret_cast<const uint8_t *>(opt_s + P.max_options + P.prof_entries)[i];
+                    const uint32_t cls = class_of(i);
                     hist[0] += 1;
                     if (cls < 10) hist[16 + cls * 16] += 1;
                 }
@@ -407,8 +429,10 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
 
     int32_t my_gp = 0, my_c = 0;                          // !OSM: option `lane` of the current frame
     if (!OSM && N > 0 && lane < K) {
-        my_gp = (__ldg(og + (int64_t)(N - 1) * K + lane) << 4) | (15 - lane);
-        my_c = __ldg(oc + (int64_t)(N - 1) * K + lane);
+        int32_t g, c;
+        load_opt(N - 1, lane, g, c);
+        my_gp = (g << 4) | (15 - lane);
+        my_c = c;
     }
     int32_t *__restrict__ cur = rowA;
     int32_t *__restrict__ nxt = inplace ? rowA : rowB;
@@ -436,8 +460,10 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
             }
             if (MODE != DP_PLAN && warp == 0 && lane < K) cst[i * K + lane] = my_c;
             if (i > 0 && lane < K) {                      // prefetch frame i-1
-                my_gp = (__ldg(og + (int64_t)(i - 1) * K + lane) << 4) | (15 - lane);
-                my_c = __ldg(oc + (int64_t)(i - 1) * K + lane);
+                int32_t g, c;
+                load_opt(i - 1, lane, g, c);
+                my_gp = (g << 4) | (15 - lane);
+                my_c = c;
             }
         }
         int32_t cmax = cc[0];
@@ -477,29 +503,38 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     if (MODE == DP_PLAN) return;
 
     // ---- a5 fused: forward backtrack from (frame 0, b = C*)
-    uint8_t *exit_s = nullptr;
-    if (FUSE)
+    uint8_t *exit_s = nullptr;                            // fused + staged options: exits in smem
+    if (FUSE && OSM)
         exit_s = reinterpret_cast<uint8_t *>(opt_s + P.max_options + P.prof_entries) + ((N + 3) & ~3);
     if (!feas) {
         for (int32_t i = tid; i < N; i += nthr) {
             P.exit_out[ff + i] = 0;
-            if (FUSE) exit_s[i] = 0;
+            if (exit_s) exit_s[i] = 0;
         }
     } else if (warp == 0) {
         backtrack_warp<K, MODE, OSM>(N, Cst, sch, gch, ntiles, gtiles, opt_s, cst, P.exit_out + ff, exit_s, lane);
     }
     if (FUSE) {                                           // a6: CTA-private histograms
         if (nwarps > 1) __syncthreads(); else __syncwarp();
-        const uint8_t *cls_s = reinterpret_cast<const uint8_t *>(opt_s + P.max_options + P.prof_entries);
         for (int32_t i = tid; i < N; i += nthr) {
-            const uint32_t k = exit_s[i];
-            const uint32_t cls = cls_s[i];
+            const uint32_t k = exit_s ? exit_s[i] : P.exit_out[ff + i];   // global: visible after the barrier
+            const uint32_t cls = class_of(i);
             atomicAdd(&hist[k], 1u);
             if (cls < 10) atomicAdd(&hist[16 + cls * 16 + k], 1u);
         }
         if (nwarps > 1) __syncthreads(); else __syncwarp();
         flush_window_stats(P, hist, G, Cst, feas, N, tid, nthr);
     }
+}
+
+// Out-of-line instance per K for the mixed-K kernel: keeps that kernel a small switch over
+// separately compiled bodies (compile time, register allocation per K).
+template <int K, int MODE, bool OSM, bool FUSE>
+__device__ __noinline__ void dp_window_call(const DpParams &P, int64_t w, int32_t *rowA, int32_t *rowB,
+                                            uint32_t *sch, int32_t *cst, int2 *opt_s, int64_t *red, uint32_t *hist,
+                                            int warp, int nwarps, int lane)
+{
+    dp_window<K, MODE, OSM, FUSE>(P, w, rowA, rowB, sch, cst, opt_s, red, hist, warp, nwarps, lane);
 }
 
 // smem layout per CTA: [red: 8 x int64][pad][rowA][pad][rowB (G > 1)][options (OSM) | costs]
@@ -538,7 +573,8 @@ __global__ void __launch_bounds__(512, (KSEL == 0) ? 1 : 2) dp_cta_kernel(DpPara
         } else {
             switch (P.windows[w].num_exits) {
 #define TURBO_K_CASE(KK) \
-    case KK: dp_window<KK, MODE, OSM, FUSE>(P, w, rowA, rowB, sch, cst, opt_s, red, hist, warp, nwarps, lane); break;
+    case KK: dp_window_call<KK, MODE, OSM, FUSE>(P, w, rowA, rowB, sch, cst, opt_s, red, hist, warp, nwarps, lane); \
+        break;
                 TURBO_K_CASE(2) TURBO_K_CASE(3) TURBO_K_CASE(4) TURBO_K_CASE(5) TURBO_K_CASE(6)
                 TURBO_K_CASE(7) TURBO_K_CASE(8) TURBO_K_CASE(9) TURBO_K_CASE(10) TURBO_K_CASE(11)
                 TURBO_K_CASE(12) TURBO_K_CASE(13) TURBO_K_CASE(14) TURBO_K_CASE(15) TURBO_K_CASE(16)
@@ -552,17 +588,18 @@ __global__ void __launch_bounds__(512, (KSEL == 0) ? 1 : 2) dp_cta_kernel(DpPara
 
 typedef void (*dp_kernel_t)(DpParams);
 
+// Fixed-K specialisations for the exit counts of the paper-shaped workloads (beta = 3..7,
+// PAPER.md:533 "4-5" levels, :919 beta = 5); any other K, and batches mixing K, run the
+// mixed-K kernel (every K inlined behind a switch).
 template <int MODE, bool OSM, bool FUSE = false>
 dp_kernel_t pick_dp_kernel(int kmin, int kmax)
 {
     if (kmin != kmax) return dp_cta_kernel<0, MODE, OSM, FUSE>;
     switch (kmin) {
-#define TURBO_K_PICK(KK) \
-    case KK: return dp_cta_kernel<KK, MODE, OSM, FUSE>;
-        TURBO_K_PICK(2) TURBO_K_PICK(3) TURBO_K_PICK(4) TURBO_K_PICK(5) TURBO_K_PICK(6)
-        TURBO_K_PICK(7) TURBO_K_PICK(8) TURBO_K_PICK(9) TURBO_K_PICK(10) TURBO_K_PICK(11)
-        TURBO_K_PICK(12) TURBO_K_PICK(13) TURBO_K_PICK(14) TURBO_K_PICK(15) TURBO_K_PICK(16)
-#undef TURBO_K_PICK
+        case 4: return dp_cta_kernel<4, MODE, OSM, FUSE>;
+        case 5: return dp_cta_kernel<5, MODE, OSM, FUSE>;
+        case 6: return dp_cta_kernel<6, MODE, OSM, FUSE>;
+        case 8: return dp_cta_kernel<8, MODE, OSM, FUSE>;
         default: return dp_cta_kernel<0, MODE, OSM, FUSE>;
     }
 }
@@ -570,6 +607,6 @@ dp_kernel_t pick_dp_kernel(int kmin, int kmax)
 dp_kernel_t dp_kernel_plan(int kmin, int kmax, bool osm);
 dp_kernel_t dp_kernel_solve_smem(int kmin, int kmax, bool osm);
 dp_kernel_t dp_kernel_solve_global(int kmin, int kmax, bool osm);
-dp_kernel_t dp_kernel_schedule(int kmin, int kmax, int mode);
+dp_kernel_t dp_kernel_schedule(int kmin, int kmax, int mode, bool osm);
 
 }  // namespace turbo

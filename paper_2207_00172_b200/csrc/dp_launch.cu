@@ -86,7 +86,7 @@ cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P0, 
     const size_t need = dp_smem_bytes(P, G);
 
     const bool osm = P.osm != 0;
-    dp_kernel_t kern = P.fuse                  ? dp_kernel_schedule(shape->min_exits, shape->max_exits, mode)
+    dp_kernel_t kern = P.fuse                  ? dp_kernel_schedule(shape->min_exits, shape->max_exits, mode, osm)
                        : mode == DP_PLAN         ? dp_kernel_plan(shape->min_exits, shape->max_exits, osm)
                        : mode == DP_SOLVE_SMEM ? dp_kernel_solve_smem(shape->min_exits, shape->max_exits, osm)
                                                : dp_kernel_solve_global(shape->min_exits, shape->max_exits, osm);
@@ -162,4 +162,16 @@ cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P0, 
     return cudaGetLastError();
 }
 
+}  // namespace turbo
+
+namespace turbo {
+dp_kernel_t dp_kernel_sched_smem_osm(int kmin, int kmax);
+dp_kernel_t dp_kernel_sched_smem_reg(int kmin, int kmax);
+dp_kernel_t dp_kernel_sched_global_osm(int kmin, int kmax);
+dp_kernel_t dp_kernel_sched_global_reg(int kmin, int kmax);
+dp_kernel_t dp_kernel_schedule(int kmin, int kmax, int mode, bool osm)
+{
+    if (mode == DP_SOLVE_SMEM) return osm ? dp_kernel_sched_smem_osm(kmin, kmax) : dp_kernel_sched_smem_reg(kmin, kmax);
+    return osm ? dp_kernel_sched_global_osm(kmin, kmax) : dp_kernel_sched_global_reg(kmin, kmax);
+}
 }  // namespace turbo

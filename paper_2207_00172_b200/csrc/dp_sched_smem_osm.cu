@@ -1,0 +1,7 @@
+// dp_sched_smem_osm.cu -- fused a1..a6 kernels (turbo_schedule): choice planes in smem,
+// options osm (split per file for parallel builds).
+#include "dp_kernel.cuh"
+
+namespace turbo {
+dp_kernel_t dp_kernel_sched_smem_osm(int kmin, int kmax) { return pick_dp_kernel<DP_SOLVE_SMEM, true, true>(kmin, kmax); }
+}  // namespace turbo
