@@ -57,7 +57,7 @@ static void dp_smem_words(const turbo_shape_t *s, int mode, DpParams *P)
     const int64_t row_bytes = (int64_t)P->row_words * 4 * (dp_warps_per_window(s) > 1 ? 2 : 1);
     P->osm = (opts * 8 <= OSM_LIMIT_BYTES && opts * 8 <= (row_bytes > 4096 ? row_bytes : 4096) &&
               !(g_variant & 4)) ? 1 : 0;
-    P->cst_words = P->osm ? (int32_t)(2 * opts) : (mode == DP_PLAN ? 0 : (int32_t)((int64_t)s->max_frames * s->max_exits));
+    P->cst_words = P->osm ? (int32_t)(2 * opts) : 0;   // words after the rows: the staged option table
     P->max_options = (int32_t)opts;
 }
 
@@ -69,7 +69,9 @@ static int32_t dp_pad_words(const turbo_shape_t *s)
     return (int32_t)(row < 256 ? row : 256);
 }
 
-static size_t smem_choice_limit = 64 * 1024;   // per-CTA bytes above which choices go to HBM
+// fused solve keeps choice planes in shared memory when they are at most this many bytes or
+// twice the row(s): otherwise they would cap the CTAs resident per SM (and HBM/L2 is fine)
+static int64_t smem_choice_floor = 16 * 1024;
 
 }  // namespace turbo
 
@@ -205,7 +207,7 @@ static turbo_shape_t class_shape(const turbo_shape_t *s, int c)
 enum { RUN_PLAN = 0, RUN_SOLVE = 1, RUN_SCHEDULE = 2 };
 
 // Fused-solve variant of one class: choice planes in shared memory when they fit under
-// smem_choice_limit per CTA (or, when forced by the debug hook, under the per-CTA maximum).
+// smem_choice_floor bytes or twice the rows (or, forced by the debug hook, up to the per-CTA max).
 static int solve_mode(const turbo_shape_t *cs)
 {
     if ((g_variant & 3) == 2) return DP_SOLVE_GLOBAL;
@@ -219,7 +221,9 @@ static int solve_mode(const turbo_shape_t *cs)
         if (device_info(&d) == cudaSuccess && bytes <= (int64_t)d.smem_per_cta_optin) return DP_SOLVE_SMEM;
         return DP_SOLVE_GLOBAL;
     }
-    return bytes <= (int64_t)smem_choice_limit ? DP_SOLVE_SMEM : DP_SOLVE_GLOBAL;
+    const int64_t planes = (int64_t)P.chs_words * 4;
+    const int64_t rows = bytes - planes;
+    return (planes <= smem_choice_floor || planes <= 2 * rows) ? DP_SOLVE_SMEM : DP_SOLVE_GLOBAL;
 }
 
 // Does a fused solve / schedule of this batch write any choice plane to HBM?

@@ -418,8 +418,8 @@ __device__ __noinline__ void grid_window(const DpParams &P, cg::grid_group &grid
     if (!feas) {
         for (int32_t i = j * nthr + tid; i < N; i += NP * nthr) P.exit_out[ff + i] = 0;
     } else if (j == 0 && warp == 0) {
-        backtrack_warp<K, DP_SOLVE_GLOBAL, false>(N, Cst, nullptr, gch, 0, gtiles, nullptr, oc, P.exit_out + ff,
-                                                  nullptr, lane);
+        auto cost = [&](int32_t i, int32_t k) -> int32_t { return __ldg(oc + (int64_t)i * K + k); };
+        backtrack_warp<K, DP_SOLVE_GLOBAL>(N, Cst, nullptr, gch, 0, gtiles, cost, P.exit_out + ff, nullptr, lane);
     }
 }
 

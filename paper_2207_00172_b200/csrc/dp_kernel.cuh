@@ -167,11 +167,11 @@ __device__ __forceinline__ void dp_tile(const DpParams &P, int32_t t, int32_t i,
 // choice at b, lane 1 + a reads frame i+1's at b - c_{i,a} and (D = 3, when 1 + K + K^2 <= 32)
 // lane 1 + K + a K + a' reads frame i+2's at b - c_{i,a} - c_{i+1,a'}; shuffles then pick the
 // realised branch. Lane 0 writes the exits (global, and shared when exit_s != nullptr).
-template <int K, int MODE, bool OSM>
+template <int K, int MODE, class CostF>
 __device__ __forceinline__ void backtrack_warp(int32_t N, int32_t b, const uint32_t *__restrict__ sch,
                                                const uint32_t *__restrict__ gch, int32_t ntiles, int32_t gtiles,
-                                               const int2 *__restrict__ opt_s, const int32_t *__restrict__ cst,
-                                               uint8_t *__restrict__ exit_g, uint8_t *__restrict__ exit_s, int lane)
+                                               CostF cost, uint8_t *__restrict__ exit_g, uint8_t *__restrict__ exit_s,
+                                               int lane)
 {
     constexpr int CB = (K <= 4) ? 2 : 4;
     constexpr int RPT = 32 / CB;
@@ -188,7 +188,6 @@ __device__ __forceinline__ void backtrack_warp(int32_t N, int32_t b, const uint3
         a = (lane - 1 - K) / K;
         a2 = (lane - 1 - K) % K;
     }
-    auto cost = [&](int32_t i, int32_t k) -> int32_t { return OSM ? opt_s[i * K + k].y : cst[i * K + k]; };
     auto choice = [&](int32_t i, int32_t cell) -> int32_t {
         const int32_t t = cell / (32 * RPT);
         const int32_t j = (cell >> 5) & (RPT - 1);
@@ -458,7 +457,6 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
                 gp[k] = __shfl_sync(0xffffffffu, my_gp, k);
                 cc[k] = __shfl_sync(0xffffffffu, my_c, k);
             }
-            if (MODE != DP_PLAN && warp == 0 && lane < K) cst[i * K + lane] = my_c;
             if (i > 0 && lane < K) {                      // prefetch frame i-1
                 int32_t g, c;
                 load_opt(i - 1, lane, g, c);
@@ -512,7 +510,14 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
             if (exit_s) exit_s[i] = 0;
         }
     } else if (warp == 0) {
-        backtrack_warp<K, MODE, OSM>(N, Cst, sch, gch, ntiles, gtiles, opt_s, cst, P.exit_out + ff, exit_s, lane);
+        // costs of the walk: the staged table, or global memory (option table / profile row)
+        auto cost = [&](int32_t i, int32_t k) -> int32_t {
+            if (OSM) return opt_s[i * K + k].y;
+            int32_t g, c;
+            load_opt(i, k, g, c);
+            return c;
+        };
+        backtrack_warp<K, MODE>(N, Cst, sch, gch, ntiles, gtiles, cost, P.exit_out + ff, exit_s, lane);
     }
     if (FUSE) {                                           // a6: CTA-private histograms
         if (nwarps > 1) __syncthreads(); else __syncwarp();
