@@ -281,13 +281,20 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     const int32_t *__restrict__ oc = P.opt_cost + fo;
     // option (g, c) of frame i, exit k straight from global memory: the option table (lookup
     // path) or, fused, the profile row of the frame's class (a zero row for a class >= C)
-    const turbo_profile_t *prof = FUSE ? P.profiles + win->profile : nullptr;
+    int32_t prof_C = 0;
+    const int32_t *prof_g = nullptr, *prof_c = nullptr;
+    if (FUSE) {
+        const turbo_profile_t *prof = P.profiles + win->profile;
+        prof_C = prof->num_classes;
+        prof_g = prof->gain;
+        prof_c = prof->cost;
+    }
     auto load_opt = [&](int32_t i, int32_t k, int32_t &g, int32_t &c) {
         if (FUSE) {
             const int32_t cls = P.class_id[ff + i];
-            if (cls < prof->num_classes) {
-                g = __ldg(prof->gain + cls * K + k);
-                c = __ldg(prof->cost + cls * K + k);
+            if (cls < prof_C) {
+                g = __ldg(prof_g + cls * K + k);
+                c = __ldg(prof_c + cls * K + k);
             } else {
                 g = 0;
                 c = 0;
@@ -372,7 +379,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
                 } else {
                     load_opt(i, k, g, c);
                     bad |= (c < 0) || (c >= (1 << 30)) || (g > (1 << 24)) || (g < -(1 << 24));
-                    if (FUSE && k == 0 && (int32_t)P.class_id[ff + i] >= prof->num_classes)
+                    if (FUSE && k == 0 && (int32_t)P.class_id[ff + i] >= prof_C)
                         atomic_min_i64(&P.status[0], ff + i);
                 }
                 const int32_t a = g < 0 ? -g : g;
@@ -426,12 +433,24 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     const int32_t gtiles = (int32_t)(((Bb + 32) >> 5) + RPT - 1) / RPT;
     uint32_t *__restrict__ gch = reinterpret_cast<uint32_t *>(P.workspace + choff);
 
-    int32_t my_gp = 0, my_c = 0;                          // !OSM: option `lane` of the current frame
-    if (!OSM && N > 0 && lane < K) {
-        int32_t g, c;
-        load_opt(N - 1, lane, g, c);
-        my_gp = (g << 4) | (15 - lane);
-        my_c = c;
+    // !OSM: options live in registers, CH = 32/K frames per warp-wide chunk (lane q*K + k holds
+    // option k of the chunk's q-th frame); the next chunk is loaded while the current one is
+    // consumed, so CH frames of work hide the global-load latency.
+    constexpr int CH = 32 / K;
+    int32_t a_gp = 0, a_c = 0, b_gp = 0, b_c = 0;
+    const int lq = lane / K, lk = lane - (lane / K) * K;
+    auto load_chunk = [&](int32_t hi, int32_t &gp_out, int32_t &c_out) {   // frames hi, hi-1, ...
+        const int32_t i = hi - lq;
+        if (lq < CH && i >= 0) {
+            int32_t g, c;
+            load_opt(i, lk, g, c);
+            gp_out = (g << 4) | (15 - lk);
+            c_out = c;
+        }
+    };
+    if (!OSM && N > 0) {
+        load_chunk(N - 1, a_gp, a_c);
+        load_chunk(N - 1 - CH, b_gp, b_c);
     }
     int32_t *__restrict__ cur = rowA;
     int32_t *__restrict__ nxt = inplace ? rowA : rowB;
@@ -452,16 +471,17 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
                 cc[k] = v.y;
             }
         } else {
+            const int32_t f = N - 1 - i;
+            const int q = f % CH;
+            if (q == 0 && f > 0) {                        // next chunk becomes current; prefetch
+                a_gp = b_gp;
+                a_c = b_c;
+                load_chunk(i - CH, b_gp, b_c);
+            }
 #pragma unroll
             for (int k = 0; k < K; ++k) {
-                gp[k] = __shfl_sync(0xffffffffu, my_gp, k);
-                cc[k] = __shfl_sync(0xffffffffu, my_c, k);
-            }
-            if (i > 0 && lane < K) {                      // prefetch frame i-1
-                int32_t g, c;
-                load_opt(i - 1, lane, g, c);
-                my_gp = (g << 4) | (15 - lane);
-                my_c = c;
+                gp[k] = __shfl_sync(0xffffffffu, a_gp, q * K + k);
+                cc[k] = __shfl_sync(0xffffffffu, a_c, q * K + k);
             }
         }
         int32_t cmax = cc[0];
