@@ -44,7 +44,7 @@ static const int64_t OSM_LIMIT_BYTES = 48 * 1024;   // largest per-window option
 
 static void dp_smem_words(const turbo_shape_t *s, int mode, DpParams *P)
 {
-    const int64_t rows = num_rows(s->max_budget_small);
+    const int64_t rows = (num_rows(s->max_budget_small) + 15) & ~(int64_t)15;   // whole tiles (<= 16 rows)
     P->row_words = (int32_t)(rows * 32);
     const int rpt_min = s->max_exits <= 4 ? 16 : 8;
     const int64_t tiles = (rows + rpt_min - 1) / rpt_min;
@@ -67,6 +67,33 @@ static int32_t dp_pad_words(const turbo_shape_t *s)
 {
     const int64_t row = num_rows(s->max_budget_small) * 32;
     return (int32_t)(row < 256 ? row : 256);
+}
+
+// Per-device streams and events used to run the row-size class launches concurrently.
+struct ForkJoin {
+    std::mutex mu;
+    cudaStream_t streams[TURBO_NUM_CLASSES];
+    cudaEvent_t fork;
+    cudaEvent_t join[TURBO_NUM_CLASSES];
+};
+
+static ForkJoin *fork_join_for_device()
+{
+    static std::mutex mu;
+    static ForkJoin *per_dev[64] = {nullptr};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!per_dev[dev]) {
+        ForkJoin *fj = new ForkJoin();
+        for (int c = 0; c < TURBO_NUM_CLASSES; ++c) {
+            if (cudaStreamCreateWithFlags(&fj->streams[c], cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+            if (cudaEventCreateWithFlags(&fj->join[c], cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        }
+        if (cudaEventCreateWithFlags(&fj->fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        per_dev[dev] = fj;
+    }
+    return per_dev[dev];
 }
 
 // fused solve keeps choice planes in shared memory when they are at most this many bytes or
@@ -268,10 +295,31 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int kind, const DpParam
     }
     DpLaunch info;
     cudaError_t e = cudaSuccess;
-    for (int c = 0; c < TURBO_NUM_CLASSES && e == cudaSuccess; ++c)
-        if (shape->cls_count[c])
-            e = launch_dp(&shapes[c], modes[c], Ps[c], d.num_sms, d.smem_per_sm, d.smem_per_cta_optin,
-                          (cudaStream_t)stream, &info);
+    int n_cls = 0;
+    for (int c = 0; c < TURBO_NUM_CLASSES; ++c) n_cls += shape->cls_count[c] ? 1 : 0;
+    if (n_cls <= 1) {
+        for (int c = 0; c < TURBO_NUM_CLASSES && e == cudaSuccess; ++c)
+            if (shape->cls_count[c])
+                e = launch_dp(&shapes[c], modes[c], Ps[c], d.num_sms, d.smem_per_sm, d.smem_per_cta_optin,
+                              (cudaStream_t)stream, &info);
+    } else {
+        // Several classes: each class launch is bounded by its longest window's frame chain, so the
+        // launches run CONCURRENTLY on library-owned streams forked from (and joined back into) the
+        // caller's stream with events -- stream-ordered for the caller and capturable in graphs.
+        ForkJoin *fj = fork_join_for_device();
+        if (!fj) return TURBO_ERR_CUDA;
+        std::lock_guard<std::mutex> lk(fj->mu);
+        e = cudaEventRecord(fj->fork, (cudaStream_t)stream);
+        for (int c = 0; c < TURBO_NUM_CLASSES && e == cudaSuccess; ++c) {
+            if (!shape->cls_count[c]) continue;
+            if ((e = cudaStreamWaitEvent(fj->streams[c], fj->fork, 0)) != cudaSuccess) break;
+            if ((e = launch_dp(&shapes[c], modes[c], Ps[c], d.num_sms, d.smem_per_sm, d.smem_per_cta_optin,
+                               fj->streams[c], &info)) != cudaSuccess)
+                break;
+            if ((e = cudaEventRecord(fj->join[c], fj->streams[c])) != cudaSuccess) break;
+            e = cudaStreamWaitEvent((cudaStream_t)stream, fj->join[c], 0);
+        }
+    }
     if (e == cudaSuccess && shape->num_big > 0) {          // long windows: the whole grid per window
         DpParams P = base;
         P.grid_scratch_offset = shape->grid_scratch_offset;

@@ -402,9 +402,12 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
             red[3] = 0;                                   // C* counter
         }
     }
-    const int32_t nrows = (B + 32) >> 5;
-    const int32_t ntiles = (nrows + RPT - 1) / RPT;
-    // S_N = 0 on every cell (including the padding cells above B in the top row)
+    const int32_t ntiles = (((B + 32) >> 5) + RPT - 1) / RPT;
+    // rows are computed in whole tiles: the cells above B (up to the tile edge, inside the row
+    // allocation) are garbage nobody valid reads (cell b only reads cells <= b), and every tile
+    // takes the unpredicated path
+    const int32_t nrows = ntiles * RPT;
+    // S_N = 0 on every cell (including the padding cells above B)
     for (int32_t x = tid; x < nrows * 32; x += nthr) rowA[x] = 0;
     if (nwarps > 1) __syncthreads(); else __syncwarp();
     if (red[0]) {
