@@ -212,6 +212,20 @@ turbo_status_t turbo_schedule(const turbo_shape_t *shape /* host */, const turbo
                               uint8_t *exit_out, int64_t *stats, int64_t *status, turbo_stream_t stream);
 
 /* ---------------------------------------------------------------------------
+ * NEXT-1 (comparison arm): the paper's own scheduler, prune-and-search (PAPER.md:539-545,
+ * §5.2), on the option tables of turbo_profile_lookup: all frames start at level K-1; while the
+ * cost sum_i c_{i,k_i} exceeds the budget, the frame with the minimal marginal gain
+ * g_{i,k} - g_{i,k-1} is downgraded one level (ties: larger latency reduction, then smaller frame
+ * id); stops when the plan fits or every frame is at level 0 (feasible = 0, plan kept).
+ * gain_out/cost_out: int32 [W] (the heuristic plan's totals); feasible: u8 [W];
+ * exit_out: u8 [total_frames]; steps: int32 [W] downgrade steps (nullable).
+ * Shared memory holds one byte per frame per warp: UNSUPPORTED if max_frames is too large. */
+turbo_status_t turbo_heuristic_plan(const turbo_shape_t *shape /* host */, const turbo_window_t *windows,
+                                    const int32_t *opt_gain, const int32_t *opt_cost, int32_t *gain_out,
+                                    int32_t *cost_out, uint8_t *feasible, uint8_t *exit_out,
+                                    int32_t *steps /* nullable */, turbo_stream_t stream);
+
+/* ---------------------------------------------------------------------------
  * a6 (per GPU): ACCUMULATES the plan statistics into stats (int64[181], layout
  * above; caller zeroes it). The cross-GPU sum (one allreduce over NVLink) is done by
  * the caller's communicator, not inside the library. */

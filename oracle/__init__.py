@@ -121,6 +121,29 @@ def plan(num_frames, budget_, K, opt_gain, opt_cost, mode: str = "table",
     return exits[:F], bg[:W], bc[:W], fe[:W]
 
 
+def heuristic(num_frames, budget_, K, opt_gain, opt_cost):
+    """NEXT-1: the paper's prune-and-search heuristic per window.
+    Returns (exits, gain, cost, feasible, steps)."""
+    lib = _load()
+    nf, bud, Kw = _i32(num_frames), _i32(budget_), _i32(K)
+    W = len(nf)
+    ff = np.zeros(W, dtype=np.int64)
+    if W > 1:
+        ff[1:] = np.cumsum(nf[:-1].astype(np.int64))
+    fo, total = option_offsets(nf, Kw)
+    F = int(nf.astype(np.int64).sum())
+    exits = np.zeros(max(F, 1), dtype=np.uint8)
+    g = np.zeros(max(W, 1), dtype=np.int64)
+    c = np.zeros(max(W, 1), dtype=np.int64)
+    fe = np.zeros(max(W, 1), dtype=np.uint8)
+    st = np.zeros(max(W, 1), dtype=np.int64)
+    og = _i32(opt_gain) if total else np.zeros(1, np.int32)
+    oc = _i32(opt_cost) if total else np.zeros(1, np.int32)
+    lib.oracle_heuristic_batch(ctypes.c_int32(W), _p(nf), _p(bud), _p(Kw), _p(ff), _p(fo), _p(og), _p(oc),
+                               _p(exits), _p(g), _p(c), _p(fe), _p(st))
+    return exits[:F], g[:W], c[:W], fe[:W], st[:W]
+
+
 def stats(num_frames, class_id, exits, best_gain, best_cost, feasible) -> np.ndarray:
     lib = _load()
     out = np.zeros(181, dtype=np.int64)

@@ -316,3 +316,58 @@ void oracle_stats(int32_t num_windows, const int32_t *num_frames, const uint8_t 
         stats[180] += feasible[w] ? 0 : 1;
     }
 }
+
+/* ------------------------------------------------------------------ NEXT-1: the paper's heuristic
+ * Prune-and-search, PAPER.md:539-545 (§5.2): "1) We assign all the m frames with the maximum
+ * kappa. 2) ... we select the frame that has the minimal marginal accuracy gain, and assign
+ * kappa-1. 3) We repeat the prior step until the T is met." With per-frame additive costs
+ * (reading R1) the constraint is sum_i c_{i,k_i} <= B. Marginal gain of frame i at level k >= 1:
+ * g_{i,k} - g_{i,k-1} (one-level difference). Ties: the larger
+ * latency reduction c_{i,k} - c_{i,k-1} first, then the smaller frame id. Frames at level 0 cannot
+ * be downgraded. If every frame reaches level 0 and the cost still exceeds B, the all-zero plan
+ * is returned with feasible = 0. Returns the number of downgrade steps (<= N (K-1)). */
+int64_t oracle_heuristic(int32_t N, int32_t K, const int32_t *g, const int32_t *c, int32_t B, uint8_t *exits,
+                         int64_t *gain_out, int64_t *cost_out, uint8_t *feasible)
+{
+    int64_t cost = 0, steps = 0;
+    for (int32_t i = 0; i < N; ++i) {
+        exits[i] = (uint8_t)(K - 1);
+        cost += c[(int64_t)i * K + K - 1];
+    }
+    while (cost > B) {
+        int32_t pick = -1;
+        int64_t best_m = 0, best_dc = 0;
+        for (int32_t i = 0; i < N; ++i) {
+            int32_t k = exits[i];
+            if (k == 0) continue;
+            int64_t m = (int64_t)g[(int64_t)i * K + k] - g[(int64_t)i * K + k - 1];
+            int64_t dc = (int64_t)c[(int64_t)i * K + k] - c[(int64_t)i * K + k - 1];
+            if (pick < 0 || m < best_m || (m == best_m && dc > best_dc)) {   /* smaller id wins: strict */
+                pick = i;
+                best_m = m;
+                best_dc = dc;
+            }
+        }
+        if (pick < 0) break;                /* everything at level 0 */
+        exits[pick] -= 1;
+        cost -= best_dc;
+        steps += 1;
+    }
+    int64_t gain = 0;
+    for (int32_t i = 0; i < N; ++i) gain += g[(int64_t)i * K + exits[i]];
+    *gain_out = gain;
+    *cost_out = cost;
+    *feasible = (uint8_t)(cost <= B);
+    return steps;
+}
+
+int oracle_heuristic_batch(int32_t num_windows, const int32_t *num_frames, const int32_t *budget, const int32_t *K,
+                           const int64_t *first_frame, const int64_t *first_option, const int32_t *opt_gain,
+                           const int32_t *opt_cost, uint8_t *exits, int64_t *gain, int64_t *cost, uint8_t *feasible,
+                           int64_t *steps)
+{
+    for (int32_t w = 0; w < num_windows; ++w)
+        steps[w] = oracle_heuristic(num_frames[w], K[w], opt_gain + first_option[w], opt_cost + first_option[w],
+                                    budget[w], exits + first_frame[w], &gain[w], &cost[w], &feasible[w]);
+    return 0;
+}

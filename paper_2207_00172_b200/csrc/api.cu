@@ -441,6 +441,27 @@ turbo_status_t turbo_schedule(const turbo_shape_t *shape, const turbo_profile_t 
     return run_dp(shape, RUN_SCHEDULE, P, stream);
 }
 
+turbo_status_t turbo_heuristic_plan(const turbo_shape_t *shape, const turbo_window_t *windows,
+                                    const int32_t *opt_gain, const int32_t *opt_cost, int32_t *gain_out,
+                                    int32_t *cost_out, uint8_t *feasible, uint8_t *exit_out, int32_t *steps,
+                                    turbo_stream_t stream)
+{
+    if (!shape) return TURBO_ERR_INVALID_ARG;
+    if (shape->num_windows == 0) return TURBO_OK;
+    if (!windows || !gain_out || !cost_out || !feasible) return TURBO_ERR_INVALID_ARG;
+    if (shape->total_frames > 0 && !exit_out) return TURBO_ERR_INVALID_ARG;
+    if (shape->total_options > 0 && (!opt_gain || !opt_cost)) return TURBO_ERR_INVALID_ARG;
+    DeviceInfo d;
+    if (device_info(&d) != cudaSuccess) return TURBO_ERR_CUDA;
+    cudaError_t e = launch_heuristic(shape, windows, opt_gain, opt_cost, gain_out, cost_out, feasible, exit_out, steps,
+                                     d.num_sms, d.smem_per_cta_optin, (cudaStream_t)stream);
+    if (e == cudaErrorInvalidConfiguration) {
+        cudaGetLastError();
+        return TURBO_ERR_UNSUPPORTED;
+    }
+    return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
+}
+
 turbo_status_t turbo_stats(const turbo_shape_t *shape, const turbo_window_t *windows, const uint8_t *class_id,
                            const uint8_t *exit_out, const int32_t *best_gain, const int32_t *best_cost,
                            const uint8_t *feasible, int64_t *stats, turbo_stream_t stream)

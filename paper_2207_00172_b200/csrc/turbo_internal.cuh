@@ -117,6 +117,10 @@ __host__ __device__ constexpr int64_t grid_scratch_bytes()
 {
     return 4 * grid_flags_words() + 8 * (int64_t)GRID_RING_DEPTH * GRID_MAX_CTAS * TURBO_BIG_MAX_COST;
 }
+cudaError_t launch_heuristic(const turbo_shape_t *shape, const turbo_window_t *windows, const int32_t *opt_gain,
+                             const int32_t *opt_cost, int32_t *gain_out, int32_t *cost_out, uint8_t *feasible,
+                             uint8_t *exit_out, int32_t *steps, int num_sms, int smem_per_cta_max,
+                             cudaStream_t stream);
 cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams &P, int num_sms,
                            int smem_per_cta_max, cudaStream_t stream);
 size_t dp_smem_bytes(const DpParams &P, int nwarps);

@@ -62,7 +62,8 @@ WINDOW_DTYPE = np.dtype([("first_frame", "<i8"), ("first_option", "<i8"), ("choi
 assert WINDOW_DTYPE.itemsize == 48
 
 EXPORTS = ["turbo_mckp_workspace", "turbo_profile_lookup", "turbo_mckp_plan", "turbo_backtrack",
-           "turbo_mckp_solve", "turbo_mckp_solve_workspace", "turbo_schedule", "turbo_stats", "turbo_debug_set_variant",
+           "turbo_mckp_solve", "turbo_mckp_solve_workspace", "turbo_schedule", "turbo_heuristic_plan", "turbo_stats",
+           "turbo_debug_set_variant",
            "turbo_status_string", "turbo_abi_version"]
 
 _lib = None
@@ -86,6 +87,7 @@ def load(path: Optional[str] = None):
     lib.turbo_mckp_solve_workspace.argtypes = [vp, vp]
     lib.turbo_stats.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.turbo_schedule.argtypes = [vp, vp, vp, vp, vp, i32, vp, sz, vp, vp, vp, vp, vp, vp, vp]
+    lib.turbo_heuristic_plan.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.turbo_debug_set_variant.argtypes = [i32]
     lib.turbo_status_string.restype = ctypes.c_char_p
     lib.turbo_abi_version.restype = i32
@@ -173,6 +175,15 @@ def schedule(shape, profiles_dev, windows_dev, class_id, capacity, base_cost, wo
                                  _ptr(capacity), int(base_cost), _ptr(workspace), nbytes, _ptr(best_gain),
                                  _ptr(best_cost), _ptr(feasible), _ptr(exit_out), _ptr(stats_out), _ptr(status),
                                  _stream(stream)))
+
+
+def heuristic_plan(shape, windows_dev, opt_gain, opt_cost, gain_out, cost_out, feasible, exit_out, steps=None,
+                   stream=None):
+    """NEXT-1: the paper's prune-and-search heuristic on the option tables (comparison arm)."""
+    _check("turbo_heuristic_plan",
+           load().turbo_heuristic_plan(ctypes.addressof(shape), _ptr(windows_dev), _ptr(opt_gain), _ptr(opt_cost),
+                                       _ptr(gain_out), _ptr(cost_out), _ptr(feasible), _ptr(exit_out), _ptr(steps),
+                                       _stream(stream)))
 
 
 def stats(shape, windows_dev, class_id, exit_out, best_gain, best_cost, feasible, stats_out, stream=None):
