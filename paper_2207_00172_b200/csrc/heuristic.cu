@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) heuristic_kernel(HeurParams P)
                 }
             }
             if (k == LLONG_MAX) break;                    // 3) every frame at level 0
-            const int32_t dc = 0x7fffffff - (int32_t)(uint32_t)(k & 0xffffffffll);
+            const long long dc = 0x7fffffffll - (long long)(uint32_t)(k & 0xffffffffll);   // may be < 0
             cost -= dc;
             steps += 1;
             if ((id & 31) == lane) {
