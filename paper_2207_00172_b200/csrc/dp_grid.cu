@@ -71,7 +71,7 @@ __device__ __forceinline__ void tma_load_1d(void *dst, const void *src, uint32_t
 __device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t phase)
 {
     asm volatile(
-        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+        "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 100000;\n @!p bra WAIT_%=;\n}\n" ::"r"(
             smem_addr(mbar)),
         "r"(phase)
         : "memory");
@@ -106,13 +106,22 @@ __device__ __forceinline__ void st_release_gpu(int *p, int v)
     asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Spin until *p >= target. Bounded (~seconds): a lost publication must not hang the GPU; on
+__device__ __forceinline__ int ld_relaxed_gpu(const int *p)
+{
+    int v;
+    asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Spin until *p >= target (the back-pressure counter: no data is read behind it, so a relaxed
+// load suffices -- an acquire would invalidate the SM's L1 on every poll and slow the compute
+// warps' local-memory traffic). Bounded (~seconds): a lost update must not hang the GPU; on
 // timeout the caller flags the window (status[1]) and carries on, so the kernel always exits.
 __device__ __forceinline__ bool wait_at_least(const int *p, int target)
 {
     for (long long it = 0; it < (1ll << 22); ++it) {
-        if (ld_acquire_gpu(p) >= target) return true;
-        __nanosleep(32);
+        if (ld_relaxed_gpu(p) >= target) return true;
+        __nanosleep(256);                  // the comm warp shares its SMSP with compute warps
     }
     return false;
 }
@@ -145,6 +154,7 @@ struct GridCtx {
     int *con;               // [GRID_MAX_CTAS] steps whose halo was consumed
     long long *misc;        // [8] per-window reductions (zeroed between windows)
     unsigned long long *ring;   // [D][GRID_MAX_CTAS][TURBO_BIG_MAX_COST] of {value, step tag}
+    long long *trace;           // [GRID_MAX_CTAS][8] cycle counters (debug bit 2)
 };
 
 template <int K, int MODE>
@@ -306,7 +316,10 @@ __device__ __noinline__ void grid_window(const DpParams &P, cg::grid_group &grid
                     bool mine_ok = true;
                     for (int32_t x = lane; x < hl8; x += 32) mine_ok &= (uint32_t)(stage_in[x] >> 32) == tag;
                     ok = __all_sync(0xffffffffu, mine_ok);
-                    if (!ok) __nanosleep(64);
+                    if (!ok) {
+                        if ((P.debug & 2) && lane == 0) X.trace[(int64_t)j * 8 + 6] += 1;
+                        __nanosleep(256);
+                    }
                 }
                 if (!ok && lane == 0) atomic_min_i64(&P.status[1], w);
                 for (int32_t x = lane; x < hl8; x += 32) cur[H - hl8 + x] = (int32_t)(uint32_t)stage_in[x];
@@ -344,6 +357,9 @@ __device__ __noinline__ void grid_window(const DpParams &P, cg::grid_group &grid
             const int C = nwarps - 1;
             const int par = f & 1;
             const int bar_top = 1 + par, bar_halo = 3 + par, bar_step = 5;
+            const bool trace = (P.debug & 2) != 0;
+            long long *tr = X.trace + (int64_t)j * 8;
+            long long t_a = trace ? clock64() : 0;
             if (warp < C) {
                 const int32_t n_pre = split ? t_end - bot_end : 0;      // top first, then the middle
                 bool arrived = false;
@@ -359,20 +375,33 @@ __device__ __noinline__ void grid_window(const DpParams &P, cg::grid_group &grid
                         arrived = true;
                     }
                 }
+                long long t_b = trace ? clock64() : 0;
                 named_sync(bar_halo, nthr);
+                if (trace && tid == 0) tr[1] += clock64() - t_b;
                 for (int32_t t = (split ? bot_end : t_end) - 1 - warp; t >= t_first; t -= C) do_tile(t);
                 if (!arrived) {
                     __threadfence_block();
                     named_arrive(bar_top, nthr);
                 }
+                t_b = trace ? clock64() : 0;
                 named_sync(bar_step, C * 32);
+                if (trace && tid == 0) {
+                    tr[2] += clock64() - t_b;
+                    tr[0] += clock64() - t_a;
+                    tr[7] += 1;
+                }
             } else if (split) {
                 // the halo (published a step ago, normally already in L2) is requested at once and
                 // lands while we wait for our top tiles and publish them
                 if (need_halo) issue_halo();
                 named_sync(bar_top, nthr);
+                long long t_c = trace ? clock64() : 0;
+                if (trace && lane == 0) tr[3] += t_c - t_a;
                 if (publish) do_publish();
+                long long t_d = trace ? clock64() : 0;
+                if (trace && lane == 0) tr[4] += t_d - t_c;
                 if (need_halo) fetch_halo(true);
+                if (trace && lane == 0) tr[5] += clock64() - t_d;
                 __threadfence_block();
                 named_arrive(bar_halo, nthr);
                 if (need_halo) release_halo_slot();
@@ -443,6 +472,7 @@ __global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg
     X.con = flags + GRID_MAX_CTAS;
     X.misc = reinterpret_cast<long long *>(flags + 2 * GRID_MAX_CTAS);
     X.ring = reinterpret_cast<unsigned long long *>(flags + grid_flags_words());
+    X.trace = reinterpret_cast<long long *>(flags + 2 * GRID_MAX_CTAS + 64);
     int step_base = tag_base;          // ring tags of this launch never repeat an earlier launch's
     for (int64_t w = 0; w < P.num_windows; ++w) {
         if ((int64_t)P.windows[w].budget_bound + 1 <= TURBO_BIG_CELLS) continue;

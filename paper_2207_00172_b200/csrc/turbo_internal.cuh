@@ -112,7 +112,7 @@ int dp_warps_per_window(const turbo_shape_t *shape);
 // long-window (grid) kernel: scratch = flags (pub/con per CTA + misc) + halo ring
 constexpr int GRID_MAX_CTAS = 256;
 constexpr int GRID_RING_DEPTH = 8;
-__host__ __device__ constexpr int64_t grid_flags_words() { return 2 * GRID_MAX_CTAS + 64; }
+__host__ __device__ constexpr int64_t grid_flags_words() { return 2 * GRID_MAX_CTAS + 64 + 16 * GRID_MAX_CTAS; }
 __host__ __device__ constexpr int64_t grid_scratch_bytes()
 {
     return 4 * grid_flags_words() + 8 * (int64_t)GRID_RING_DEPTH * GRID_MAX_CTAS * TURBO_BIG_MAX_COST;
