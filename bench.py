@@ -295,28 +295,20 @@ def run_turbo(args):
 
     # ---- e2e through the C ABI with HOST buffers (pinned), H2D inputs + D2H results inside
     F = int(b.shape.total_frames)
-    h_cls = torch.from_numpy(np.ascontiguousarray(wl.class_id)).pin_memory()
-    h_cap = torch.from_numpy(np.ascontiguousarray(wl.capacity)).pin_memory()
-    h_exits = torch.empty(max(F, 1), dtype=torch.uint8).pin_memory()
-    h_gain = torch.empty(max(W, 1), dtype=torch.int32).pin_memory()
-    h_cost = torch.empty(max(W, 1), dtype=torch.int32).pin_memory()
-    h_feas = torch.empty(max(W, 1), dtype=torch.uint8).pin_memory()
-    h_stats = torch.empty(181, dtype=torch.int64).pin_memory()
-    h2d = F + 4 * W
-    d2h = F + 9 * W + 8 * 181
+    # host buffers (pinned) mirroring the device input / output arenas: one copy each way
+    h_in = torch.empty_like(b.in_arena, device="cpu").pin_memory()
+    h_in.copy_(b.in_arena)
+    h_out = torch.empty_like(b.out_arena, device="cpu").pin_memory()
+    h2d = b.in_arena.numel()
+    d2h = b.out_arena.numel()
 
     def e2e_step():
         # the public API, called eagerly (no graph): H2D inputs, the C-ABI calls, D2H results
-        b.class_id[:F].copy_(h_cls, non_blocking=True)
-        b.capacity.copy_(h_cap, non_blocking=True)
+        b.in_arena.copy_(h_in, non_blocking=True)
         step()
         if dist is not None:
             dist.all_reduce(b.stats)
-        h_exits[:F].copy_(b.exit_out[:F], non_blocking=True)
-        h_gain[:W].copy_(b.best_gain[:W], non_blocking=True)
-        h_cost[:W].copy_(b.best_cost[:W], non_blocking=True)
-        h_feas[:W].copy_(b.feasible[:W], non_blocking=True)
-        h_stats.copy_(b.stats, non_blocking=True)
+        h_out.copy_(b.out_arena, non_blocking=True)
 
     e2e_steps = max(1, min(args.steps, 50))
     for _ in range(3):

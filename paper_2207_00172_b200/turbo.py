@@ -219,6 +219,8 @@ class Batch:
     status: object
     stats: object
     solve_ws: object
+    in_arena: object = None      # [capacity | class_id] (one H2D per step)
+    out_arena: object = None     # [stats | status | best_gain | best_cost | feasible | exit_out] (one D2H)
 
 
 def make_batch(profiles_gain: List[np.ndarray], profiles_cost: List[np.ndarray], profiles_shape: List[tuple],
@@ -253,12 +255,31 @@ def make_batch(profiles_gain: List[np.ndarray], profiles_cost: List[np.ndarray],
     profiles_dev = torch.as_tensor(pbytes.copy(), device=dev)
     windows_dev = torch.as_tensor(wins.view(np.uint8).copy(), device=dev)
     F = int(shape.total_frames)
-    cls = torch.zeros(max(F, 1), dtype=torch.uint8, device=dev)
+    # inputs in one device arena [capacity int32 W | class_id u8 F] and outputs in another
+    # [stats int64 181 | status int64 2 | best_gain int32 W | best_cost int32 W | feasible u8 W |
+    # exit_out u8 F]: one host<->device copy each way per step (sub-buffers 16-B aligned)
+    def _carve(arena, sizes):
+        views, off = [], 0
+        for nbytes, dt in sizes:
+            views.append(arena[off: off + nbytes].view(dt))
+            off += (nbytes + 15) & ~15
+        return views
+    def _total(sizes):
+        return sum((n + 15) & ~15 for n, _ in sizes)
+    in_sizes = [(4 * max(W, 1), torch.int32), (max(F, 1), torch.uint8)]
+    in_arena = torch.zeros(_total(in_sizes), dtype=torch.uint8, device=dev)
+    cap_v, cls = _carve(in_arena, in_sizes)
     if class_id is not None and F:
         cls[:F] = torch.as_tensor(np.ascontiguousarray(class_id, dtype=np.uint8), device=dev)
     cap = None
     if capacity is not None:
-        cap = torch.as_tensor(np.ascontiguousarray(capacity, dtype=np.int32), device=dev)
+        cap = cap_v
+        cap[:W] = torch.as_tensor(np.ascontiguousarray(capacity, dtype=np.int32), device=dev)
+    out_sizes = [(8 * STATS_WORDS, torch.int64), (8 * STATUS_WORDS, torch.int64), (4 * max(W, 1), torch.int32),
+                 (4 * max(W, 1), torch.int32), (max(W, 1), torch.uint8), (max(F, 1), torch.uint8)]
+    out_arena = torch.zeros(_total(out_sizes), dtype=torch.uint8, device=dev)
+    st_v, status_v, bg_v, bc_v, fe_v, ex_v = _carve(out_arena, out_sizes)
+    status_v.fill_(-1)
     nopt = max(int(shape.total_options), 4)
     ws_bytes = int(shape.workspace_bytes) if with_plan_workspace else 0
     solve_bytes = mckp_solve_workspace(shape)
@@ -268,13 +289,9 @@ def make_batch(profiles_gain: List[np.ndarray], profiles_cost: List[np.ndarray],
                  opt_gain=torch.zeros(nopt, dtype=torch.int32, device=dev),
                  opt_cost=torch.zeros(nopt, dtype=torch.int32, device=dev),
                  workspace=torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev) if ws_bytes else None,
-                 best_gain=torch.zeros(max(W, 1), dtype=torch.int32, device=dev),
-                 best_cost=torch.zeros(max(W, 1), dtype=torch.int32, device=dev),
-                 feasible=torch.zeros(max(W, 1), dtype=torch.uint8, device=dev),
-                 exit_out=torch.zeros(max(F, 1), dtype=torch.uint8, device=dev),
-                 status=torch.full((STATUS_WORDS,), -1, dtype=torch.int64, device=dev),
-                 stats=torch.zeros(STATS_WORDS, dtype=torch.int64, device=dev),
-                 solve_ws=torch.empty(solve_bytes, dtype=torch.uint8, device=dev) if solve_bytes else None)
+                 best_gain=bg_v, best_cost=bc_v, feasible=fe_v, exit_out=ex_v, status=status_v, stats=st_v,
+                 solve_ws=torch.empty(solve_bytes, dtype=torch.uint8, device=dev) if solve_bytes else None,
+                 in_arena=in_arena, out_arena=out_arena)
 
 
 def batch_from_workload(wl, device="cuda", with_plan_workspace: bool = True) -> Batch:
