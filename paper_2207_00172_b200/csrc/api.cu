@@ -1,5 +1,6 @@
 // api.cu -- host side of the C ABI (include/turbo.h): validation, sizing, dispatch.
 // No device memory is allocated here and nothing synchronises the device.
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -351,6 +352,12 @@ static DpParams base_params(const turbo_shape_t *shape, const turbo_window_t *wi
     P.status = status;
     P.grid_scratch_offset = shape->grid_scratch_offset;
     P.cls = -1;
+    static int dbg = -1;                     // TURBO_DP_DEBUG: timing-only switches (8: no stats
+    if (dbg < 0) {                           // flush, 16: no backtrack); results are then wrong
+        const char *e = getenv("TURBO_DP_DEBUG");
+        dbg = e ? atoi(e) : 0;
+    }
+    P.debug = dbg;
     return P;
 }
 

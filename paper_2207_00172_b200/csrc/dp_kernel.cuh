@@ -195,42 +195,46 @@ __device__ __forceinline__ void backtrack_warp(int32_t N, int32_t b, const uint3
                                                       : gch[((int64_t)i * gtiles + t) * 32 + (cell & 31)];
         return (int32_t)((word >> choice_shift(j, CB)) & CMASK);
     };
-    for (int32_t i = 0; i < N; i += D) {
-        const int32_t ca = (depth >= 1 && i + 1 < N) ? cost(i, a) : 0;
-        const int32_t cb = (depth == 2 && i + 2 < N) ? cost(i + 1, a2) : 0;
-        const int32_t cl = (lane < K && i + D - 1 < N) ? cost(i + D - 1, lane) : 0;   // last frame's costs
+    auto emit = [&](int32_t i, int32_t k) {
+        exit_g[i] = (uint8_t)k;
+        if (exit_s) exit_s[i] = (uint8_t)k;
+    };
+    int32_t i = 0;
+    // full rounds: the deepest lane whose speculated prefix matches the realised choices holds
+    // the whole round -- one vote and two shuffles resolve it (no serial shuffle chain)
+    for (; i + D <= N; i += D) {
+        const int32_t ca = depth >= 1 ? cost(i, a) : 0;
+        const int32_t cb = depth == 2 ? cost(i + 1, a2) : 0;
         int32_t kk = 0;
-        if (depth == 0) {
-            kk = choice(i, b);
-        } else if (depth >= 1 && i + depth < N) {
+        if (depth >= 0) {
             const int32_t bt = b - ca - cb;
             kk = bt >= 0 ? choice(i + depth, bt) : 0;
         }
         const int32_t k0 = __shfl_sync(0xffffffffu, kk, 0);
-        const int32_t c0 = __shfl_sync(0xffffffffu, ca, 1 + k0);
-        const int32_t k1 = __shfl_sync(0xffffffffu, kk, 1 + k0);
-        int32_t k2 = 0, step;
-        if (D == 3) {
-            const int32_t l2 = 1 + K + k0 * K + k1;
-            const int32_t c1 = __shfl_sync(0xffffffffu, cb, l2);
-            k2 = __shfl_sync(0xffffffffu, kk, l2);
-            step = c0 + c1 + __shfl_sync(0xffffffffu, cl, k2);
-        } else {
-            step = c0 + __shfl_sync(0xffffffffu, cl, k1);
+        const int32_t k1 = __shfl_sync(0xffffffffu, kk, D == 3 && depth == 2 ? 1 + a : lane);
+        const bool on_path = (depth == D - 1) && (a == k0) && (D == 2 || a2 == k1);
+        int32_t packed = 0, step = 0;
+        if (on_path) {
+            step = ca + cb + cost(i + depth, kk);
+            packed = D == 3 ? (k0 | (k1 << 4) | (kk << 8)) : (k0 | (kk << 4));
         }
+        const int src = __ffs(__ballot_sync(0xffffffffu, on_path)) - 1;
+        packed = __shfl_sync(0xffffffffu, packed, src);
+        step = __shfl_sync(0xffffffffu, step, src);
         if (lane == 0) {
-            exit_g[i] = (uint8_t)k0;
-            if (exit_s) exit_s[i] = (uint8_t)k0;
-            if (i + 1 < N) {
-                exit_g[i + 1] = (uint8_t)k1;
-                if (exit_s) exit_s[i + 1] = (uint8_t)k1;
-            }
-            if (D == 3 && i + 2 < N) {
-                exit_g[i + 2] = (uint8_t)k2;
-                if (exit_s) exit_s[i + 2] = (uint8_t)k2;
-            }
+            emit(i, packed & 15);
+            emit(i + 1, (packed >> 4) & 15);
+            if (D == 3) emit(i + 2, (packed >> 8) & 15);
         }
         b -= step;
+    }
+    // tail (< D frames): plain walk by lane 0
+    if (lane == 0) {
+        for (; i < N; ++i) {
+            const int32_t k = choice(i, b);
+            emit(i, k);
+            b -= cost(i, k);
+        }
     }
 }
 
@@ -532,7 +536,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
             P.exit_out[ff + i] = 0;
             if (exit_s) exit_s[i] = 0;
         }
-    } else if (warp == 0) {
+    } else if (warp == 0 && !(P.debug & 16)) {
         // costs of the walk: the staged table, or global memory (option table / profile row)
         auto cost = [&](int32_t i, int32_t k) -> int32_t {
             if (OSM) return opt_s[i * K + k].y;
@@ -551,7 +555,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
             if (cls < 10) atomicAdd(&hist[16 + cls * 16 + k], 1u);
         }
         if (nwarps > 1) __syncthreads(); else __syncwarp();
-        flush_window_stats(P, hist, G, Cst, feas, N, tid, nthr);
+        if (!(P.debug & 8)) flush_window_stats(P, hist, G, Cst, feas, N, tid, nthr);
     }
 }
 
