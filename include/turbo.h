@@ -226,6 +226,26 @@ turbo_status_t turbo_heuristic_plan(const turbo_shape_t *shape /* host */, const
                                     int32_t *steps /* nullable */, turbo_stream_t stream);
 
 /* ---------------------------------------------------------------------------
+ * NEXT-3 (the step before the path): difficulty score -> difficulty class. PAPER.md:511
+ * buckets of width 0.1; theta'_x from D_f (:525); reading R6: class = bucket of d = 1 - theta,
+ * class_out[x] = clamp(floor((1 - theta[x]) * (1 / bucket_width)), 0, C-1), decided in IEEE
+ * float32 (1/bucket_width rounded to float32 once); NaN -> 0. theta: float32 [n], 16-B aligned;
+ * class_out: u8 [n], 4-B aligned. */
+turbo_status_t turbo_bucketize(const float *theta, int64_t num_frames, int32_t num_classes,
+                               float bucket_width, uint8_t *class_out, turbo_stream_t stream);
+
+/* ---------------------------------------------------------------------------
+ * NEXT-2 (the step after the path): plan -> per-exit batches ("organize the frames
+ * assigned by the same enhancement level to execute in a batch", :545). Per window w:
+ * count_out[16 w + k] = n_k, the number of frames planned at level k; order_out[first_frame_w
+ * + j] = window-local frame indices grouped by level ascending, arrival order inside a level
+ * (a stable partition; the batch of level k starts at sum_{k' < k} n_k'). exit_out: the plan
+ * (u8 [total_frames]); count_out: int32 [16 W]; order_out: int32 [total_frames]. */
+turbo_status_t turbo_batches(const turbo_shape_t *shape /* host */, const turbo_window_t *windows,
+                             const uint8_t *exit_out, int32_t *count_out, int32_t *order_out,
+                             turbo_stream_t stream);
+
+/* ---------------------------------------------------------------------------
  * a6 (per GPU): ACCUMULATES the plan statistics into stats (int64[181], layout
  * above; caller zeroes it). The cross-GPU sum (one allreduce over NVLink) is done by
  * the caller's communicator, not inside the library. */

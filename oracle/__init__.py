@@ -26,7 +26,7 @@ def build(force: bool = False) -> str:
     """Compile the oracle with plain gcc -O2 (no intrinsics)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         subprocess.check_call(["gcc", "-O2", "-std=c99", "-shared", "-fPIC", "-pthread",
-                               "-o", _LIB, _SRC])
+                               "-o", _LIB, _SRC, "-lm"])
     return _LIB
 
 
@@ -142,6 +142,29 @@ def heuristic(num_frames, budget_, K, opt_gain, opt_cost):
     lib.oracle_heuristic_batch(ctypes.c_int32(W), _p(nf), _p(bud), _p(Kw), _p(ff), _p(fo), _p(og), _p(oc),
                                _p(exits), _p(g), _p(c), _p(fe), _p(st))
     return exits[:F], g[:W], c[:W], fe[:W], st[:W]
+
+
+def bucketize(theta, num_classes: int = 10, width: float = 0.1) -> np.ndarray:
+    """NEXT-3: class = clamp(floor((1 - theta) * (1/width)), 0, C-1) in float32."""
+    lib = _load()
+    th = np.ascontiguousarray(theta, dtype=np.float32)
+    out = np.zeros(max(len(th), 1), dtype=np.uint8)
+    lib.oracle_bucketize(ctypes.c_int64(len(th)), _p(th), ctypes.c_float(np.float32(1.0) / np.float32(width)),
+                         ctypes.c_int32(num_classes), _p(out))
+    return out[:len(th)]
+
+
+def batches(num_frames, exits):
+    """NEXT-2: per-window exit counts [W, 16] and the stable per-exit frame order [F]."""
+    lib = _load()
+    nf = _i32(num_frames)
+    W = len(nf)
+    F = int(nf.astype(np.int64).sum())
+    count = np.zeros(max(W, 1) * 16, dtype=np.int32)
+    order = np.zeros(max(F, 1), dtype=np.int32)
+    lib.oracle_batches(ctypes.c_int32(W), _p(nf), _p(np.ascontiguousarray(exits, dtype=np.uint8)), _p(count),
+                       _p(order))
+    return count[:W * 16].reshape(W, 16), order[:F]
 
 
 def stats(num_frames, class_id, exits, best_gain, best_cost, feasible) -> np.ndarray:

@@ -21,6 +21,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <pthread.h>
+#include <math.h>
 
 #define ORACLE_NEG_INF INT64_MIN  /* "no plan of cost <= b exists" */
 
@@ -370,4 +371,46 @@ int oracle_heuristic_batch(int32_t num_windows, const int32_t *num_frames, const
         steps[w] = oracle_heuristic(num_frames[w], K[w], opt_gain + first_option[w], opt_cost + first_option[w],
                                     budget[w], exits + first_frame[w], &gain[w], &cost[w], &feasible[w]);
     return 0;
+}
+
+/* ------------------------------------------------------------------ NEXT-3: score -> class
+ * PAPER.md:511 (§5.1): frames are bucketised by difficulty with granularity 0.1; the online
+ * classifier D_f gives the estimated score theta'_x. Reading R6: the class is the
+ * bucket of d = 1 - theta' (class C-1 hardest); SPEC.md:65-73 bucket_index: floor(d / g), d = 1
+ * clamped into the top bucket, d < 0 into bucket 0. The decision is taken in IEEE float32 (the
+ * kernel's precision): d = 1 - theta (one rounding), q = d * (1/g) with 1/g given as a float32
+ * (one rounding), class = floor(q) clamped to [0, C-1]. NaN scores map to class 0. */
+void oracle_bucketize(int64_t n, const float *theta, float inv_width, int32_t C, uint8_t *cls)
+{
+    for (int64_t x = 0; x < n; ++x) {
+        volatile float d = 1.0f - theta[x];
+        volatile float q = d * inv_width;
+        int32_t c = 0;
+        if (q >= (float)C) c = C - 1;
+        else if (q >= 0.0f) c = (int32_t)floorf(q);     /* NaN fails both tests -> 0 */
+        if (c > C - 1) c = C - 1;
+        cls[x] = (uint8_t)c;
+    }
+}
+
+/* ------------------------------------------------------------------ NEXT-2: per-exit batches
+ * PAPER.md:525 "organize the frames assigned by the same enhancement level to execute in a batch"
+ * and :545 "we execute each frame according to the plan": per window, the frames of every exit
+ * level kappa in arrival order (a stable partition), the batch sizes n_kappa, and the batch
+ * offsets. Outputs: count[w*16 + k] = n_k; order[first_frame_w + j] = window-local frame index,
+ * grouped by k ascending, arrival order within a group. */
+void oracle_batches(int32_t num_windows, const int32_t *num_frames, const uint8_t *exits, int32_t *count,
+                    int32_t *order)
+{
+    int64_t f0 = 0;
+    for (int32_t w = 0; w < num_windows; ++w) {
+        int32_t N = num_frames[w];
+        for (int k = 0; k < 16; ++k) count[(int64_t)w * 16 + k] = 0;
+        for (int32_t i = 0; i < N; ++i) count[(int64_t)w * 16 + exits[f0 + i]] += 1;
+        int64_t pos = f0;
+        for (int k = 0; k < 16; ++k)
+            for (int32_t i = 0; i < N; ++i)
+                if (exits[f0 + i] == k) order[pos++] = i;
+        f0 += N;
+    }
 }

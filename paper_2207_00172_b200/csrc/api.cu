@@ -469,6 +469,35 @@ turbo_status_t turbo_heuristic_plan(const turbo_shape_t *shape, const turbo_wind
     return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
 }
 
+turbo_status_t turbo_bucketize(const float *theta, int64_t num_frames, int32_t num_classes, float bucket_width,
+                               uint8_t *class_out, turbo_stream_t stream)
+{
+    if (num_frames < 0 || num_classes < 1 || num_classes > 256 || !(bucket_width > 0.0f)) return TURBO_ERR_INVALID_ARG;
+    if (num_frames == 0) return TURBO_OK;
+    if (!theta || !class_out) return TURBO_ERR_INVALID_ARG;
+    if ((reinterpret_cast<uintptr_t>(theta) & 15) || (reinterpret_cast<uintptr_t>(class_out) & 3))
+        return TURBO_ERR_INVALID_ARG;
+    DeviceInfo d;
+    if (device_info(&d) != cudaSuccess) return TURBO_ERR_CUDA;
+    const float inv = 1.0f / bucket_width;
+    cudaError_t e = launch_bucketize(theta, num_frames, num_classes, inv, class_out, d.num_sms, (cudaStream_t)stream);
+    return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
+}
+
+turbo_status_t turbo_batches(const turbo_shape_t *shape, const turbo_window_t *windows, const uint8_t *exit_out,
+                             int32_t *count_out, int32_t *order_out, turbo_stream_t stream)
+{
+    if (!shape) return TURBO_ERR_INVALID_ARG;
+    if (shape->num_windows == 0) return TURBO_OK;
+    if (!windows || !count_out) return TURBO_ERR_INVALID_ARG;
+    if (shape->total_frames > 0 && (!exit_out || !order_out)) return TURBO_ERR_INVALID_ARG;
+    DeviceInfo d;
+    if (device_info(&d) != cudaSuccess) return TURBO_ERR_CUDA;
+    cudaError_t e = launch_batches(windows, shape->num_windows, exit_out, count_out, order_out, d.num_sms,
+                                   (cudaStream_t)stream);
+    return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
+}
+
 turbo_status_t turbo_stats(const turbo_shape_t *shape, const turbo_window_t *windows, const uint8_t *class_id,
                            const uint8_t *exit_out, const int32_t *best_gain, const int32_t *best_cost,
                            const uint8_t *feasible, int64_t *stats, turbo_stream_t stream)

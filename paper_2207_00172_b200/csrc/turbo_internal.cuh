@@ -121,6 +121,10 @@ cudaError_t launch_heuristic(const turbo_shape_t *shape, const turbo_window_t *w
                              const int32_t *opt_cost, int32_t *gain_out, int32_t *cost_out, uint8_t *feasible,
                              uint8_t *exit_out, int32_t *steps, int num_sms, int smem_per_cta_max,
                              cudaStream_t stream);
+cudaError_t launch_bucketize(const float *theta, int64_t n, int32_t C, float inv_width, uint8_t *cls, int num_sms,
+                             cudaStream_t stream);
+cudaError_t launch_batches(const turbo_window_t *windows, int32_t num_windows, const uint8_t *exit_out,
+                           int32_t *count, int32_t *order, int num_sms, cudaStream_t stream);
 cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams &P, int num_sms,
                            int smem_per_cta_max, cudaStream_t stream);
 size_t dp_smem_bytes(const DpParams &P, int nwarps);

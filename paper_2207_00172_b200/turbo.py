@@ -63,6 +63,7 @@ assert WINDOW_DTYPE.itemsize == 48
 
 EXPORTS = ["turbo_mckp_workspace", "turbo_profile_lookup", "turbo_mckp_plan", "turbo_backtrack",
            "turbo_mckp_solve", "turbo_mckp_solve_workspace", "turbo_schedule", "turbo_heuristic_plan", "turbo_stats",
+           "turbo_bucketize", "turbo_batches",
            "turbo_debug_set_variant",
            "turbo_status_string", "turbo_abi_version"]
 
@@ -88,6 +89,8 @@ def load(path: Optional[str] = None):
     lib.turbo_stats.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.turbo_schedule.argtypes = [vp, vp, vp, vp, vp, i32, vp, sz, vp, vp, vp, vp, vp, vp, vp]
     lib.turbo_heuristic_plan.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    lib.turbo_bucketize.argtypes = [vp, i64, i32, ctypes.c_float, vp, vp]
+    lib.turbo_batches.argtypes = [vp, vp, vp, vp, vp, vp]
     lib.turbo_debug_set_variant.argtypes = [i32]
     lib.turbo_status_string.restype = ctypes.c_char_p
     lib.turbo_abi_version.restype = i32
@@ -184,6 +187,20 @@ def heuristic_plan(shape, windows_dev, opt_gain, opt_cost, gain_out, cost_out, f
            load().turbo_heuristic_plan(ctypes.addressof(shape), _ptr(windows_dev), _ptr(opt_gain), _ptr(opt_cost),
                                        _ptr(gain_out), _ptr(cost_out), _ptr(feasible), _ptr(exit_out), _ptr(steps),
                                        _stream(stream)))
+
+
+def bucketize(theta, class_out, num_classes: int = 10, bucket_width: float = 0.1, stream=None):
+    """NEXT-3: difficulty score (float32, device) -> class id (u8, device)."""
+    _check("turbo_bucketize",
+           load().turbo_bucketize(_ptr(theta), int(theta.numel()), int(num_classes), float(bucket_width),
+                                  _ptr(class_out), _stream(stream)))
+
+
+def batches(shape, windows_dev, exit_out, count_out, order_out, stream=None):
+    """NEXT-2: plan -> per-exit batch sizes [W, 16] and stable per-exit frame order."""
+    _check("turbo_batches",
+           load().turbo_batches(ctypes.addressof(shape), _ptr(windows_dev), _ptr(exit_out), _ptr(count_out),
+                                _ptr(order_out), _stream(stream)))
 
 
 def stats(shape, windows_dev, class_id, exit_out, best_gain, best_cost, feasible, stats_out, stream=None):
