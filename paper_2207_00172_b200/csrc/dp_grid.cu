@@ -91,6 +91,11 @@ __device__ __forceinline__ void tma_store_wait_read()
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 
+__device__ __forceinline__ void tma_store_wait_read_1()
+{
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+}
+
 __device__ __forceinline__ void tma_store_wait_all()
 {
     asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -278,6 +283,21 @@ __device__ __noinline__ void grid_window(const DpParams &P, cg::grid_group &grid
         if (mine) {
             const int32_t *cur_base = cur + H - seg_lo;
             int32_t *nxt_base = nxt + H - seg_lo;
+            const bool need_halo = (j > 0 && f > 0 && hl > 0) && !(P.debug & 1);
+            const bool publish = (j + 1 < active && hl > 0) && !(P.debug & 1);
+            // Halo exchange through the L2 ring with the Tensor Memory Accelerator. Ring words are
+            // 64-bit {value, step tag}: the tag proves a word is current, so neither side needs a
+            // fence or a flag. The published cells (the top hl8 of S_i) are packed by the warps
+            // that compute them; thread 0 ships them with ONE bulk store; thread 0 requests the
+            // halo with ONE bulk load at step start (mbarrier completion) and every thread later
+            // checks a slice of the tags and unpacks it (a stale slot just re-issues the load).
+            const int32_t hl8 = (hl + 1) & ~1;                         // 16-byte multiple of 8-B words
+            const uint32_t pub_tag = (uint32_t)(step_base + f + 1);
+            const int32_t pub_lo = seg_lo + seg - hl8;                 // first published cell
+            unsigned long long *stg = stage_out + (f & 1) * H;         // two publication stages
+            const unsigned long long *halo_src =
+                X.ring + ((int64_t)((step_base + f - 1) % D) * GRID_MAX_CTAS + (j - 1)) * H;
+            if (need_halo && tid == 0) tma_load_1d(stage_in, halo_src, hl8 * 8, mbar);
             auto do_tile = [&](int32_t t) {
                 const int32_t b_lo = t * RPT * 32;
                 const int32_t nr = min(RPT, nrows - t * RPT);
@@ -286,140 +306,71 @@ __device__ __noinline__ void grid_window(const DpParams &P, cg::grid_group &grid
                 else
                     tile_keys<K, RPT>(cur_base, b_lo, nr, H - seg_lo, gp, cc, lane, key);
                 int32_t *dst = nxt_base + b_lo + lane;
+                const bool pack = publish && b_lo + RPT * 32 > pub_lo;
 #pragma unroll
-                for (int r = 0; r < RPT; ++r)
-                    if (r < nr) dst[r * 32] = key[r] & ~15;
+                for (int r = 0; r < RPT; ++r) {
+                    const int32_t v = key[r] & ~15;
+                    if (r < nr) dst[r * 32] = v;
+                    const int32_t b = b_lo + r * 32 + lane;
+                    if (pack && b >= pub_lo) stg[b - pub_lo] = ((unsigned long long)pub_tag << 32) | (uint32_t)v;
+                }
                 gch[((int64_t)i * gtiles + t) * 32 + lane] = pack_choices<RPT, CB>(key);
             };
-            // halo of S_{i+1} from CTA j-1 (its step f-1); step 0 reads S_N = 0 (already set).
-            // Executed by one warp (the leader lane polls).
-            const bool need_halo = (j > 0 && f > 0 && hl > 0) && !(P.debug & 1);
-            // Halo exchange through the L2 ring with the Tensor Memory Accelerator: every ring element
-            // is one 64-bit word {value, step tag}. The publisher packs its top cells into a smem
-            // stage and issues ONE bulk store (cp.async.bulk global <- shared); the consumer issues
-            // ONE bulk load into its own stage (mbarrier completion) and checks the tags -- a stale
-            // tag (publication still in flight) just re-issues the copy. No fence, no flag word.
-            const int32_t hl8 = (hl + 1) & ~1;                         // 16-byte multiple of 8-B words
-            const unsigned long long *halo_src =
-                X.ring + ((int64_t)((step_base + f - 1) % D) * GRID_MAX_CTAS + (j - 1)) * H;
-            auto issue_halo = [&]() {                                 // async: TMA load of the slot
-                if (lane == 0) tma_load_1d(stage_in, halo_src, hl8 * 8, mbar);
-            };
-            auto fetch_halo = [&](bool issued) {
-                const uint32_t tag = (uint32_t)(step_base + f);          // j-1's step f-1 publishes tag sb+f
-                bool ok = false;
-                for (int attempt = 0; attempt < (1 << 16) && !ok; ++attempt) {
-                    if (!issued || attempt > 0) issue_halo();
-                    if (lane == 0) mbar_wait(mbar, mbar_phase);
-                    mbar_phase ^= 1u;
-                    __syncwarp();
-                    bool mine_ok = true;
-                    for (int32_t x = lane; x < hl8; x += 32) mine_ok &= (uint32_t)(stage_in[x] >> 32) == tag;
-                    ok = __all_sync(0xffffffffu, mine_ok);
-                    if (!ok) {
-                        if ((P.debug & 2) && lane == 0) X.trace[(int64_t)j * 8 + 6] += 1;
-                        __nanosleep(256);
-                    }
-                }
-                if (!ok && lane == 0) atomic_min_i64(&P.status[1], w);
-                for (int32_t x = lane; x < hl8; x += 32) cur[H - hl8 + x] = (int32_t)(uint32_t)stage_in[x];
-            };
-            auto release_halo_slot = [&]() {                               // back-pressure only
-                if (lane == 0) st_relaxed_u32(&X.con[j], step_base + f);
-            };
-            // publish the top hl8 cells of S_i for CTA j+1 (ring slot back-pressured)
-            const bool publish = (j + 1 < active && hl > 0) && !(P.debug & 1);
-            auto do_publish = [&]() {
-                const int32_t slot_step = step_base + f;
-                if (lane == 0) {
+            auto ship = [&]() {                                        // after the stage is complete
+                if (tid == 0) {
+                    const int32_t slot_step = step_base + f;
                     if (f >= D && !wait_at_least(&X.con[j + 1], slot_step - D + 1)) atomic_min_i64(&P.status[1], w);
-                    tma_store_wait_read();                                 // previous store has read the stage
-                }
-                __syncwarp();
-                const unsigned long long tag = (unsigned long long)(uint32_t)(slot_step + 1) << 32;
-                for (int32_t x = lane; x < hl8; x += 32) stage_out[x] = tag | (uint32_t)nxt[H + seg - hl8 + x];
-                fence_proxy_async();                                       // generic smem writes -> TMA
-                __syncwarp();
-                if (lane == 0) {
                     unsigned long long *dst = X.ring + ((int64_t)(slot_step % D) * GRID_MAX_CTAS + j) * H;
-                    tma_store_1d(dst, stage_out, hl8 * 8);
+                    tma_store_1d(dst, stg, hl8 * 8);
                 }
             };
             const int32_t n_edge = (hl + 32 * RPT - 1) / (32 * RPT);   // tiles within hl of an edge
             const int32_t bot_end = min(t_end, t_first + n_edge);        // tiles that read the halo
             const int32_t top_lo = t_end - n_edge;                       // tiles holding published cells
             const bool split = top_lo >= bot_end;                        // top tiles never need the halo
-            // Warp specialisation: warps 0..C-1 compute tiles, warp C (the last) exchanges halos.
-            // Named barriers (ids by step parity; 0 is __syncthreads): TOP = compute warps have
-            // written the published cells (arrive) -> comm warp publishes (sync); HALO = comm warp
-            // has fetched the halo (arrive) -> compute warps may do the bottom tiles (sync);
-            // STEP = compute warps only, S_i complete before the buffers swap.
-            const int C = nwarps - 1;
-            const int par = f & 1;
-            const int bar_top = 1 + par, bar_halo = 3 + par, bar_step = 5;
-            const bool trace = (P.debug & 2) != 0;
-            long long *tr = X.trace + (int64_t)j * 8;
-            long long t_a = trace ? clock64() : 0;
-            if (warp < C) {
-                const int32_t n_pre = split ? t_end - bot_end : 0;      // top first, then the middle
-                bool arrived = false;
-                if (split && n_edge <= warp) {
-                    named_arrive(bar_top, nthr);
-                    arrived = true;
+            if (split) {
+                // top tiles first and shipped at once, then the middle while the halo lands
+                for (int32_t t = t_end - 1 - warp; t >= top_lo; t -= nwarps) do_tile(t);
+                if (publish) {
+                    fence_proxy_async();                               // stage writes -> TMA reads
+                    __syncthreads();
+                    ship();
                 }
-                for (int32_t idx = warp; idx < n_pre; idx += C) {
-                    do_tile(t_end - 1 - idx);
-                    if (!arrived && idx + C >= n_edge) {
-                        __threadfence_block();
-                        named_arrive(bar_top, nthr);
-                        arrived = true;
-                    }
-                }
-                long long t_b = trace ? clock64() : 0;
-                named_sync(bar_halo, nthr);
-                if (trace && tid == 0) tr[1] += clock64() - t_b;
-                for (int32_t t = (split ? bot_end : t_end) - 1 - warp; t >= t_first; t -= C) do_tile(t);
-                if (!arrived) {
-                    __threadfence_block();
-                    named_arrive(bar_top, nthr);
-                }
-                t_b = trace ? clock64() : 0;
-                named_sync(bar_step, C * 32);
-                if (trace && tid == 0) {
-                    tr[2] += clock64() - t_b;
-                    tr[0] += clock64() - t_a;
-                    tr[7] += 1;
-                }
-            } else if (split) {
-                // the halo (published a step ago, normally already in L2) is requested at once and
-                // lands while we wait for our top tiles and publish them
-                if (need_halo) issue_halo();
-                named_sync(bar_top, nthr);
-                long long t_c = trace ? clock64() : 0;
-                if (trace && lane == 0) tr[3] += t_c - t_a;
-                if (publish) do_publish();
-                long long t_d = trace ? clock64() : 0;
-                if (trace && lane == 0) tr[4] += t_d - t_c;
-                if (need_halo) fetch_halo(true);
-                if (trace && lane == 0) tr[5] += clock64() - t_d;
-                __threadfence_block();
-                named_arrive(bar_halo, nthr);
-                if (need_halo) release_halo_slot();
-            } else {
-                // short segment: every tile may read the halo, so it must come first
-                if (need_halo) fetch_halo(false);
-                __threadfence_block();
-                named_arrive(bar_halo, nthr);
-                if (need_halo) release_halo_slot();
-                named_sync(bar_top, nthr);
-                if (publish) do_publish();
+                for (int32_t t = top_lo - 1 - warp; t >= bot_end; t -= nwarps) do_tile(t);
             }
+            if (need_halo) {
+                bool ok = false;
+                for (int attempt = 0; attempt < (1 << 16) && !ok; ++attempt) {
+                    if (attempt > 0) {
+                        __nanosleep(256);
+                        if (tid == 0) tma_load_1d(stage_in, halo_src, hl8 * 8, mbar);
+                    }
+                    mbar_wait(mbar, mbar_phase);
+                    mbar_phase ^= 1u;
+                    bool stale = false;
+                    for (int32_t x = tid; x < hl8; x += nthr) stale |= (uint32_t)(stage_in[x] >> 32) != (uint32_t)(step_base + f);
+                    ok = !__syncthreads_or(stale);
+                }
+                if (!ok && tid == 0) atomic_min_i64(&P.status[1], w);
+                for (int32_t x = tid; x < hl8; x += nthr) cur[H - hl8 + x] = (int32_t)(uint32_t)stage_in[x];
+                __syncthreads();
+                if (tid == 0) st_relaxed_u32(&X.con[j], step_base + f);      // slot consumed
+            }
+            for (int32_t t = (split ? bot_end : t_end) - 1 - warp; t >= t_first; t -= nwarps) do_tile(t);
+            if (!split && publish) {                                   // short segment: ship last
+                fence_proxy_async();
+                __syncthreads();
+                ship();
+            }
+            // the stage of step f-1 must have been read before step f+1 overwrites it
+            if (tid == 0) tma_store_wait_read_1();
+            __syncthreads();                                           // S_i complete before the swap
         }
         int32_t *tmp = cur;
         cur = nxt;
         nxt = tmp;
     }
-    if (warp == nwarps - 1 && lane == 0) tma_store_wait_all();   // last publication has left smem
+    if (tid == 0) tma_store_wait_all();                // every publication has left shared memory
     __syncthreads();                                   // compute and comm warps leave the frame loop
     step_base += N;
 
@@ -461,8 +412,8 @@ __global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg
     int32_t *bufA = reinterpret_cast<int32_t *>(smem_raw) + 32;
     int32_t *bufB = bufA + TURBO_BIG_MAX_COST + seg_max;
     unsigned long long *stage_in = reinterpret_cast<unsigned long long *>(bufB + TURBO_BIG_MAX_COST + seg_max);
-    unsigned long long *stage_out = stage_in + TURBO_BIG_MAX_COST;
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(stage_out + TURBO_BIG_MAX_COST);
+    unsigned long long *stage_out = stage_in + TURBO_BIG_MAX_COST;          // two stages (parity)
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(stage_out + 2 * TURBO_BIG_MAX_COST);
     uint32_t mbar_phase = 0;
     if (threadIdx.x == 0) mbar_init(mbar, 1);
     __syncthreads();
@@ -521,7 +472,7 @@ cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams 
     int32_t seg = (int32_t)(((int64_t)shape->max_budget + 1 + NP - 1) / NP);
     seg = (seg + 511) & ~511;
     if (seg < TURBO_BIG_MAX_COST) seg = TURBO_BIG_MAX_COST;
-    const size_t smem = 128 + (size_t)8 * (TURBO_BIG_MAX_COST + seg) + (size_t)16 * TURBO_BIG_MAX_COST + 16;
+    const size_t smem = 128 + (size_t)8 * (TURBO_BIG_MAX_COST + seg) + (size_t)24 * TURBO_BIG_MAX_COST + 16;
     if (smem > (size_t)smem_per_cta_max) return cudaErrorInvalidConfiguration;
     dp_grid_kernel_t kern = mode == DP_PLAN ? pick_grid<DP_PLAN>(shape->min_exits, shape->max_exits)
                                             : pick_grid<DP_SOLVE_GLOBAL>(shape->min_exits, shape->max_exits);
