@@ -436,6 +436,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
         return;
     }
 
+    if (P.debug & 64) return;                         // timing: prologue only
     // choice-plane stride (tiles per frame): the layout bound for HBM planes, exact for smem
     const int32_t gtiles = (int32_t)(((Bb + 32) >> 5) + RPT - 1) / RPT;
     uint32_t *__restrict__ gch = reinterpret_cast<uint32_t *>(P.workspace + choff);
@@ -596,6 +597,7 @@ __global__ void __launch_bounds__(512, (KSEL == 0) ? 1 : 2) dp_cta_kernel(DpPara
         if (nwarps > 1) rowB[x - P.pad_words] = NEG_R;
     }
     __syncthreads();
+    if (P.debug & 32) return;                         // timing: launch only
     for (int64_t w = blockIdx.x; w < P.num_windows; w += gridDim.x) {
         const int rc = row_class((int64_t)P.windows[w].budget_bound + 1);
         if (rc >= TURBO_NUM_CLASSES || (P.cls >= 0 && rc != P.cls)) continue;   // other launch serves it
