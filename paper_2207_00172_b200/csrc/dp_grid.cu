@@ -122,11 +122,12 @@ __device__ __forceinline__ int ld_relaxed_gpu(const int *p)
 // load suffices -- an acquire would invalidate the SM's L1 on every poll and slow the compute
 // warps' local-memory traffic). Bounded (~seconds): a lost update must not hang the GPU; on
 // timeout the caller flags the window (status[1]) and carries on, so the kernel always exits.
-__device__ __forceinline__ bool wait_at_least(const int *p, int target)
+__device__ __forceinline__ bool wait_at_least(const int *p, int target, int &seen)
 {
     for (long long it = 0; it < (1ll << 22); ++it) {
-        if (ld_relaxed_gpu(p) >= target) return true;
-        __nanosleep(256);                  // the comm warp shares its SMSP with compute warps
+        seen = ld_relaxed_gpu(p);
+        if (seen >= target) return true;
+        __nanosleep(256);
     }
     return false;
 }
@@ -134,6 +135,18 @@ __device__ __forceinline__ bool wait_at_least(const int *p, int target)
 __device__ __forceinline__ void named_sync(int id, int n)
 {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// named barrier with an OR reduction of a predicate over the participating threads
+__device__ __forceinline__ bool named_sync_or(int id, int n, bool v)
+{
+    uint32_t r;
+    asm volatile(
+        "{\n .reg .pred p, q;\n setp.ne.u32 p, %1, 0;\n bar.red.or.pred q, %2, %3, p;\n selp.u32 %0, 1, 0, q;\n}\n"
+        : "=r"(r)
+        : "r"((uint32_t)v), "r"(id), "r"(n)
+        : "memory");
+    return r != 0;
 }
 
 __device__ __forceinline__ void named_arrive(int id, int n)
@@ -163,9 +176,9 @@ struct GridCtx {
 };
 
 template <int K, int MODE>
-__device__ __noinline__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, int32_t *bufA, int32_t *bufB,
+__device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, int32_t *bufA, int32_t *bufB,
                            long long *red, GridCtx X, int &step_base, unsigned long long *stage_in,
-                           unsigned long long *stage_out, uint64_t *mbar, uint32_t &mbar_phase)
+                           unsigned long long *stage_out, uint64_t *mbar, uint32_t *mbar_uses)
 {
     constexpr int CB = (K <= 4) ? 2 : 4;
     constexpr int RPT = 32 / CB;
@@ -258,9 +271,9 @@ __device__ __noinline__ void grid_window(const DpParams &P, cg::grid_group &grid
     }
     __syncthreads();
 
-    int32_t my_gp = 0, my_c = 0;
+    int32_t my_g = 0, my_c = 0;                       // lane k < K: option k of the next frame (raw)
     if (N > 0 && lane < K) {
-        my_gp = (__ldg(og + (int64_t)(N - 1) * K + lane) << 4) | (15 - lane);
+        my_g = __ldg(og + (int64_t)(N - 1) * K + lane);
         my_c = __ldg(oc + (int64_t)(N - 1) * K + lane);
     }
     int32_t *cur = bufA, *nxt = bufB;
@@ -268,110 +281,195 @@ __device__ __noinline__ void grid_window(const DpParams &P, cg::grid_group &grid
     const int32_t t_end = min((int32_t)((seg_lo + seg) / (32 * RPT)), (nrows + RPT - 1) / RPT);
     int key[RPT];
 
+    // Step schedule. Tiles are numbered q = 0, 1, ... from the top of the segment down; warp w
+    // takes q = w, w + G, ... (round r = q / G). The top n_edge tiles hold the published cells,
+    // the bottom n_edge tiles read the halo. "Piped" (every segment of a long row): no CTA
+    // barrier inside a step --
+    //  * the warps of the top tiles (all in round 0) pack their cells into the stage and arrive
+    //    on named barrier 2; the ship warp (no top tile, no halo reader) waits there and ships;
+    //  * the warps of the bottom tiles (all in the last round) wait for the halo together
+    //    (named barrier 1) right before computing them; every other warp keeps computing.
+    // Otherwise (short segments): halo first, then every tile, then a CTA barrier and the ship.
+    const int32_t ntl = max(0, t_end - t_first);
+    const int32_t n_edge = (hl + 32 * RPT - 1) / (32 * RPT);
+    const int32_t n_top = min(ntl, n_edge);
+    const int32_t q_bot0 = max(0, ntl - n_edge);
+    const int32_t rounds = (ntl + nwarps - 1) / nwarps;
+    const int32_t rb = q_bot0 / nwarps;
+    const int32_t wb_lo = q_bot0 - rb * nwarps;
+    const int32_t group_threads = (ntl - rb * nwarps - wb_lo) * 32;
+    const bool in_group = warp >= wb_lo && warp - wb_lo < group_threads / 32;
+    const int ship_warp = nwarps - 1;
+    const bool ship_in_group = ship_warp >= wb_lo && ship_warp - wb_lo < group_threads / 32;
+    const bool piped = n_top <= nwarps && q_bot0 >= n_top && rounds - 1 == rb && ship_warp >= n_top &&
+                       !ship_in_group && n_top > 0;
+    const int top_threads = (n_top + 1) * 32;                  // top warps + the ship warp
+    // helper warps: no tile in the last round (and not the ship warp). They take the halo at
+    // step start, while round 0 computes, and release the halo readers through barrier 3.
+    const int32_t hw_lo = ntl - (rounds - 1) * nwarps;
+    const int n_help = piped ? max(0, (nwarps - 1) - hw_lo) : 0;
+    const bool is_helper = n_help > 0 && warp >= hw_lo && warp < nwarps - 1;
+    const int join_threads = (n_help + group_threads / 32) * 32;
+    const int ship_tid = ship_warp * 32;
+    int con_seen = 0;                                 // ship thread: last consumer count seen
+
+    const int32_t sb = step_base;                     // ring tag base (register copy)
+    const bool exch = !(P.debug & 1);                 // timing switch: no halo exchange
+    const bool trace = (P.debug & 2) != 0;            // cycle counters in X.trace (grid_trace.py)
+    int64_t *const status = P.status;
     for (int32_t f = 0; f < N; ++f) {
         const int32_t i = N - 1 - f;
         int32_t gp[K], cc[K];
 #pragma unroll
         for (int k = 0; k < K; ++k) {
-            gp[k] = __shfl_sync(0xffffffffu, my_gp, k);
+            gp[k] = (__shfl_sync(0xffffffffu, my_g, k) << 4) | (15 - k);
             cc[k] = __shfl_sync(0xffffffffu, my_c, k);
         }
-        if (i > 0 && lane < K) {
-            my_gp = (__ldg(og + (int64_t)(i - 1) * K + lane) << 4) | (15 - lane);
+        if (i > 0 && lane < K) {                       // consumed one frame later (no stall here)
+            my_g = __ldg(og + (int64_t)(i - 1) * K + lane);
             my_c = __ldg(oc + (int64_t)(i - 1) * K + lane);
         }
+        const long long c_step = trace ? clock64() : 0;
         if (mine) {
             const int32_t *cur_base = cur + H - seg_lo;
             int32_t *nxt_base = nxt + H - seg_lo;
-            const bool need_halo = (j > 0 && f > 0 && hl > 0) && !(P.debug & 1);
-            const bool publish = (j + 1 < active && hl > 0) && !(P.debug & 1);
+            const bool need_halo = (j > 0 && f > 0 && hl > 0) && exch;
+            const bool publish = (j + 1 < active && hl > 0) && exch;
             // Halo exchange through the L2 ring with the Tensor Memory Accelerator. Ring words are
             // 64-bit {value, step tag}: the tag proves a word is current, so neither side needs a
             // fence or a flag. The published cells (the top hl8 of S_i) are packed by the warps
             // that compute them; thread 0 ships them with ONE bulk store; thread 0 requests the
-            // halo with ONE bulk load at step start (mbarrier completion) and every thread later
-            // checks a slice of the tags and unpacks it (a stale slot just re-issues the load).
+            // halo with ONE bulk load at step start (mbarrier completion) and the consumers later
+            // check the tags and unpack it (a stale slot just re-issues the load).
             const int32_t hl8 = (hl + 1) & ~1;                         // 16-byte multiple of 8-B words
-            const uint32_t pub_tag = (uint32_t)(step_base + f + 1);
+            const uint32_t pub_tag = (uint32_t)(sb + f + 1);
             const int32_t pub_lo = seg_lo + seg - hl8;                 // first published cell
             unsigned long long *stg = stage_out + (f & 1) * H;         // two publication stages
             const unsigned long long *halo_src =
-                X.ring + ((int64_t)((step_base + f - 1) % D) * GRID_MAX_CTAS + (j - 1)) * H;
+                X.ring + ((int64_t)((sb + f - 1) % D) * GRID_MAX_CTAS + (j - 1)) * H;
             if (need_halo && tid == 0) tma_load_1d(stage_in, halo_src, hl8 * 8, mbar);
             auto do_tile = [&](int32_t t) {
                 const int32_t b_lo = t * RPT * 32;
                 const int32_t nr = min(RPT, nrows - t * RPT);
-                if (nr == RPT)
-                    tile_keys_fast<K, RPT>(cur_base + lane, b_lo, gp, cc, key);
-                else
-                    tile_keys<K, RPT>(cur_base, b_lo, nr, H - seg_lo, gp, cc, lane, key);
-                int32_t *dst = nxt_base + b_lo + lane;
                 const bool pack = publish && b_lo + RPT * 32 > pub_lo;
+                int32_t *dst = nxt_base + b_lo + lane;
+                if (nr == RPT && !pack) {                              // interior tile: no checks
+                    tile_keys_fast<K, RPT>(cur_base + lane, b_lo, gp, cc, key);
 #pragma unroll
-                for (int r = 0; r < RPT; ++r) {
-                    const int32_t v = key[r] & ~15;
-                    if (r < nr) dst[r * 32] = v;
-                    const int32_t b = b_lo + r * 32 + lane;
-                    if (pack && b >= pub_lo) stg[b - pub_lo] = ((unsigned long long)pub_tag << 32) | (uint32_t)v;
+                    for (int r = 0; r < RPT; ++r) dst[r * 32] = key[r] & ~15;
+                } else {
+                    if (nr == RPT)
+                        tile_keys_fast<K, RPT>(cur_base + lane, b_lo, gp, cc, key);
+                    else
+                        tile_keys<K, RPT>(cur_base, b_lo, nr, H - seg_lo, gp, cc, lane, key);
+#pragma unroll
+                    for (int r = 0; r < RPT; ++r) {
+                        const int32_t v = key[r] & ~15;
+                        if (r < nr) dst[r * 32] = v;
+                        const int32_t b = b_lo + r * 32 + lane;
+                        if (pack && b >= pub_lo) stg[b - pub_lo] = ((unsigned long long)pub_tag << 32) | (uint32_t)v;
+                    }
                 }
                 gch[((int64_t)i * gtiles + t) * 32 + lane] = pack_choices<RPT, CB>(key);
             };
-            auto ship = [&]() {                                        // after the stage is complete
-                if (tid == 0) {
-                    const int32_t slot_step = step_base + f;
-                    if (f >= D && !wait_at_least(&X.con[j + 1], slot_step - D + 1)) atomic_min_i64(&P.status[1], w);
+            auto ship = [&]() {                                        // the stage is complete
+                if (tid == ship_tid) {
+                    const long long c0 = trace ? clock64() : 0;
+                    const int32_t slot_step = sb + f;
+                    // back-pressure: the consumer must have taken the slot's previous content; the
+                    // last value seen usually still proves it, so the L2 poll is rare
+                    if (f >= D && con_seen < slot_step - D + 1 &&
+                        !wait_at_least(&X.con[j + 1], slot_step - D + 1, con_seen))
+                        atomic_min_i64(&status[1], w);
                     unsigned long long *dst = X.ring + ((int64_t)(slot_step % D) * GRID_MAX_CTAS + j) * H;
                     tma_store_1d(dst, stg, hl8 * 8);
+                    if (trace) X.trace[j * 8 + 2] += clock64() - c0;
                 }
             };
-            const int32_t n_edge = (hl + 32 * RPT - 1) / (32 * RPT);   // tiles within hl of an edge
-            const int32_t bot_end = min(t_end, t_first + n_edge);        // tiles that read the halo
-            const int32_t top_lo = t_end - n_edge;                       // tiles holding published cells
-            const bool split = top_lo >= bot_end;                        // top tiles never need the halo
-            if (split) {
-                // top tiles first and shipped at once, then the middle while the halo lands
-                for (int32_t t = t_end - 1 - warp; t >= top_lo; t -= nwarps) do_tile(t);
+            // wait for the halo, check its tags, unpack it into the row buffer (group = the
+            // consumers: the halo-reading warps (named barrier 1) or the whole CTA)
+            auto consume = [&](bool group, int gtid, int gn) {
+                uint32_t uses = *mbar_uses;                            // loads completed so far
+                const long long c0 = trace ? clock64() : 0;
+                bool ok = false;
+                int attempt = 0;
+                for (; attempt < (1 << 16) && !ok; ++attempt) {
+                    if (attempt > 0) {
+                        __nanosleep(128);
+                        if (gtid == 0) tma_load_1d(stage_in, halo_src, hl8 * 8, mbar);
+                    }
+                    const long long cw = trace ? clock64() : 0;
+                    mbar_wait(mbar, uses & 1u);
+                    if (trace && gtid == 0) X.trace[j * 8 + 4] += clock64() - cw;
+                    ++uses;
+                    // unpack and check the tags in one pass (a stale word just repeats the load)
+                    bool stale = false;
+                    for (int32_t x = gtid; x < hl8; x += gn) {
+                        const unsigned long long u = stage_in[x];
+                        stale |= (uint32_t)(u >> 32) != (uint32_t)(sb + f);
+                        cur[H - hl8 + x] = (int32_t)(uint32_t)u;
+                    }
+                    ok = !(group ? named_sync_or(1, gn, stale) : __syncthreads_or(stale));
+                }
+                if (!ok && gtid == 0) atomic_min_i64(&status[1], w);
+                if (trace && gtid == 0) {
+                    X.trace[j * 8 + 0] += attempt - 1;
+                    X.trace[j * 8 + 1] += clock64() - c0;
+                    X.trace[j * 8 + 5] += c0 - c_step;                 // step start -> consume
+                }
+                if (gtid == 0) {
+                    st_relaxed_u32(&X.con[j], sb + f);          // slot consumed
+                    *mbar_uses = uses;
+                }
+            };
+            if (piped) {
+                if (need_halo && is_helper) {
+                    consume(true, tid - hw_lo * 32, n_help * 32);
+                    named_arrive(3, join_threads);
+                }
+                for (int32_t r = 0; r < rounds; ++r) {
+                    const int32_t q = r * nwarps + warp;
+                    if (q < ntl) {
+                        if (r == rb && need_halo && in_group) {
+                            if (n_help > 0)
+                                named_sync(3, join_threads);
+                            else
+                                consume(true, tid - wb_lo * 32, group_threads);
+                        }
+                        do_tile(t_end - 1 - q);
+                        if (q < n_top && publish) {                    // stage writes -> TMA reads
+                            fence_proxy_async();
+                            named_arrive(2, top_threads);
+                        }
+                    }
+                    if (r == 0 && warp == ship_warp && publish) {
+                        named_sync(2, top_threads);
+                        ship();
+                    }
+                }
+            } else {
+                if (need_halo) consume(false, tid, nthr);
+                for (int32_t q = warp; q < ntl; q += nwarps) do_tile(t_end - 1 - q);
                 if (publish) {
-                    fence_proxy_async();                               // stage writes -> TMA reads
+                    fence_proxy_async();
                     __syncthreads();
                     ship();
                 }
-                for (int32_t t = top_lo - 1 - warp; t >= bot_end; t -= nwarps) do_tile(t);
-            }
-            if (need_halo) {
-                bool ok = false;
-                for (int attempt = 0; attempt < (1 << 16) && !ok; ++attempt) {
-                    if (attempt > 0) {
-                        __nanosleep(256);
-                        if (tid == 0) tma_load_1d(stage_in, halo_src, hl8 * 8, mbar);
-                    }
-                    mbar_wait(mbar, mbar_phase);
-                    mbar_phase ^= 1u;
-                    bool stale = false;
-                    for (int32_t x = tid; x < hl8; x += nthr) stale |= (uint32_t)(stage_in[x] >> 32) != (uint32_t)(step_base + f);
-                    ok = !__syncthreads_or(stale);
-                }
-                if (!ok && tid == 0) atomic_min_i64(&P.status[1], w);
-                for (int32_t x = tid; x < hl8; x += nthr) cur[H - hl8 + x] = (int32_t)(uint32_t)stage_in[x];
-                __syncthreads();
-                if (tid == 0) st_relaxed_u32(&X.con[j], step_base + f);      // slot consumed
-            }
-            for (int32_t t = (split ? bot_end : t_end) - 1 - warp; t >= t_first; t -= nwarps) do_tile(t);
-            if (!split && publish) {                                   // short segment: ship last
-                fence_proxy_async();
-                __syncthreads();
-                ship();
             }
             // the stage of step f-1 must have been read before step f+1 overwrites it
-            if (tid == 0) tma_store_wait_read_1();
+            if (tid == ship_tid) tma_store_wait_read_1();
             __syncthreads();                                           // S_i complete before the swap
+            if (trace && tid == 0) {
+                X.trace[j * 8 + 3] += clock64() - c_step;
+                X.trace[j * 8 + 7] += 1;
+            }
         }
         int32_t *tmp = cur;
         cur = nxt;
         nxt = tmp;
     }
-    if (tid == 0) tma_store_wait_all();                // every publication has left shared memory
-    __syncthreads();                                   // compute and comm warps leave the frame loop
+    if (tid == ship_tid) tma_store_wait_all();         // every publication has left shared memory
+    __syncthreads();
     step_base += N;
 
     // ---- a4: G* = S_0[B] (owned by the last active CTA), C* = #{b <= B : S_0[b] < G*}
@@ -399,8 +497,18 @@ __device__ __noinline__ void grid_window(const DpParams &P, cg::grid_group &grid
         for (int32_t i = j * nthr + tid; i < N; i += NP * nthr) P.exit_out[ff + i] = 0;
     } else if (j == 0 && warp == 0) {
         auto cost = [&](int32_t i, int32_t k) -> int32_t { return __ldg(oc + (int64_t)i * K + k); };
-        backtrack_warp<K, DP_SOLVE_GLOBAL>(N, Cst, nullptr, gch, 0, gtiles, cost, P.exit_out + ff, nullptr, lane);
+        backtrack_warp_spec<K, DP_SOLVE_GLOBAL>(N, Cst, nullptr, gch, 0, gtiles, cost, P.exit_out + ff, nullptr, lane);
     }
+}
+
+// Out-of-line instance per K for the mixed-K kernel (compile time); fixed-K kernels inline it.
+template <int K, int MODE>
+__device__ __noinline__ void grid_window_call(const DpParams &P, cg::grid_group &grid, int64_t w, int32_t *bufA,
+                                              int32_t *bufB, long long *red, GridCtx X, int &step_base,
+                                              unsigned long long *stage_in, unsigned long long *stage_out,
+                                              uint64_t *mbar, uint32_t *mbar_uses)
+{
+    grid_window<K, MODE>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar, mbar_uses);
 }
 
 template <int KSEL, int MODE>
@@ -414,8 +522,11 @@ __global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg
     unsigned long long *stage_in = reinterpret_cast<unsigned long long *>(bufB + TURBO_BIG_MAX_COST + seg_max);
     unsigned long long *stage_out = stage_in + TURBO_BIG_MAX_COST;          // two stages (parity)
     uint64_t *mbar = reinterpret_cast<uint64_t *>(stage_out + 2 * TURBO_BIG_MAX_COST);
-    uint32_t mbar_phase = 0;
-    if (threadIdx.x == 0) mbar_init(mbar, 1);
+    uint32_t *mbar_uses = reinterpret_cast<uint32_t *>(mbar + 1);           // completed halo loads
+    if (threadIdx.x == 0) {
+        mbar_init(mbar, 1);
+        *mbar_uses = 0;
+    }
     __syncthreads();
     int *flags = reinterpret_cast<int *>(P.workspace + P.grid_scratch_offset);
     GridCtx X;
@@ -429,11 +540,11 @@ __global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg
         if ((int64_t)P.windows[w].budget_bound + 1 <= TURBO_BIG_CELLS) continue;
         if (KSEL != 0) {
             grid_window<(KSEL > 0 ? KSEL : 2), MODE>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar,
-                                                     mbar_phase);
+                                                     mbar_uses);
         } else {
             switch (P.windows[w].num_exits) {
 #define TURBO_K_CASE(KK) \
-    case KK: grid_window<KK, MODE>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar, mbar_phase); \
+    case KK: grid_window_call<KK, MODE>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar, mbar_uses); \
         break;
                 TURBO_K_CASE(2) TURBO_K_CASE(3) TURBO_K_CASE(4) TURBO_K_CASE(5) TURBO_K_CASE(6)
                 TURBO_K_CASE(7) TURBO_K_CASE(8) TURBO_K_CASE(9) TURBO_K_CASE(10) TURBO_K_CASE(11)

@@ -159,9 +159,133 @@ __device__ __forceinline__ void dp_tile(const DpParams &P, int32_t t, int32_t i,
         gch[((int64_t)i * gtiles + t) * 32 + lane] = word;
 }
 
-// OSM: the window's options staged in shared memory as packed (g << 4 | 15 - k, c) pairs and read
-// with broadcast LDS.64; otherwise lane k holds option k (prefetched a frame ahead) and the warp
-// broadcasts it with shuffles (windows whose option table does not fit).
+// a5 of the standalone and long-window backtracks (choice planes in HBM, costs from the option
+// table): one warp walks the planes from (frame 0, b = C*) and resolves D frames per dependent
+// round trip.
+// Speculation: lane q is a CANDIDATE prefix (p_0 .. p_{d-1}) of d < D choices (q = 0: the empty
+// prefix; then the K one-frame prefixes, the K^2 two-frame ones, ...). Costs do not depend on b,
+// so each lane knows its cells b_j = b - sum_{l<j} c_{i+l, p_l} before the round, reads the
+// choices at all of them at once, and decides ON ITS OWN whether its prefix is the realised one
+// (every p_j equals the choice read at b_j). The realised deepest candidate holds the round:
+// one ballot and two shuffles hand its exits and its cost to the warp. Costs are loaded one
+// round ahead, so the only dependent latency per round is one choice read + ballot + shuffle.
+// (Inside the DP kernels the walk shares the SM's load/store pipe with other CTAs' DP and its
+// extra loads cost more than the shorter chain saves: there backtrack_warp below is used.)
+template <int K>
+struct BtGeom {
+    static constexpr int D = (K == 2) ? 5 : (K <= 5 ? 3 : 2);   // sum_{j<D} K^j <= 32
+};
+
+template <int K, int MODE, class CostF>
+__device__ __forceinline__ void backtrack_warp_spec(int32_t N, int32_t b, const uint32_t *__restrict__ sch,
+                                                    const uint32_t *__restrict__ gch, int32_t ntiles,
+                                                    int32_t gtiles, CostF cost, uint8_t *__restrict__ exit_g,
+                                                    uint8_t *__restrict__ exit_s, int lane)
+{
+    constexpr int CB = (K <= 4) ? 2 : 4;
+    constexpr int RPT = 32 / CB;
+    constexpr uint32_t CMASK = (1u << CB) - 1u;
+    constexpr int D = BtGeom<K>::D;
+    // decode the lane's candidate: depth d (-1: idle lane) and digits (4 bits each, frame i first)
+    int d = -1;
+    uint32_t dig = 0;
+    {
+        int q = lane, pw = 1;
+#pragma unroll
+        for (int dd = 0; dd < D; ++dd) {
+            if (d < 0) {
+                if (q < pw) {
+                    d = dd;
+                    int r = q;
+                    for (int j = dd - 1; j >= 0; --j) {
+                        dig |= (uint32_t)(r % K) << (4 * j);
+                        r /= K;
+                    }
+                } else {
+                    q -= pw;
+                }
+            }
+            pw *= K;
+        }
+    }
+    auto choice = [&](int32_t i, int32_t cell) -> int32_t {
+        const int32_t t = cell / (32 * RPT);
+        const int32_t j = (cell >> 5) & (RPT - 1);
+        const uint32_t word = (MODE == DP_SOLVE_SMEM) ? sch[(i * ntiles + t) * 32 + (cell & 31)]
+                                                      : gch[((int64_t)i * gtiles + t) * 32 + (cell & 31)];
+        return (int32_t)((word >> choice_shift(j, CB)) & CMASK);
+    };
+    // costs of round starting at frame i0: the prefix costs and every cost of frame i0 + d
+    auto load_costs = [&](int32_t i0, int32_t (&pcv)[D], int32_t (&lcv)[K]) {
+#pragma unroll
+        for (int j = 0; j < D - 1; ++j)
+            pcv[j] = (j < d && i0 + j < N) ? cost(i0 + j, (int)((dig >> (4 * j)) & 15u)) : 0;
+        pcv[D - 1] = 0;
+        const bool last = d >= 0 && i0 + d < N;
+#pragma unroll
+        for (int k = 0; k < K; ++k) lcv[k] = last ? cost(i0 + d, k) : 0;
+    };
+    // one round at frame i with this round's costs (pcv, lcv); prefetches the next round's into
+    // (pcn, lcn). Returns false when the walk is over.
+    auto round = [&](int32_t i, const int32_t (&pcv)[D], const int32_t (&lcv)[K], int32_t (&pcn)[D],
+                     int32_t (&lcn)[K]) -> bool {
+        const int32_t dm = min(D, N - i);
+        if (i + D < N) load_costs(i + D, pcn, lcn);           // next round's costs, off the chain
+        // the choices at every cell of the lane's prefix: D unconditional loads (clamped to a
+        // valid cell and frame) so they are all in flight at once
+        int32_t kv[D];
+        int32_t bj = b, bd = b;
+        bool neg = false;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            kv[j] = choice(min(i + j, N - 1), max(bj, 0));
+            if (j <= d) neg |= bj < 0;
+            if (j == d) bd = bj;
+            if (j < D - 1 && j < d) bj -= pcv[j];
+        }
+        bool on = d >= 0 && d == dm - 1 && !neg;
+        int32_t kd = 0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            if (j < d) on = on && kv[j] == (int32_t)((dig >> (4 * j)) & 15u);
+            if (j == d) kd = kv[j];
+        }
+        int32_t lk = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) lk = (k == kd) ? lcv[k] : lk;
+        const unsigned mask = __ballot_sync(0xffffffffu, on);
+        const int src = (__ffs(mask) - 1) & 31;
+        const uint32_t packed = __shfl_sync(0xffffffffu, dig | ((uint32_t)kd << (4 * (d < 0 ? 0 : d))), src);
+        const int32_t step = __shfl_sync(0xffffffffu, (b - bd) + lk, src);
+        if (mask == 0) {                                      // unreachable for a consistent plane
+            if (lane == 0)
+                for (int32_t x = i; x < N; ++x) {
+                    exit_g[x] = 0;
+                    if (exit_s) exit_s[x] = 0;
+                }
+            return false;
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int j = 0; j < D; ++j)
+                if (j < dm) {
+                    const uint8_t k = (uint8_t)((packed >> (4 * j)) & 15u);
+                    exit_g[i + j] = k;
+                    if (exit_s) exit_s[i + j] = k;
+                }
+        }
+        b -= step;
+        return i + D < N;
+    };
+    // rounds alternate between two cost register sets (no copies of in-flight loads)
+    int32_t pcA[D], lcA[K], pcB[D], lcB[K];
+    load_costs(0, pcA, lcA);
+    for (int32_t i = 0; i < N; i += 2 * D) {
+        if (!round(i, pcA, lcA, pcB, lcB)) break;
+        if (!round(i + D, pcB, lcB, pcA, lcA)) break;
+    }
+}
+
 // a5 inside the DP kernel: warp 0 walks the choice planes from (frame 0, b = C*) and resolves
 // D frames per dependent round trip. Costs do not depend on b, so while lane 0 reads frame i's
 // choice at b, lane 1 + a reads frame i+1's at b - c_{i,a} and (D = 3, when 1 + K + K^2 <= 32)
@@ -258,6 +382,9 @@ __device__ __forceinline__ void flush_window_stats(const DpParams &P, uint32_t *
     }
 }
 
+// OSM: the window's options staged in shared memory as packed (g << 4 | 15 - k, c) pairs and read
+// with broadcast LDS.64; otherwise lane q*K + k holds option k of a chunk of frames (prefetched a
+// chunk ahead) and the warp broadcasts it with shuffles (windows whose option table does not fit).
 // FUSE (turbo_schedule): a1 (budget from capacity) and a2 (options straight from class ids and
 // the profile, never materialised in HBM) in the prologue, a6 (statistics) in the epilogue.
 template <int K, int MODE, bool OSM, bool FUSE>
@@ -445,20 +572,44 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     // option k of the chunk's q-th frame); the next chunk is loaded while the current one is
     // consumed, so CH frames of work hide the global-load latency.
     constexpr int CH = 32 / K;
-    int32_t a_gp = 0, a_c = 0, b_gp = 0, b_c = 0;
+    // Pipeline (no load is consumed before a whole chunk of frames has been computed):
+    // a = current chunk (packed keys), b = next chunk (raw values, as loaded), n_cls = class ids of
+    // the chunk after next (fused: the profile row address of chunk m+1 needs chunk m+1's class).
+    int32_t a_gp = 0, a_c = 0, b_g = 0, b_c = 0, n_cls = 0;
+    bool b_ok = true;
     const int lq = lane / K, lk = lane - (lane / K) * K;
-    auto load_chunk = [&](int32_t hi, int32_t &gp_out, int32_t &c_out) {   // frames hi, hi-1, ...
+    auto load_cls = [&](int32_t hi) -> int32_t {               // frames hi, hi-1, ... of a chunk
         const int32_t i = hi - lq;
+        return (FUSE && lq < CH && i >= 0) ? (int32_t)P.class_id[ff + i] : 0;
+    };
+    auto load_raw = [&](int32_t hi, int32_t cls, int32_t &g, int32_t &c, bool &ok) {
+        const int32_t i = hi - lq;
+        g = 0;
+        c = 0;
+        ok = true;
         if (lq < CH && i >= 0) {
-            int32_t g, c;
-            load_opt(i, lk, g, c);
-            gp_out = (g << 4) | (15 - lk);
-            c_out = c;
+            if (FUSE) {                                        // a class >= C reads as a zero row
+                ok = cls < prof_C;
+                const int32_t row = ok ? cls : 0;
+                g = __ldg(prof_g + row * K + lk);
+                c = __ldg(prof_c + row * K + lk);
+            } else {
+                g = __ldg(og + (int64_t)i * K + lk);
+                c = __ldg(oc + (int64_t)i * K + lk);
+            }
         }
     };
+    auto pack = [&](int32_t g, int32_t c, bool ok) {
+        a_gp = ((ok ? g : 0) << 4) | (15 - lk);
+        a_c = ok ? c : 0;
+    };
     if (!OSM && N > 0) {
-        load_chunk(N - 1, a_gp, a_c);
-        load_chunk(N - 1 - CH, b_gp, b_c);
+        int32_t g, c;
+        bool ok;
+        load_raw(N - 1, load_cls(N - 1), g, c, ok);                 // chunk 0 (the one wait)
+        pack(g, c, ok);
+        load_raw(N - 1 - CH, load_cls(N - 1 - CH), b_g, b_c, b_ok);  // chunk 1
+        n_cls = load_cls(N - 1 - 2 * CH);                            // chunk 2's classes
     }
     int32_t *__restrict__ cur = rowA;
     int32_t *__restrict__ nxt = inplace ? rowA : rowB;
@@ -482,9 +633,9 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
             const int32_t f = N - 1 - i;
             const int q = f % CH;
             if (q == 0 && f > 0) {                        // next chunk becomes current; prefetch
-                a_gp = b_gp;
-                a_c = b_c;
-                load_chunk(i - CH, b_gp, b_c);
+                pack(b_g, b_c, b_ok);
+                load_raw(i - CH, n_cls, b_g, b_c, b_ok);
+                n_cls = load_cls(i - 2 * CH);
             }
 #pragma unroll
             for (int k = 0; k < K; ++k) {

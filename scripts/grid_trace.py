@@ -20,14 +20,14 @@ def main():
     ws = b.solve_ws.cpu().numpy()
     off = int(b.shape.grid_scratch_offset)
     tr = ws[off + 4 * (2 * 256 + 64): off + 4 * (2 * 256 + 64) + 8 * 8 * 256].view(np.int64).reshape(256, 8)[:148]
-    names = ["loop", "wait_halo", "wait_step", "comm_wait_top", "comm_publish", "comm_fetch", "retries", "steps"]
+    names = ["retries", "consume", "ship", "step", "mbar_wait", "to_consume", "-", "steps"]
     steps = np.maximum(tr[:, 7], 1)
-    for k, n in enumerate(names):
-        per = tr[:, k] / steps if k < 6 else tr[:, k]
-        print(f"{n:14s} mean {per.mean():10.1f} min {per.min():10.1f} max {per.max():10.1f}  (cycles/step)"
-              if k < 6 else f"{n:14s} mean {per.mean():10.1f} min {per.min()} max {per.max()}")
-    for j in (0, 1, 2, 73, 146, 147):
-        print(j, (tr[j, :6] / steps[j]).round(0).tolist(), tr[j, 6:].tolist())
+    for k in (0, 1, 2, 3, 4, 5):
+        per = tr[:, k] / steps
+        print(f"{names[k]:8s} per step: mean {per.mean():10.1f} min {per.min():10.1f} max {per.max():10.1f}"
+              + ("" if k == 0 else "  (cycles)"))
+    for j in (0, 1, 2, 73, 145, 146, 147):
+        print(j, (tr[j, :6] / steps[j]).round(1).tolist(), int(tr[j, 7]))
 
 
 if __name__ == "__main__":
