@@ -159,21 +159,27 @@ __device__ __forceinline__ void dp_tile(const DpParams &P, int32_t t, int32_t i,
         gch[((int64_t)i * gtiles + t) * 32 + lane] = word;
 }
 
-// a5 of the standalone and long-window backtracks (choice planes in HBM, costs from the option
-// table): one warp walks the planes from (frame 0, b = C*) and resolves D frames per dependent
-// round trip.
-// Speculation: lane q is a CANDIDATE prefix (p_0 .. p_{d-1}) of d < D choices (q = 0: the empty
-// prefix; then the K one-frame prefixes, the K^2 two-frame ones, ...). Costs do not depend on b,
+// a5 of the long-window kernel (ONE window walked by one warp while the rest of the GPU idles:
+// the round-trip latency is everything): one warp walks the HBM planes from (frame 0, b = C*) and
+// resolves D frames per dependent round trip.
+// Speculation: candidate q (lane q, or q - 32 in a lane's second slot) is a prefix
+// (p_0 .. p_{d-1}) of d < D choices (q = 0: the empty prefix; then the K one-frame prefixes,
+// the K^2 two-frame ones, ...). Costs do not depend on b,
 // so each lane knows its cells b_j = b - sum_{l<j} c_{i+l, p_l} before the round, reads the
 // choices at all of them at once, and decides ON ITS OWN whether its prefix is the realised one
 // (every p_j equals the choice read at b_j). The realised deepest candidate holds the round:
-// one ballot and two shuffles hand its exits and its cost to the warp. Costs are loaded one
+// one ballot per slot and two shuffles hand its exits and its cost to the warp. Costs are loaded one
 // round ahead, so the only dependent latency per round is one choice read + ballot + shuffle.
-// (Inside the DP kernels the walk shares the SM's load/store pipe with other CTAs' DP and its
-// extra loads cost more than the shorter chain saves: there backtrack_warp below is used.)
+// (With many windows in flight -- the DP kernels and the standalone backtrack -- the walks share
+// the load/store pipes and the extra loads cost more than the shorter chain saves: there
+// backtrack_warp below is used.)
 template <int K>
 struct BtGeom {
-    static constexpr int D = (K == 2) ? 5 : (K <= 5 ? 3 : 2);   // sum_{j<D} K^j <= 32
+    // candidates per lane (C) and frames per round (D): the largest D with sum_{j<D} K^j <= 32 C.
+    // (C = 2, e.g. D = 3 for K = 6, measured slower on c4: the wider rounds cost more than the
+    // saved round trips.)
+    static constexpr int C = 1;
+    static constexpr int D = (K == 2) ? 5 : (K <= 5 ? 3 : 2);
 };
 
 template <int K, int MODE, class CostF>
@@ -186,19 +192,23 @@ __device__ __forceinline__ void backtrack_warp_spec(int32_t N, int32_t b, const 
     constexpr int RPT = 32 / CB;
     constexpr uint32_t CMASK = (1u << CB) - 1u;
     constexpr int D = BtGeom<K>::D;
-    // decode the lane's candidate: depth d (-1: idle lane) and digits (4 bits each, frame i first)
-    int d = -1;
-    uint32_t dig = 0;
-    {
-        int q = lane, pw = 1;
+    constexpr int C = BtGeom<K>::C;
+    // decode each slot's candidate q = lane + 32 s: depth d (-1: idle) and digits (frame i first)
+    int d[C];
+    uint32_t dig[C];
+#pragma unroll
+    for (int sl = 0; sl < C; ++sl) {
+        d[sl] = -1;
+        dig[sl] = 0;
+        int q = lane + 32 * sl, pw = 1;
 #pragma unroll
         for (int dd = 0; dd < D; ++dd) {
-            if (d < 0) {
+            if (d[sl] < 0) {
                 if (q < pw) {
-                    d = dd;
+                    d[sl] = dd;
                     int r = q;
                     for (int j = dd - 1; j >= 0; --j) {
-                        dig |= (uint32_t)(r % K) << (4 * j);
+                        dig[sl] |= (uint32_t)(r % K) << (4 * j);
                         r /= K;
                     }
                 } else {
@@ -215,49 +225,83 @@ __device__ __forceinline__ void backtrack_warp_spec(int32_t N, int32_t b, const 
                                                       : gch[((int64_t)i * gtiles + t) * 32 + (cell & 31)];
         return (int32_t)((word >> choice_shift(j, CB)) & CMASK);
     };
-    // costs of round starting at frame i0: the prefix costs and every cost of frame i0 + d
-    auto load_costs = [&](int32_t i0, int32_t (&pcv)[D], int32_t (&lcv)[K]) {
+    // costs of the round starting at frame i0, per slot: the prefix costs and every cost of frame
+    // i0 + d
+    auto load_costs = [&](int32_t i0, int32_t (&pcv)[C][D], int32_t (&lcv)[C][K]) {
 #pragma unroll
-        for (int j = 0; j < D - 1; ++j)
-            pcv[j] = (j < d && i0 + j < N) ? cost(i0 + j, (int)((dig >> (4 * j)) & 15u)) : 0;
-        pcv[D - 1] = 0;
-        const bool last = d >= 0 && i0 + d < N;
+        for (int sl = 0; sl < C; ++sl) {
 #pragma unroll
-        for (int k = 0; k < K; ++k) lcv[k] = last ? cost(i0 + d, k) : 0;
+            for (int j = 0; j < D - 1; ++j)
+                pcv[sl][j] = (j < d[sl] && i0 + j < N) ? cost(i0 + j, (int)((dig[sl] >> (4 * j)) & 15u)) : 0;
+            pcv[sl][D - 1] = 0;
+            const bool last = d[sl] >= 0 && i0 + d[sl] < N;
+#pragma unroll
+            for (int k = 0; k < K; ++k) lcv[sl][k] = last ? cost(i0 + d[sl], k) : 0;
+        }
     };
-    // one round at frame i with this round's costs (pcv, lcv); prefetches the next round's into
-    // (pcn, lcn). Returns false when the walk is over.
-    auto round = [&](int32_t i, const int32_t (&pcv)[D], const int32_t (&lcv)[K], int32_t (&pcn)[D],
-                     int32_t (&lcn)[K]) -> bool {
+    // one round at frame i with this round's costs; prefetches the next round's into (pcn, lcn).
+    // Returns false when the walk is over.
+    auto round = [&](int32_t i, const int32_t (&pcv)[C][D], const int32_t (&lcv)[C][K], int32_t (&pcn)[C][D],
+                     int32_t (&lcn)[C][K]) -> bool {
         const int32_t dm = min(D, N - i);
         if (i + D < N) load_costs(i + D, pcn, lcn);           // next round's costs, off the chain
-        // the choices at every cell of the lane's prefix: D unconditional loads (clamped to a
-        // valid cell and frame) so they are all in flight at once
-        int32_t kv[D];
-        int32_t bj = b, bd = b;
-        bool neg = false;
+        // the choices at every cell of each slot's prefix: D unconditional loads per slot
+        // (clamped to a valid cell and frame) so they are all in flight at once
+        int32_t kv[C][D], bd[C];
+        bool neg[C];
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-            kv[j] = choice(min(i + j, N - 1), max(bj, 0));
-            if (j <= d) neg |= bj < 0;
-            if (j == d) bd = bj;
-            if (j < D - 1 && j < d) bj -= pcv[j];
+        for (int sl = 0; sl < C; ++sl) {
+            int32_t bj = b;
+            bd[sl] = b;
+            neg[sl] = false;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                kv[sl][j] = choice(min(i + j, N - 1), max(bj, 0));
+                if (j <= d[sl]) neg[sl] |= bj < 0;
+                if (j == d[sl]) bd[sl] = bj;
+                if (j < D - 1 && j < d[sl]) bj -= pcv[sl][j];
+            }
         }
-        bool on = d >= 0 && d == dm - 1 && !neg;
-        int32_t kd = 0;
+        uint32_t packed_v[C];
+        int32_t step_v[C];
+        unsigned mask[C];
 #pragma unroll
-        for (int j = 0; j < D; ++j) {
-            if (j < d) on = on && kv[j] == (int32_t)((dig >> (4 * j)) & 15u);
-            if (j == d) kd = kv[j];
+        for (int sl = 0; sl < C; ++sl) {
+            bool on = d[sl] >= 0 && d[sl] == dm - 1 && !neg[sl];
+            int32_t kd = 0;
+#pragma unroll
+            for (int j = 0; j < D; ++j) {
+                if (j < d[sl]) on = on && kv[sl][j] == (int32_t)((dig[sl] >> (4 * j)) & 15u);
+                if (j == d[sl]) kd = kv[sl][j];
+            }
+            int32_t lk = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) lk = (k == kd) ? lcv[sl][k] : lk;
+            mask[sl] = __ballot_sync(0xffffffffu, on);
+            packed_v[sl] = dig[sl] | ((uint32_t)kd << (4 * (d[sl] < 0 ? 0 : d[sl])));
+            step_v[sl] = (b - bd[sl]) + lk;
         }
-        int32_t lk = 0;
+        // the realised candidate: its slot (warp-uniform) and lane
+        int ws = 0;
+        unsigned m = mask[0];
 #pragma unroll
-        for (int k = 0; k < K; ++k) lk = (k == kd) ? lcv[k] : lk;
-        const unsigned mask = __ballot_sync(0xffffffffu, on);
-        const int src = (__ffs(mask) - 1) & 31;
-        const uint32_t packed = __shfl_sync(0xffffffffu, dig | ((uint32_t)kd << (4 * (d < 0 ? 0 : d))), src);
-        const int32_t step = __shfl_sync(0xffffffffu, (b - bd) + lk, src);
-        if (mask == 0) {                                      // unreachable for a consistent plane
+        for (int sl = 1; sl < C; ++sl)
+            if (m == 0) {
+                ws = sl;
+                m = mask[sl];
+            }
+        uint32_t pk = packed_v[0];
+        int32_t st = step_v[0];
+#pragma unroll
+        for (int sl = 1; sl < C; ++sl)
+            if (ws == sl) {
+                pk = packed_v[sl];
+                st = step_v[sl];
+            }
+        const int src = (__ffs(m) - 1) & 31;
+        const uint32_t packed = __shfl_sync(0xffffffffu, pk, src);
+        const int32_t step = __shfl_sync(0xffffffffu, st, src);
+        if (m == 0) {                                         // unreachable for a consistent plane
             if (lane == 0)
                 for (int32_t x = i; x < N; ++x) {
                     exit_g[x] = 0;
@@ -278,7 +322,7 @@ __device__ __forceinline__ void backtrack_warp_spec(int32_t N, int32_t b, const 
         return i + D < N;
     };
     // rounds alternate between two cost register sets (no copies of in-flight loads)
-    int32_t pcA[D], lcA[K], pcB[D], lcB[K];
+    int32_t pcA[C][D], lcA[C][K], pcB[C][D], lcB[C][K];
     load_costs(0, pcA, lcA);
     for (int32_t i = 0; i < N; i += 2 * D) {
         if (!round(i, pcA, lcA, pcB, lcB)) break;
