@@ -122,6 +122,17 @@ const char *turbo_status_string(turbo_status_t s)
     return "unknown";
 }
 
+static int64_t *g_trace = nullptr;
+static int64_t g_trace_words = 0;
+
+turbo_status_t turbo_debug_trace(int64_t *trace, int64_t words)
+{
+    if (trace != nullptr && words < 8) return TURBO_ERR_INVALID_ARG;
+    g_trace = trace;
+    g_trace_words = trace ? words : 0;
+    return TURBO_OK;
+}
+
 turbo_status_t turbo_debug_set_variant(int32_t variant)
 {
     if (variant < 0 || variant > 6 || (variant & 3) == 3) return TURBO_ERR_INVALID_ARG;
@@ -275,10 +286,18 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int kind, const DpParam
     DpParams Ps[TURBO_NUM_CLASSES];
     turbo_shape_t shapes[TURBO_NUM_CLASSES];
     int modes[TURBO_NUM_CLASSES];
+    bool walk[TURBO_NUM_CLASSES];
     for (int c = 0; c < TURBO_NUM_CLASSES; ++c) {          // validate every class before launching
+        walk[c] = false;
         if (!shape->cls_count[c]) continue;
         shapes[c] = class_shape(shape, c);
         modes[c] = kind == RUN_PLAN ? DP_PLAN : solve_mode(&shapes[c]);
+        // choice planes in HBM: the DP runs in plan mode and a separate kernel walks the planes
+        // (thousands of latency-bound walks in flight instead of one per DP CTA slot)
+        if (modes[c] == DP_SOLVE_GLOBAL) {
+            modes[c] = DP_PLAN;
+            walk[c] = true;
+        }
         DpParams &P = Ps[c];
         P = base;
         dp_smem_words(&shapes[c], modes[c], &P);
@@ -296,13 +315,24 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int kind, const DpParam
     }
     DpLaunch info;
     cudaError_t e = cudaSuccess;
+    auto launch_walk = [&](int c, cudaStream_t st) -> cudaError_t {
+        if (!walk[c]) return cudaSuccess;
+        const DpParams &P = Ps[c];
+        if (kind == RUN_SCHEDULE)
+            return launch_walk_sched(P.windows, shape->num_windows, P.profiles, P.class_id, P.workspace, P.best_gain,
+                                     P.best_cost, P.feasible, P.exit_out, P.stats, d.num_sms, st, c);
+        return launch_backtrack(P.windows, shape->num_windows, P.opt_cost, P.workspace, P.best_cost, P.feasible,
+                                P.exit_out, d.num_sms, st, c);
+    };
     int n_cls = 0;
     for (int c = 0; c < TURBO_NUM_CLASSES; ++c) n_cls += shape->cls_count[c] ? 1 : 0;
     if (n_cls <= 1) {
         for (int c = 0; c < TURBO_NUM_CLASSES && e == cudaSuccess; ++c)
-            if (shape->cls_count[c])
+            if (shape->cls_count[c]) {
                 e = launch_dp(&shapes[c], modes[c], Ps[c], d.num_sms, d.smem_per_sm, d.smem_per_cta_optin,
                               (cudaStream_t)stream, &info);
+                if (e == cudaSuccess) e = launch_walk(c, (cudaStream_t)stream);
+            }
     } else {
         // Several classes: each class launch is bounded by its longest window's frame chain, so the
         // launches run CONCURRENTLY on library-owned streams forked from (and joined back into) the
@@ -317,6 +347,7 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int kind, const DpParam
             if ((e = launch_dp(&shapes[c], modes[c], Ps[c], d.num_sms, d.smem_per_sm, d.smem_per_cta_optin,
                                fj->streams[c], &info)) != cudaSuccess)
                 break;
+            if ((e = launch_walk(c, fj->streams[c])) != cudaSuccess) break;
             if ((e = cudaEventRecord(fj->join[c], fj->streams[c])) != cudaSuccess) break;
             e = cudaStreamWaitEvent((cudaStream_t)stream, fj->join[c], 0);
         }
@@ -358,6 +389,8 @@ static DpParams base_params(const turbo_shape_t *shape, const turbo_window_t *wi
         dbg = e ? atoi(e) : 0;
     }
     P.debug = dbg;
+    P.trace = g_trace;
+    P.trace_words = g_trace_words;
     return P;
 }
 

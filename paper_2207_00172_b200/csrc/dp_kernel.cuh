@@ -594,7 +594,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
         }
         if (MODE != DP_PLAN)
             for (int32_t i = tid; i < N; i += nthr) P.exit_out[ff + i] = 0;
-        if (FUSE) {
+        if (FUSE && MODE != DP_PLAN) {                    // (plan mode: the walk kernel counts it)
             if (tid == 0)
                 for (int32_t i = 0; i < N; ++i) {
                     const uint32_t cls = class_of(i);
@@ -607,6 +607,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
         return;
     }
 
+    trace_mark(P, 1);
     if (P.debug & 64) return;                         // timing: prologue only
     // choice-plane stride (tiles per frame): the layout bound for HBM planes, exact for smem
     const int32_t gtiles = (int32_t)(((Bb + 32) >> 5) + RPT - 1) / RPT;
@@ -702,6 +703,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
         nxt = tmp;
     }
     // after the swap `cur` holds S_0 (in place: cur == nxt == rowA)
+    trace_mark(P, 2);
 
     // ---- a4: optimum extraction
     const int32_t RB = cur[B];
@@ -721,6 +723,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
         P.best_cost[w] = Cst;
         P.feasible[w] = feas ? 1 : 0;
     }
+    trace_mark(P, 3);
     if (MODE == DP_PLAN) return;
 
     // ---- a5 fused: forward backtrack from (frame 0, b = C*)
@@ -740,10 +743,14 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
             load_opt(i, k, g, c);
             return c;
         };
-        backtrack_warp<K, MODE>(N, Cst, sch, gch, ntiles, gtiles, cost, P.exit_out + ff, exit_s, lane);
+        if (MODE == DP_SOLVE_SMEM && OSM && (P.debug & 256))
+            backtrack_warp_spec<K, MODE>(N, Cst, sch, gch, ntiles, gtiles, cost, P.exit_out + ff, exit_s, lane);
+        else
+            backtrack_warp<K, MODE>(N, Cst, sch, gch, ntiles, gtiles, cost, P.exit_out + ff, exit_s, lane);
     }
     if (FUSE) {                                           // a6: CTA-private histograms
         if (nwarps > 1) __syncthreads(); else __syncwarp();
+        trace_mark(P, 4);
         for (int32_t i = tid; i < N; i += nthr) {
             const uint32_t k = exit_s ? exit_s[i] : P.exit_out[ff + i];   // global: visible after the barrier
             const uint32_t cls = class_of(i);
@@ -787,6 +794,7 @@ __global__ void __launch_bounds__(512, (KSEL == 0) ? 1 : 2) dp_cta_kernel(DpPara
     int32_t *cst = after;                                      // !OSM: costs for the backtrack
     uint32_t *sch = reinterpret_cast<uint32_t *>(after + P.cst_words);
     __shared__ uint32_t hist[FUSE ? 176 : 1];
+    trace_mark(P, 0);
     for (int32_t x = threadIdx.x; x < P.pad_words; x += blockDim.x) {
         rowA[x - P.pad_words] = NEG_R;
         if (nwarps > 1) rowB[x - P.pad_words] = NEG_R;
@@ -812,6 +820,7 @@ __global__ void __launch_bounds__(512, (KSEL == 0) ? 1 : 2) dp_cta_kernel(DpPara
             }
         }
         __syncthreads();                              // smem reused by the next window
+        trace_mark(P, 5);
     }
 }
 
@@ -835,7 +844,6 @@ dp_kernel_t pick_dp_kernel(int kmin, int kmax)
 
 dp_kernel_t dp_kernel_plan(int kmin, int kmax, bool osm);
 dp_kernel_t dp_kernel_solve_smem(int kmin, int kmax, bool osm);
-dp_kernel_t dp_kernel_solve_global(int kmin, int kmax, bool osm);
 dp_kernel_t dp_kernel_schedule(int kmin, int kmax, int mode, bool osm);
 
 }  // namespace turbo

@@ -86,10 +86,11 @@ cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P0, 
     const size_t need = dp_smem_bytes(P, G);
 
     const bool osm = P.osm != 0;
+    // (HBM choice planes are always walked by a separate kernel: DP_SOLVE_GLOBAL never gets here)
+    if (mode == DP_SOLVE_GLOBAL) return cudaErrorInvalidValue;
     dp_kernel_t kern = P.fuse                  ? dp_kernel_schedule(shape->min_exits, shape->max_exits, mode, osm)
                        : mode == DP_PLAN         ? dp_kernel_plan(shape->min_exits, shape->max_exits, osm)
-                       : mode == DP_SOLVE_SMEM ? dp_kernel_solve_smem(shape->min_exits, shape->max_exits, osm)
-                                               : dp_kernel_solve_global(shape->min_exits, shape->max_exits, osm);
+                                                 : dp_kernel_solve_smem(shape->min_exits, shape->max_exits, osm);
     // the dynamic-smem ceiling is the per-CTA opt-in maximum minus the kernel's static smem
     static std::mutex amu;
     static std::map<const void *, size_t> static_smem;
@@ -172,6 +173,7 @@ dp_kernel_t dp_kernel_sched_global_reg(int kmin, int kmax);
 dp_kernel_t dp_kernel_schedule(int kmin, int kmax, int mode, bool osm)
 {
     if (mode == DP_SOLVE_SMEM) return osm ? dp_kernel_sched_smem_osm(kmin, kmax) : dp_kernel_sched_smem_reg(kmin, kmax);
+    // DP_PLAN: fused a1..a4, the walk and statistics follow in walk_sched_kernel
     return osm ? dp_kernel_sched_global_osm(kmin, kmax) : dp_kernel_sched_global_reg(kmin, kmax);
 }
 }  // namespace turbo

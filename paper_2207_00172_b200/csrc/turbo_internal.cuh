@@ -93,7 +93,20 @@ struct DpParams {
     int32_t cls;                   // row-size class served by this launch (-1: every window)
     int32_t cls_count;             // windows in that class (residency / wave planning)
     int64_t *stats;
+    int64_t *trace;                // debug: per-CTA phase timestamps (turbo_debug_trace)
+    int64_t trace_words;
 };
+
+// turbo_debug_trace: %globaltimer at phase p of this CTA (thread 0, first window only)
+__device__ __forceinline__ void trace_mark(const DpParams &P, int p)
+{
+    if (P.trace != nullptr && threadIdx.x == 0 && (int64_t)blockIdx.x * 8 + 8 <= P.trace_words &&
+        P.trace[(int64_t)blockIdx.x * 8 + p] == 0) {
+        uint64_t t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        P.trace[(int64_t)blockIdx.x * 8 + p] = (int64_t)t;
+    }
+}
 
 struct DpLaunch {
     int mode;
@@ -128,9 +141,16 @@ cudaError_t launch_batches(const turbo_window_t *windows, int32_t num_windows, c
 cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams &P, int num_sms,
                            int smem_per_cta_max, cudaStream_t stream);
 size_t dp_smem_bytes(const DpParams &P, int nwarps);
+// cls >= 0: only the windows of that row-size class (the others were walked elsewhere)
 cudaError_t launch_backtrack(const turbo_window_t *windows, int32_t num_windows, const int32_t *opt_cost,
                              const uint8_t *workspace, const int32_t *best_cost, const uint8_t *feasible,
-                             uint8_t *exit_out, int num_sms, cudaStream_t stream);
+                             uint8_t *exit_out, int num_sms, cudaStream_t stream, int cls = -1);
+// turbo_schedule, windows of row-size class cls whose DP ran in plan mode: a5 walk with costs from
+// class ids + profile, then a6 statistics of those windows
+cudaError_t launch_walk_sched(const turbo_window_t *windows, int32_t num_windows, const turbo_profile_t *profiles,
+                              const uint8_t *class_id, const uint8_t *workspace, const int32_t *best_gain,
+                              const int32_t *best_cost, const uint8_t *feasible, uint8_t *exit_out, int64_t *stats,
+                              int num_sms, cudaStream_t stream, int cls);
 cudaError_t launch_stats(const turbo_window_t *windows, int32_t num_windows, const uint8_t *class_id,
                          const uint8_t *exit_out, const int32_t *best_gain, const int32_t *best_cost,
                          const uint8_t *feasible, int64_t *stats, int num_sms, cudaStream_t stream);

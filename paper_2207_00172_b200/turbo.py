@@ -64,7 +64,7 @@ assert WINDOW_DTYPE.itemsize == 48
 EXPORTS = ["turbo_mckp_workspace", "turbo_profile_lookup", "turbo_mckp_plan", "turbo_backtrack",
            "turbo_mckp_solve", "turbo_mckp_solve_workspace", "turbo_schedule", "turbo_heuristic_plan", "turbo_stats",
            "turbo_bucketize", "turbo_batches",
-           "turbo_debug_set_variant",
+           "turbo_debug_set_variant", "turbo_debug_trace",
            "turbo_status_string", "turbo_abi_version"]
 
 _lib = None
@@ -92,6 +92,7 @@ def load(path: Optional[str] = None):
     lib.turbo_bucketize.argtypes = [vp, i64, i32, ctypes.c_float, vp, vp]
     lib.turbo_batches.argtypes = [vp, vp, vp, vp, vp, vp]
     lib.turbo_debug_set_variant.argtypes = [i32]
+    lib.turbo_debug_trace.argtypes = [vp, i64]
     lib.turbo_status_string.restype = ctypes.c_char_p
     lib.turbo_abi_version.restype = i32
     for name in EXPORTS:
@@ -211,6 +212,15 @@ def stats(shape, windows_dev, class_id, exit_out, best_gain, best_cost, feasible
 
 def debug_set_variant(v: int):
     _check("turbo_debug_set_variant", load().turbo_debug_set_variant(int(v)))
+
+
+def debug_trace(buf=None):
+    """Per-CTA phase timestamps of the DP kernels into `buf` (int64 device tensor, zeroed by the
+    caller; see turbo.h turbo_debug_trace); None disables."""
+    if buf is None:
+        _check("turbo_debug_trace", load().turbo_debug_trace(None, 0))
+    else:
+        _check("turbo_debug_trace", load().turbo_debug_trace(ctypes.c_void_p(buf.data_ptr()), int(buf.numel())))
 
 
 # ----------------------------------------------------------------------------- planner object
