@@ -67,7 +67,10 @@ typedef struct {
     int32_t num_exits;           /* K of the profile (turbo_mckp_workspace)                      */
     int32_t budget_bound;        /* layout bound: budget at sizing time (turbo_mckp_workspace);
                                     a device-side budget above it rejects the window            */
-    int32_t reserved;            /* 0 */
+    int32_t order;               /* (turbo_mckp_workspace) a permutation stored across the
+                                    array: order of entry r = the window served r-th -- windows
+                                    grouped by row-size class, largest work N (B+1) (K+1) first
+                                    inside a class (longest-processing-time first)             */
 } turbo_window_t;                /* 48 bytes; array lives on the host (sizing) and the device */
 
 /* Launch shape of a window batch, computed on the host by turbo_mckp_workspace
@@ -89,7 +92,10 @@ typedef struct {
     int32_t num_big;             /* windows whose row (budget_bound + 1 > TURBO_BIG_CELLS cells)
                                     is split over the whole grid (long-window kernel)           */
     int64_t grid_scratch_offset; /* workspace offset of the long-window kernel's halo ring/flags */
-    int64_t reserved1[2];
+    int32_t ordered;             /* 1: the kernels serve windows through turbo_window_t.order
+                                    (several classes, or uneven work); 0: in index order        */
+    int32_t reserved2;
+    int64_t reserved3;
     /* per row-size class (TURBO_NUM_CLASSES, see below): windows of one class are planned by one
      * launch shaped for them (warps per window, shared memory, residency) */
     int32_t cls_count[4];

@@ -3,6 +3,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
+#include <algorithm>
+#include <climits>
 
 #include "turbo_internal.cuh"
 
@@ -172,7 +175,7 @@ turbo_status_t turbo_mckp_workspace(const turbo_profile_t *profiles_host, int32_
         win.budget_bound = win.budget;
         win.first_option = opt;
         win.choice_offset = ws;
-        win.reserved = 0;
+        win.order = w;
         opt += ((int64_t)win.num_frames * K + 3) & ~(int64_t)3;    // 16-B aligned option blocks
         ws += choice_plane_bytes(win.num_frames, win.budget, K);
         frames = frames > win.first_frame + win.num_frames ? frames : win.first_frame + win.num_frames;
@@ -198,6 +201,37 @@ turbo_status_t turbo_mckp_workspace(const turbo_profile_t *profiles_host, int32_
             s.num_classes_max = profiles_host[win.profile].num_classes;
     }
     if (num_windows == 0) s.min_exits = s.max_exits = 2;
+    // Serving order (turbo_window_t.order): windows grouped by row-size class (the long ones
+    // last), largest work first inside a class -- the CTA scheduler hands out blocks in index
+    // order, so the longest windows start first and the short ones fill the gaps (LPT). Used
+    // when there are several classes or the work inside a class is uneven.
+    {
+        std::vector<std::pair<int64_t, int32_t>> key((size_t)num_windows);
+        int n_cls = s.num_big > 0 ? 1 : 0;
+        for (int c = 0; c < TURBO_NUM_CLASSES; ++c) n_cls += s.cls_count[c] ? 1 : 0;
+        bool uneven = false;
+        int64_t wmin[TURBO_NUM_CLASSES + 1], wmax[TURBO_NUM_CLASSES + 1];
+        for (int c = 0; c <= TURBO_NUM_CLASSES; ++c) {
+            wmin[c] = INT64_MAX;
+            wmax[c] = 0;
+        }
+        for (int32_t w = 0; w < num_windows; ++w) {
+            const turbo_window_t &win = windows_host[w];
+            const int rc = std::min(row_class((int64_t)win.budget_bound + 1), TURBO_NUM_CLASSES);
+            const int64_t work = (int64_t)win.num_frames * ((int64_t)win.budget_bound + 1) * (win.num_exits + 1);
+            wmin[rc] = std::min(wmin[rc], work);
+            wmax[rc] = std::max(wmax[rc], work);
+            // class ascending, work descending, index ascending (deterministic)
+            key[(size_t)w] = std::make_pair(((int64_t)rc << 58) | ((((int64_t)1 << 58) - 1) - std::min(work, ((int64_t)1 << 58) - 1)), w);
+        }
+        for (int c = 0; c <= TURBO_NUM_CLASSES; ++c)
+            if (wmax[c] > 0 && wmax[c] * 2 > wmin[c] * 3) uneven = true;
+        s.ordered = (n_cls > 1 || uneven) ? 1 : 0;
+        if (s.ordered) {
+            std::sort(key.begin(), key.end());
+            for (int32_t r = 0; r < num_windows; ++r) windows_host[r].order = key[(size_t)r].second;
+        }
+    }
     s.total_frames = frames;
     s.total_options = opt;
     s.total_cells = cells;
@@ -310,6 +344,10 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int kind, const DpParam
         }
         P.cls = c;
         P.cls_count = shape->cls_count[c];
+        // the serving order is followed by the mixed-K kernels; fixed-K kernels go in index order
+        P.ordered = (shape->ordered && !dp_kernel_fixed_k(shapes[c].min_exits, shapes[c].max_exits)) ? 1 : 0;
+        P.cls_first = 0;
+        for (int c2 = 0; c2 < c; ++c2) P.cls_first += shape->cls_count[c2];
         if (dp_smem_bytes(P, dp_warps_per_window(&shapes[c])) > (size_t)d.smem_per_cta_optin)
             return TURBO_ERR_UNSUPPORTED;
     }
@@ -318,11 +356,16 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int kind, const DpParam
     auto launch_walk = [&](int c, cudaStream_t st) -> cudaError_t {
         if (!walk[c]) return cudaSuccess;
         const DpParams &P = Ps[c];
+        WinSel sel;
+        sel.cls = c;
+        sel.ordered = P.ordered;
+        sel.first = P.cls_first;
+        sel.count = P.cls_count;
         if (kind == RUN_SCHEDULE)
             return launch_walk_sched(P.windows, shape->num_windows, P.profiles, P.class_id, P.workspace, P.best_gain,
-                                     P.best_cost, P.feasible, P.exit_out, P.stats, d.num_sms, st, c);
+                                     P.best_cost, P.feasible, P.exit_out, P.stats, d.num_sms, st, sel);
         return launch_backtrack(P.windows, shape->num_windows, P.opt_cost, P.workspace, P.best_cost, P.feasible,
-                                P.exit_out, d.num_sms, st, c);
+                                P.exit_out, d.num_sms, st, sel);
     };
     int n_cls = 0;
     for (int c = 0; c < TURBO_NUM_CLASSES; ++c) n_cls += shape->cls_count[c] ? 1 : 0;

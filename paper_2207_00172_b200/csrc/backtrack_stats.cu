@@ -16,13 +16,14 @@ __global__ void __launch_bounds__(256) backtrack_kernel(const turbo_window_t *__
                                                         const uint8_t *__restrict__ workspace,
                                                         const int32_t *__restrict__ best_cost,
                                                         const uint8_t *__restrict__ feasible,
-                                                        uint8_t *__restrict__ exit_out, int32_t cls)
+                                                        uint8_t *__restrict__ exit_out, WinSel sel)
 {
     const int lane = threadIdx.x & 31;
     const int wpc = blockDim.x >> 5;
-    for (int64_t w = (int64_t)blockIdx.x * wpc + (threadIdx.x >> 5); w < num_windows;
-         w += (int64_t)gridDim.x * wpc) {
-        if (cls >= 0 && row_class((int64_t)windows[w].budget_bound + 1) != cls) continue;
+    for (int64_t r = (int64_t)blockIdx.x * wpc + (threadIdx.x >> 5); r < sel.n_iter(num_windows);
+         r += (int64_t)gridDim.x * wpc) {
+        const int64_t w = sel.window(windows, r);
+        if (w < 0) continue;
         const int64_t ff = windows[w].first_frame;
         const int64_t fo = windows[w].first_option;
         const int32_t N = windows[w].num_frames;
@@ -76,16 +77,16 @@ __global__ void __launch_bounds__(256) backtrack_kernel(const turbo_window_t *__
 
 cudaError_t launch_backtrack(const turbo_window_t *windows, int32_t num_windows, const int32_t *opt_cost,
                              const uint8_t *workspace, const int32_t *best_cost, const uint8_t *feasible,
-                             uint8_t *exit_out, int num_sms, cudaStream_t stream, int cls)
+                             uint8_t *exit_out, int num_sms, cudaStream_t stream, WinSel sel)
 {
-    if (num_windows <= 0) return cudaSuccess;
+    if (sel.n_iter(num_windows) <= 0) return cudaSuccess;
     const int threads = 128;
     const int wpc = threads / 32;
-    int64_t blocks = ((int64_t)num_windows + wpc - 1) / wpc;
+    int64_t blocks = (sel.n_iter(num_windows) + wpc - 1) / wpc;
     const int64_t cap = (int64_t)num_sms * 16;
     if (blocks > cap) blocks = cap;
     backtrack_kernel<<<(unsigned)blocks, threads, 0, stream>>>(windows, num_windows, opt_cost, workspace,
-                                                               best_cost, feasible, exit_out, cls);
+                                                               best_cost, feasible, exit_out, sel);
     return cudaGetLastError();
 }
 
@@ -117,7 +118,7 @@ __global__ void __launch_bounds__(128) walk_sched_kernel(const turbo_window_t *_
                                                          const int32_t *__restrict__ best_cost,
                                                          const uint8_t *__restrict__ feasible,
                                                          uint8_t *__restrict__ exit_out,
-                                                         unsigned long long *__restrict__ stats, int32_t cls)
+                                                         unsigned long long *__restrict__ stats, WinSel sel)
 {
     __shared__ unsigned int hist[176];
     __shared__ unsigned long long tot[5];
@@ -127,10 +128,11 @@ __global__ void __launch_bounds__(128) walk_sched_kernel(const turbo_window_t *_
     const int lane = threadIdx.x & 31;
     const int wpc = blockDim.x >> 5;
     long long sg = 0, sc = 0, nw = 0, nf = 0, ni = 0;
-    for (int64_t w = (int64_t)blockIdx.x * wpc + (threadIdx.x >> 5); w < num_windows;
-         w += (int64_t)gridDim.x * wpc) {
+    for (int64_t r = (int64_t)blockIdx.x * wpc + (threadIdx.x >> 5); r < sel.n_iter(num_windows);
+         r += (int64_t)gridDim.x * wpc) {
+        const int64_t w = sel.window(windows, r);
+        if (w < 0) continue;
         const turbo_window_t win = windows[w];
-        if (row_class((int64_t)win.budget_bound + 1) != cls) continue;
         const int64_t ff = win.first_frame;
         const int32_t N = win.num_frames;
         const bool feas = feasible[w] != 0;
@@ -184,17 +186,17 @@ __global__ void __launch_bounds__(128) walk_sched_kernel(const turbo_window_t *_
 cudaError_t launch_walk_sched(const turbo_window_t *windows, int32_t num_windows, const turbo_profile_t *profiles,
                               const uint8_t *class_id, const uint8_t *workspace, const int32_t *best_gain,
                               const int32_t *best_cost, const uint8_t *feasible, uint8_t *exit_out, int64_t *stats,
-                              int num_sms, cudaStream_t stream, int cls)
+                              int num_sms, cudaStream_t stream, WinSel sel)
 {
-    if (num_windows <= 0) return cudaSuccess;
+    if (sel.n_iter(num_windows) <= 0) return cudaSuccess;
     const int threads = 128;
     const int wpc = threads / 32;
-    int64_t blocks = ((int64_t)num_windows + wpc - 1) / wpc;
+    int64_t blocks = (sel.n_iter(num_windows) + wpc - 1) / wpc;
     const int64_t cap = (int64_t)num_sms * 16;
     if (blocks > cap) blocks = cap;
     walk_sched_kernel<<<(unsigned)blocks, threads, 0, stream>>>(windows, num_windows, profiles, class_id, workspace,
                                                                 best_gain, best_cost, feasible, exit_out,
-                                                                reinterpret_cast<unsigned long long *>(stats), cls);
+                                                                reinterpret_cast<unsigned long long *>(stats), sel);
     return cudaGetLastError();
 }
 

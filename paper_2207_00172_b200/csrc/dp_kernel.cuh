@@ -801,6 +801,28 @@ __global__ void __launch_bounds__(512, (KSEL == 0) ? 1 : 2) dp_cta_kernel(DpPara
     }
     __syncthreads();
     if (P.debug & 32) return;                         // timing: launch only
+    if (KSEL == 0 && P.ordered) {
+        // mixed-K kernel, serving order (the class's range of it): the window index comes from
+        // memory, which is fine here -- the out-of-line bodies take it as a parameter anyway
+        for (int64_t r = blockIdx.x; r < P.cls_count; r += gridDim.x) {
+            const int64_t w = P.windows[P.cls_first + r].order;
+            switch (P.windows[w].num_exits) {
+#define TURBO_K_CASE(KK) \
+    case KK: dp_window_call<KK, MODE, OSM, FUSE>(P, w, rowA, rowB, sch, cst, opt_s, red, hist, warp, nwarps, lane); \
+        break;
+                TURBO_K_CASE(2) TURBO_K_CASE(3) TURBO_K_CASE(4) TURBO_K_CASE(5) TURBO_K_CASE(6)
+                TURBO_K_CASE(7) TURBO_K_CASE(8) TURBO_K_CASE(9) TURBO_K_CASE(10) TURBO_K_CASE(11)
+                TURBO_K_CASE(12) TURBO_K_CASE(13) TURBO_K_CASE(14) TURBO_K_CASE(15) TURBO_K_CASE(16)
+#undef TURBO_K_CASE
+                default: break;
+            }
+            __syncthreads();                          // smem reused by the next window
+            trace_mark(P, 5);
+        }
+        return;
+    }
+    // index order (fixed-K kernels always: their window index is the CTA index, which the
+    // compiler keeps -- with the window's fields -- in uniform registers)
     for (int64_t w = blockIdx.x; w < P.num_windows; w += gridDim.x) {
         const int rc = row_class((int64_t)P.windows[w].budget_bound + 1);
         if (rc >= TURBO_NUM_CLASSES || (P.cls >= 0 && rc != P.cls)) continue;   // other launch serves it
@@ -832,7 +854,7 @@ typedef void (*dp_kernel_t)(DpParams);
 template <int MODE, bool OSM, bool FUSE = false>
 dp_kernel_t pick_dp_kernel(int kmin, int kmax)
 {
-    if (kmin != kmax) return dp_cta_kernel<0, MODE, OSM, FUSE>;
+    if (!dp_kernel_fixed_k(kmin, kmax)) return dp_cta_kernel<0, MODE, OSM, FUSE>;
     switch (kmin) {
         case 4: return dp_cta_kernel<4, MODE, OSM, FUSE>;
         case 5: return dp_cta_kernel<5, MODE, OSM, FUSE>;

@@ -152,7 +152,8 @@ cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P0, 
         std::lock_guard<std::mutex> lk(mu);
         cache[ckey] = smem;
     }
-    const int64_t blocks = W;
+    const int64_t blocks = P.ordered ? (int64_t)P.cls_count : W;
+    if (blocks <= 0) return cudaSuccess;
     kern<<<(unsigned)blocks, 32 * G, smem, stream>>>(P);
     if (info) {
         info->mode = mode;

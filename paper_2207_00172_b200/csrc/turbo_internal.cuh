@@ -92,6 +92,8 @@ struct DpParams {
     int32_t debug;                 // long-window kernel tuning switches (TURBO_GRID_DEBUG)
     int32_t cls;                   // row-size class served by this launch (-1: every window)
     int32_t cls_count;             // windows in that class (residency / wave planning)
+    int32_t ordered;               // serve windows[cls_first + r].order, r < cls_count (LPT order)
+    int32_t cls_first;
     int64_t *stats;
     int64_t *trace;                // debug: per-CTA phase timestamps (turbo_debug_trace)
     int64_t trace_words;
@@ -106,6 +108,13 @@ __device__ __forceinline__ void trace_mark(const DpParams &P, int p)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         P.trace[(int64_t)blockIdx.x * 8 + p] = (int64_t)t;
     }
+}
+
+// Does pick_dp_kernel use a fixed-K kernel (K in {4, 5, 6, 8} for every window of the launch)?
+// Fixed-K kernels serve windows in index order; the mixed-K kernel follows the serving order.
+__host__ __device__ inline bool dp_kernel_fixed_k(int kmin, int kmax)
+{
+    return kmin == kmax && (kmin == 4 || kmin == 5 || kmin == 6 || kmin == 8);
 }
 
 struct DpLaunch {
@@ -142,15 +151,31 @@ cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams 
                            int smem_per_cta_max, cudaStream_t stream);
 size_t dp_smem_bytes(const DpParams &P, int nwarps);
 // cls >= 0: only the windows of that row-size class (the others were walked elsewhere)
+// Window selection of a per-class launch: the class's range of the serving order (ordered), or
+// every window filtered by class (cls < 0: all windows).
+struct WinSel {
+    int32_t cls = -1;
+    int32_t ordered = 0;
+    int32_t first = 0;
+    int32_t count = 0;
+    __host__ __device__ int64_t n_iter(int64_t W) const { return ordered ? count : W; }
+    // window of iteration r, or -1 when the class filter skips it
+    __device__ __forceinline__ int64_t window(const turbo_window_t *windows, int64_t r) const
+    {
+        if (ordered) return windows[first + r].order;
+        if (cls >= 0 && row_class((int64_t)windows[r].budget_bound + 1) != cls) return -1;
+        return r;
+    }
+};
 cudaError_t launch_backtrack(const turbo_window_t *windows, int32_t num_windows, const int32_t *opt_cost,
                              const uint8_t *workspace, const int32_t *best_cost, const uint8_t *feasible,
-                             uint8_t *exit_out, int num_sms, cudaStream_t stream, int cls = -1);
+                             uint8_t *exit_out, int num_sms, cudaStream_t stream, WinSel sel = WinSel());
 // turbo_schedule, windows of row-size class cls whose DP ran in plan mode: a5 walk with costs from
 // class ids + profile, then a6 statistics of those windows
 cudaError_t launch_walk_sched(const turbo_window_t *windows, int32_t num_windows, const turbo_profile_t *profiles,
                               const uint8_t *class_id, const uint8_t *workspace, const int32_t *best_gain,
                               const int32_t *best_cost, const uint8_t *feasible, uint8_t *exit_out, int64_t *stats,
-                              int num_sms, cudaStream_t stream, int cls);
+                              int num_sms, cudaStream_t stream, WinSel sel);
 cudaError_t launch_stats(const turbo_window_t *windows, int32_t num_windows, const uint8_t *class_id,
                          const uint8_t *exit_out, const int32_t *best_gain, const int32_t *best_cost,
                          const uint8_t *feasible, int64_t *stats, int num_sms, cudaStream_t stream);

@@ -38,7 +38,7 @@ class Window(ctypes.Structure):
     _fields_ = [("first_frame", ctypes.c_int64), ("first_option", ctypes.c_int64),
                 ("choice_offset", ctypes.c_int64), ("num_frames", ctypes.c_int32),
                 ("budget", ctypes.c_int32), ("profile", ctypes.c_int32), ("num_exits", ctypes.c_int32),
-                ("budget_bound", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("budget_bound", ctypes.c_int32), ("order", ctypes.c_int32)]
 
 
 class Shape(ctypes.Structure):
@@ -49,7 +49,8 @@ class Shape(ctypes.Structure):
                 ("total_frames", ctypes.c_int64), ("total_options", ctypes.c_int64),
                 ("total_cells", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
                 ("max_budget_small", ctypes.c_int32), ("num_big", ctypes.c_int32),
-                ("grid_scratch_offset", ctypes.c_int64), ("reserved1", ctypes.c_int64 * 2),
+                ("grid_scratch_offset", ctypes.c_int64), ("ordered", ctypes.c_int32), ("reserved2", ctypes.c_int32),
+                ("reserved3", ctypes.c_int64),
                 ("cls_count", ctypes.c_int32 * 4), ("cls_max_budget", ctypes.c_int32 * 4),
                 ("cls_max_frames", ctypes.c_int32 * 4), ("cls_max_options", ctypes.c_int32 * 4),
                 ("cls_min_exits", ctypes.c_int32 * 4), ("cls_max_exits", ctypes.c_int32 * 4)]
@@ -58,7 +59,7 @@ class Shape(ctypes.Structure):
 assert ctypes.sizeof(Window) == 48
 WINDOW_DTYPE = np.dtype([("first_frame", "<i8"), ("first_option", "<i8"), ("choice_offset", "<i8"),
                          ("num_frames", "<i4"), ("budget", "<i4"), ("profile", "<i4"), ("num_exits", "<i4"),
-                         ("budget_bound", "<i4"), ("reserved", "<i4")])
+                         ("budget_bound", "<i4"), ("order", "<i4")])
 assert WINDOW_DTYPE.itemsize == 48
 
 EXPORTS = ["turbo_mckp_workspace", "turbo_profile_lookup", "turbo_mckp_plan", "turbo_backtrack",

@@ -61,6 +61,36 @@ def _wins(tb, nf, bud, prof):
     return w
 
 
+def test_serving_order_groups_classes_and_puts_long_work_first(tb):
+    """turbo_window_t.order: a permutation, row-size classes ascending (long windows last),
+    largest N (B+1) (K+1) first inside a class, index ascending on ties (turbo.h)."""
+    profs = _profiles(tb, [5, 4, 16])
+    nf = [30, 7, 0, 300, 30, 60, 5, 30]
+    bud = [1000, 100, 5, 4096, 200, 100, 30000, 1000]
+    prof = [0, 1, 2, 0, 2, 1, 0, 0]
+    w = _wins(tb, nf, bud, prof)
+    s = tb.mckp_workspace(profs, w)
+    assert s.ordered == 1
+    order = w["order"].tolist()
+    assert sorted(order) == list(range(len(nf)))
+    K = w["num_exits"]
+    bounds = [256, 1024, 4608, 24576]
+
+    def cls(i):
+        cells = int(bud[i]) + 1
+        return next((c for c, b in enumerate(bounds) if cells <= b), 4)
+
+    def work(i):
+        return int(nf[i]) * (int(bud[i]) + 1) * (int(K[i]) + 1)
+    keys = [(cls(i), -work(i), i) for i in order]
+    assert keys == sorted(keys)
+    assert cls(order[-1]) == 4                      # the long window is served last
+    # one class, even work: index order, not flagged
+    w2 = _wins(tb, [30] * 5, [1000] * 5, [0] * 5)
+    s2 = tb.mckp_workspace(profs, w2)
+    assert s2.ordered == 0 and w2["order"].tolist() == list(range(5))
+
+
 def test_workspace_layout(tb):
     profs = _profiles(tb, [5, 4, 16])
     w = _wins(tb, [30, 7, 0, 300], [1000, 100, 5, 4096], [0, 1, 2, 0])
