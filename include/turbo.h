@@ -267,10 +267,10 @@ turbo_status_t turbo_stats(const turbo_shape_t *shape /* host */, const turbo_wi
 turbo_status_t turbo_debug_set_variant(int32_t variant);
 
 /* Debug / profiling hook: with trace != NULL (device memory, `words` int64 entries, caller-owned,
- * zeroed by the caller) the CTA DP kernels record, for CTA c, %globaltimer nanoseconds at
- * trace[8c + p]: p = 0 CTA start, 1 prologue done, 2 DP done, 3 optimum done, 4 plan
- * reconstructed, 5 CTA end (first window of each CTA). NULL disables (the default).
- * Process-wide; not needed in production. */
+ * zeroed by the caller) the CTA DP kernels record, for window w, %globaltimer nanoseconds at
+ * trace[8w + p]: p = 0 window start, 1 prologue done, 2 DP done, 3 optimum done, 4 plan
+ * reconstructed (fused kernels), 5 window end. NULL disables (the default). Process-wide; not
+ * needed in production. */
 turbo_status_t turbo_debug_trace(int64_t *trace, int64_t words);
 const char *turbo_status_string(turbo_status_t s);
 int32_t turbo_abi_version(void);

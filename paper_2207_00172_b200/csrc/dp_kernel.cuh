@@ -444,6 +444,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     const int tid = warp * 32 + lane;
     const int nthr = nwarps * 32;
 
+    trace_mark(P, w, 0);
     const turbo_window_t *win = P.windows + w;
     const int64_t ff = win->first_frame;
     const int64_t fo = win->first_option;
@@ -607,7 +608,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
         return;
     }
 
-    trace_mark(P, 1);
+    trace_mark(P, w, 1);
     if (P.debug & 64) return;                         // timing: prologue only
     // choice-plane stride (tiles per frame): the layout bound for HBM planes, exact for smem
     const int32_t gtiles = (int32_t)(((Bb + 32) >> 5) + RPT - 1) / RPT;
@@ -703,7 +704,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
         nxt = tmp;
     }
     // after the swap `cur` holds S_0 (in place: cur == nxt == rowA)
-    trace_mark(P, 2);
+    trace_mark(P, w, 2);
 
     // ---- a4: optimum extraction
     const int32_t RB = cur[B];
@@ -723,7 +724,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
         P.best_cost[w] = Cst;
         P.feasible[w] = feas ? 1 : 0;
     }
-    trace_mark(P, 3);
+    trace_mark(P, w, 3);
     if (MODE == DP_PLAN) return;
 
     // ---- a5 fused: forward backtrack from (frame 0, b = C*)
@@ -750,7 +751,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     }
     if (FUSE) {                                           // a6: CTA-private histograms
         if (nwarps > 1) __syncthreads(); else __syncwarp();
-        trace_mark(P, 4);
+        trace_mark(P, w, 4);
         for (int32_t i = tid; i < N; i += nthr) {
             const uint32_t k = exit_s ? exit_s[i] : P.exit_out[ff + i];   // global: visible after the barrier
             const uint32_t cls = class_of(i);
@@ -794,7 +795,6 @@ __global__ void __launch_bounds__(512, (KSEL == 0) ? 1 : 2) dp_cta_kernel(DpPara
     int32_t *cst = after;                                      // !OSM: costs for the backtrack
     uint32_t *sch = reinterpret_cast<uint32_t *>(after + P.cst_words);
     __shared__ uint32_t hist[FUSE ? 176 : 1];
-    trace_mark(P, 0);
     for (int32_t x = threadIdx.x; x < P.pad_words; x += blockDim.x) {
         rowA[x - P.pad_words] = NEG_R;
         if (nwarps > 1) rowB[x - P.pad_words] = NEG_R;
@@ -817,7 +817,7 @@ __global__ void __launch_bounds__(512, (KSEL == 0) ? 1 : 2) dp_cta_kernel(DpPara
                 default: break;
             }
             __syncthreads();                          // smem reused by the next window
-            trace_mark(P, 5);
+            trace_mark(P, w, 5);
         }
         return;
     }
@@ -842,7 +842,7 @@ __global__ void __launch_bounds__(512, (KSEL == 0) ? 1 : 2) dp_cta_kernel(DpPara
             }
         }
         __syncthreads();                              // smem reused by the next window
-        trace_mark(P, 5);
+        trace_mark(P, w, 5);
     }
 }
 

@@ -99,14 +99,13 @@ struct DpParams {
     int64_t trace_words;
 };
 
-// turbo_debug_trace: %globaltimer at phase p of this CTA (thread 0, first window only)
-__device__ __forceinline__ void trace_mark(const DpParams &P, int p)
+// turbo_debug_trace: %globaltimer at phase p of window w (thread 0 of the window's CTA)
+__device__ __forceinline__ void trace_mark(const DpParams &P, int64_t w, int p)
 {
-    if (P.trace != nullptr && threadIdx.x == 0 && (int64_t)blockIdx.x * 8 + 8 <= P.trace_words &&
-        P.trace[(int64_t)blockIdx.x * 8 + p] == 0) {
+    if (P.trace != nullptr && threadIdx.x == 0 && w * 8 + 8 <= P.trace_words) {
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        P.trace[(int64_t)blockIdx.x * 8 + p] = (int64_t)t;
+        P.trace[w * 8 + p] = (int64_t)t;
     }
 }
 
