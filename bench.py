@@ -288,8 +288,6 @@ def run_turbo(args):
                             stream)
         turbo.stats(b.shape, b.windows_dev, b.class_id, b.exit_out, b.best_gain, b.best_cost, b.feasible, b.stats,
                     stream)
-    launches_per_step = {"schedule": 1, "solve": 3, "plan": 4}[path]
-
     # L2 flush buffer (> 126 MB L2) written between timed steps (outside the timed events)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -298,6 +296,15 @@ def run_turbo(args):
         if dist is not None:
             dist.all_reduce(b.stats)
     torch.cuda.synchronize(dev)
+    # kernels one step launches, counted by the library itself (turbo_launch_count)
+    c0 = turbo.launch_count()
+    step()
+    torch.cuda.synchronize(dev)
+    launches_per_step = turbo.launch_count() - c0
+    c0 = turbo.launch_count()
+    dominant()
+    torch.cuda.synchronize(dev)
+    launches_dominant = turbo.launch_count() - c0
 
     # The step's kernels are captured once into a CUDA graph (launch latency off the device
     # timeline; the same C-ABI launches, replayed); the NCCL allreduce stays eager.
@@ -421,8 +428,10 @@ def run_turbo(args):
         "dp_cell_updates_per_s": total_cells / t_dp,
         "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
                      "frac": achieved / smem_peak, "traffic": traffic,
-                     "kernel": "turbo::dp_cta_kernel (" + {"schedule": "turbo_schedule", "solve": "turbo_mckp_solve",
-                                                           "plan": "turbo_mckp_plan"}[path] + ")",
+                     "kernel": ("turbo::dp_cta_kernel (" + {"schedule": "turbo_schedule", "solve": "turbo_mckp_solve",
+                                                            "plan": "turbo_mckp_plan"}[path] + ")"
+                                + (f"; timed as the whole call, {launches_dominant} launches (DP per row class,"
+                                   " walks of HBM planes, long-window grid kernel)" if launches_dominant > 1 else "")),
                      "note": "algorithmic smem bytes = cells x (4K+4) per launch (SURVEY.md 8(d)); "
                              "peak = SMs x 128 B/clk x sm_max_mhz (MEASURED_PEAKS.json), derived"},
         "e2e": {"value": total_cells / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

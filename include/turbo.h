@@ -270,8 +270,12 @@ turbo_status_t turbo_debug_set_variant(int32_t variant);
  * zeroed by the caller) the CTA DP kernels record, for window w, %globaltimer nanoseconds at
  * trace[8w + p]: p = 0 window start, 1 prologue done, 2 DP done, 3 optimum done, 4 plan
  * reconstructed (fused kernels), 5 window end. NULL disables (the default). Process-wide; not
- * needed in production. */
+ * needed in production. Returns TURBO_ERR_UNSUPPORTED unless the library was built with
+ * TURBO_TRACE defined (the marks are compiled out of production builds). */
 turbo_status_t turbo_debug_trace(int64_t *trace, int64_t words);
+/* Kernels this library has launched so far in the process (all threads and devices; graph
+ * capture counts the captured launches once). Lets a caller count the kernels of a call. */
+int64_t turbo_launch_count(void);
 const char *turbo_status_string(turbo_status_t s);
 int32_t turbo_abi_version(void);
 

@@ -35,7 +35,8 @@ def _stale() -> bool:
 
 
 def _compile(src: str, obj: str):
-    cmd = [NVCC, *NVCC_FLAGS, "-I", INCLUDE, "-I", CSRC, "-c", "-o", obj, src]
+    extra = ["-DTURBO_TRACE"] if os.environ.get("TURBO_TRACE") else []   # profiling build (trace marks)
+    cmd = [NVCC, *NVCC_FLAGS, *extra, "-I", INCLUDE, "-I", CSRC, "-c", "-o", obj, src]
     return subprocess.run(cmd, capture_output=True, text=True)
 
 

@@ -6,6 +6,7 @@
 #include <vector>
 #include <algorithm>
 #include <climits>
+#include <atomic>
 
 #include "turbo_internal.cuh"
 
@@ -104,6 +105,9 @@ static ForkJoin *fork_join_for_device()
 // twice the row(s): otherwise they would cap the CTAs resident per SM (and HBM/L2 is fine)
 static int64_t smem_choice_floor = 16 * 1024;
 
+static std::atomic<int64_t> g_launches{0};
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 }  // namespace turbo
 
 using namespace turbo;
@@ -125,11 +129,16 @@ const char *turbo_status_string(turbo_status_t s)
     return "unknown";
 }
 
+int64_t turbo_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
 static int64_t *g_trace = nullptr;
 static int64_t g_trace_words = 0;
 
 turbo_status_t turbo_debug_trace(int64_t *trace, int64_t words)
 {
+#ifndef TURBO_TRACE
+    if (trace != nullptr) return TURBO_ERR_UNSUPPORTED;   // library built without the marks
+#endif
     if (trace != nullptr && words < 8) return TURBO_ERR_INVALID_ARG;
     g_trace = trace;
     g_trace_words = trace ? words : 0;

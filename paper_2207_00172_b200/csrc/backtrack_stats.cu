@@ -85,6 +85,7 @@ cudaError_t launch_backtrack(const turbo_window_t *windows, int32_t num_windows,
     int64_t blocks = (sel.n_iter(num_windows) + wpc - 1) / wpc;
     const int64_t cap = (int64_t)num_sms * 16;
     if (blocks > cap) blocks = cap;
+    note_launch();
     backtrack_kernel<<<(unsigned)blocks, threads, 0, stream>>>(windows, num_windows, opt_cost, workspace,
                                                                best_cost, feasible, exit_out, sel);
     return cudaGetLastError();
@@ -194,6 +195,7 @@ cudaError_t launch_walk_sched(const turbo_window_t *windows, int32_t num_windows
     int64_t blocks = (sel.n_iter(num_windows) + wpc - 1) / wpc;
     const int64_t cap = (int64_t)num_sms * 16;
     if (blocks > cap) blocks = cap;
+    note_launch();
     walk_sched_kernel<<<(unsigned)blocks, threads, 0, stream>>>(windows, num_windows, profiles, class_id, workspace,
                                                                 best_gain, best_cost, feasible, exit_out,
                                                                 reinterpret_cast<unsigned long long *>(stats), sel);
@@ -260,6 +262,7 @@ cudaError_t launch_stats(const turbo_window_t *windows, int32_t num_windows, con
     int64_t blocks = ((int64_t)num_windows + wpc - 1) / wpc;
     const int64_t cap = (int64_t)num_sms * 2;
     if (blocks > cap) blocks = cap;
+    note_launch();
     stats_kernel<<<(unsigned)blocks, threads, 0, stream>>>(windows, num_windows, class_id, exit_out, best_gain,
                                                            best_cost, feasible,
                                                            reinterpret_cast<unsigned long long *>(stats));

@@ -617,6 +617,7 @@ cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams 
         P.debug = dbg ? atoi(dbg) : 0;
     }
     void *args[] = {(void *)&P, (void *)&seg, (void *)&tag_base};
+    note_launch();
     return cudaLaunchCooperativeKernel((const void *)kern, dim3(NP), dim3(GRID_THREADS), args, smem, stream);
 }
 

@@ -154,6 +154,7 @@ cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P0, 
     }
     const int64_t blocks = P.ordered ? (int64_t)P.cls_count : W;
     if (blocks <= 0) return cudaSuccess;
+    note_launch();
     kern<<<(unsigned)blocks, 32 * G, smem, stream>>>(P);
     if (info) {
         info->mode = mode;

@@ -148,6 +148,7 @@ cudaError_t launch_heuristic(const turbo_shape_t *shape, const turbo_window_t *w
     }
     int64_t blocks = ((int64_t)shape->num_windows + wpc - 1) / wpc;
     if (blocks > (int64_t)num_sms * 64) blocks = (int64_t)num_sms * 64;
+    note_launch();
     heuristic_kernel<<<(unsigned)blocks, 32 * wpc, smem, stream>>>(P);
     return cudaGetLastError();
 }

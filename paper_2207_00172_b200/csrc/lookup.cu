@@ -77,6 +77,7 @@ cudaError_t launch_lookup(const turbo_profile_t *profiles, turbo_window_t *windo
     int64_t blocks = ((int64_t)num_windows + warps - 1) / warps;
     const int64_t cap = (int64_t)num_sms * 8;
     if (blocks > cap) blocks = cap;
+    note_launch();
     lookup_kernel<<<(unsigned)blocks, threads, 0, stream>>>(profiles, windows, num_windows, class_id, capacity,
                                                             base_cost, opt_gain, opt_cost, status);
     return cudaGetLastError();

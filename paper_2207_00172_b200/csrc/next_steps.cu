@@ -50,6 +50,7 @@ cudaError_t launch_bucketize(const float *theta, int64_t n, int32_t C, float inv
     int64_t blocks = ((n >> 2) + 255) / 256;
     if (blocks > (int64_t)num_sms * 8) blocks = (int64_t)num_sms * 8;
     if (blocks < 1) blocks = 1;
+    note_launch();
     bucketize_kernel<<<(unsigned)blocks, 256, 0, stream>>>(theta, n, inv_width, C, cls);
     return cudaGetLastError();
 }
@@ -106,6 +107,7 @@ cudaError_t launch_batches(const turbo_window_t *windows, int32_t num_windows, c
     if (num_windows <= 0) return cudaSuccess;
     int64_t blocks = ((int64_t)num_windows + 7) / 8;
     if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
+    note_launch();
     batches_kernel<<<(unsigned)blocks, 256, 0, stream>>>(windows, num_windows, exit_out, count, order);
     return cudaGetLastError();
 }

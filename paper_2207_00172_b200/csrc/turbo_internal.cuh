@@ -99,14 +99,18 @@ struct DpParams {
     int64_t trace_words;
 };
 
-// turbo_debug_trace: %globaltimer at phase p of window w (thread 0 of the window's CTA)
+// turbo_debug_trace: %globaltimer at phase p of window w (thread 0 of the window's CTA). Compiled
+// in only with -DTURBO_TRACE (TURBO_TRACE=1 python -m paper_2207_00172_b200.build): the marks
+// change the register allocation of the 64-register DP kernels, so production builds omit them.
 __device__ __forceinline__ void trace_mark(const DpParams &P, int64_t w, int p)
 {
+#ifdef TURBO_TRACE
     if (P.trace != nullptr && threadIdx.x == 0 && w * 8 + 8 <= P.trace_words) {
         uint64_t t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         P.trace[w * 8 + p] = (int64_t)t;
     }
+#endif
 }
 
 // Does pick_dp_kernel use a fixed-K kernel (K in {4, 5, 6, 8} for every window of the launch)?
@@ -115,6 +119,9 @@ __host__ __device__ inline bool dp_kernel_fixed_k(int kmin, int kmax)
 {
     return kmin == kmax && (kmin == 4 || kmin == 5 || kmin == 6 || kmin == 8);
 }
+
+// every kernel launch of the library is counted (turbo_launch_count)
+void note_launch();
 
 struct DpLaunch {
     int mode;

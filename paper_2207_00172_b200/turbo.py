@@ -65,7 +65,7 @@ assert WINDOW_DTYPE.itemsize == 48
 EXPORTS = ["turbo_mckp_workspace", "turbo_profile_lookup", "turbo_mckp_plan", "turbo_backtrack",
            "turbo_mckp_solve", "turbo_mckp_solve_workspace", "turbo_schedule", "turbo_heuristic_plan", "turbo_stats",
            "turbo_bucketize", "turbo_batches",
-           "turbo_debug_set_variant", "turbo_debug_trace",
+           "turbo_debug_set_variant", "turbo_debug_trace", "turbo_launch_count",
            "turbo_status_string", "turbo_abi_version"]
 
 _lib = None
@@ -94,6 +94,8 @@ def load(path: Optional[str] = None):
     lib.turbo_batches.argtypes = [vp, vp, vp, vp, vp, vp]
     lib.turbo_debug_set_variant.argtypes = [i32]
     lib.turbo_debug_trace.argtypes = [vp, i64]
+    lib.turbo_launch_count.argtypes = []
+    lib.turbo_launch_count.restype = i64
     lib.turbo_status_string.restype = ctypes.c_char_p
     lib.turbo_abi_version.restype = i32
     for name in EXPORTS:
@@ -213,6 +215,11 @@ def stats(shape, windows_dev, class_id, exit_out, best_gain, best_cost, feasible
 
 def debug_set_variant(v: int):
     _check("turbo_debug_set_variant", load().turbo_debug_set_variant(int(v)))
+
+
+def launch_count() -> int:
+    """Kernels libturbo has launched so far in this process (turbo.h turbo_launch_count)."""
+    return int(load().turbo_launch_count())
 
 
 def debug_trace(buf=None):

@@ -1,5 +1,7 @@
 #!/usr/bin/env python
-"""Per-window phase timeline of the CTA DP kernels (turbo_debug_trace, %globaltimer ns):
+"""Per-window phase timeline of the CTA DP kernels (turbo_debug_trace, %globaltimer ns; needs a
+library built with the trace marks: TURBO_TRACE=1 python -c "from paper_2207_00172_b200 import build;
+build.build(force=True)"):
 window start, prologue, DP, optimum, in-kernel plan reconstruction, end -- per row-size class,
 on bench.py's workload shape."""
 import argparse

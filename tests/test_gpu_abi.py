@@ -112,3 +112,19 @@ def test_stream_ordering_nondefault_stream(tb):
     import oracle
     want = oracle.run(wl)
     np.testing.assert_array_equal(r["exits"], want["exits"])
+
+
+def test_launch_count_counts_the_kernels_of_a_call(tb):
+    """turbo_launch_count: one fused launch for a batch whose planes stay on chip (c2 shape);
+    DP + plane walk when the planes go to HBM (c3 shape); lookup + solve + stats on that path."""
+    import torch
+    for cfg, n, expect_sched in ((2, 16, 1), (3, 8, 2)):
+        b = tb.batch_from_workload(synth.make_config(cfg, num_windows=n))
+        c0 = tb.launch_count()
+        tb.run_path(b, fused="all")
+        torch.cuda.synchronize()
+        assert tb.launch_count() - c0 == expect_sched
+        c0 = tb.launch_count()
+        tb.run_path(b, fused=True)
+        torch.cuda.synchronize()
+        assert tb.launch_count() - c0 == 2 + expect_sched
