@@ -186,3 +186,52 @@ def run(wl, mode: str = "table", threads: Optional[int] = None) -> dict:
     st = stats(wl.num_frames, wl.class_id, exits, bg, bc, fe) if mode != "value" else None
     return dict(budget=bud, opt_gain=og, opt_cost=oc, first_option=fo, bad_frame=bad,
                 exits=exits, best_gain=bg, best_cost=bc, feasible=fe, stats=st)
+
+
+def batched_brute(cls, gain, C, K, batch, ncap, B):
+    """NEXT-4, one tiny window by enumeration of all K^N plans (turbo_oracle.c
+    oracle_batched_brute). Returns (G*, C*, counts of the lexicographically smallest optimal
+    count vector, feasible)."""
+    lib = _load()
+    cl = np.ascontiguousarray(cls, dtype=np.uint8)
+    g, I = _i32(gain), _i32(batch)
+    bg, bc = ctypes.c_int64(0), ctypes.c_int64(0)
+    cnt = np.zeros(16, dtype=np.int32)
+    fe = ctypes.c_uint8(0)
+    e = lib.oracle_batched_brute(ctypes.c_int32(len(cl)), ctypes.c_int32(C), ctypes.c_int32(K), _p(cl), _p(g), _p(I),
+                                 ctypes.c_int32(ncap), ctypes.c_int32(int(B)), ctypes.byref(bg), ctypes.byref(bc),
+                                 _p(cnt), ctypes.byref(fe))
+    if e:
+        raise RuntimeError(f"oracle_batched_brute failed: {e}")
+    return int(bg.value), int(bc.value), cnt[:K].copy(), int(fe.value)
+
+
+def batched(wl):
+    """NEXT-4 on a batched workload (synth profiles_batch): exact optimum per window by
+    count-vector enumeration (turbo_oracle.c oracle_batched_enum). Returns (exits, G*, C*,
+    feasible)."""
+    lib = _load()
+    gain = np.concatenate([_i32(g) for g in wl.profiles_gain])
+    gsz = np.array([len(g) for g in wl.profiles_gain], dtype=np.int64)
+    goff = np.zeros(len(gsz), dtype=np.int64)
+    goff[1:] = np.cumsum(gsz[:-1])
+    bt = np.concatenate([_i32(t) for t in wl.profiles_batch])
+    bsz = np.array([len(t) for t in wl.profiles_batch], dtype=np.int64)
+    boff = np.zeros(len(bsz), dtype=np.int64)
+    boff[1:] = np.cumsum(bsz[:-1])
+    C = np.array([s[0] for s in wl.profiles_shape], dtype=np.int32)
+    K = np.array([s[1] for s in wl.profiles_shape], dtype=np.int32)
+    W = wl.num_windows
+    F = wl.total_frames
+    ff = _i64(wl.first_frame)
+    exits = np.zeros(max(F, 1), dtype=np.uint8)
+    bg = np.zeros(max(W, 1), dtype=np.int64)
+    bc = np.zeros(max(W, 1), dtype=np.int64)
+    fe = np.zeros(max(W, 1), dtype=np.uint8)
+    cls = np.ascontiguousarray(wl.class_id, dtype=np.uint8)
+    e = lib.oracle_batched_batch(ctypes.c_int32(W), _p(_i32(wl.num_frames)), _p(_i32(wl.budget)), _p(_i32(wl.profile)),
+                                 _p(ff), _p(cls if F else np.zeros(1, np.uint8)), _p(gain), _p(goff), _p(C), _p(K),
+                                 _p(bt), _p(boff), ctypes.c_int32(wl.batch_cap), _p(exits), _p(bg), _p(bc), _p(fe))
+    if e:
+        raise RuntimeError(f"oracle_batched_batch failed: {e}")
+    return exits[:F], bg[:W], bc[:W], fe[:W]

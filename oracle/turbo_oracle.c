@@ -414,3 +414,202 @@ void oracle_batches(int32_t num_windows, const int32_t *num_frames, const uint8_
         f0 += N;
     }
 }
+
+/* ------------------------------------------------------------------ NEXT-4: batched-cost GAP
+ * PAPER.md:523-525 (§5.2): maximise sum_x P_{kappa_x}^{theta'_x} subject to f(sum I_kappa) <= T,
+ * where f batches the frames that run at the same level; PAPER.md:533 calls it a non-linear GAP.
+ * Latency does not depend on frame content, so a plan's cost depends only on its
+ * counts n_k = #{x : kappa_x = k}:   cost(n) = sum_k I_k(n_k),
+ * with I_k(n) the batch latency of n frames at level k (table I[k * (ncap + 1) + n]).
+ * Reading R18: the result is the unique maximum of -- larger gain, then smaller
+ * cost, then the lexicographically smaller count vector read from the top level down
+ * (n_{K-1}, ..., n_0), then the CANONICAL assignment for those counts: frames sorted by
+ * (class, arrival index) fill level 0 first, then level 1, ... (contiguous blocks).
+ * Reading R19: gains have increasing differences in the class ("the hardest
+ * frames have the largest marginals"): g[c+1][k+1] - g[c+1][k] >= g[c][k+1] - g[c][k]. Then the
+ * canonical assignment is optimal for its counts (assortative matching solves the C x K
+ * transportation problem), so the optimum is a maximum over count vectors.
+ * Infeasible (no count vector fits): all frames at level 0, feasible = 0, G = sum g[c_x][0],
+ * C = I_0(N) (the analogue of reading R8).
+ * Return: 0 ok; -1 bad arguments; -2 gains violate R19 (enum only). */
+
+static int batched_r19_ok(int32_t C, int32_t K, const int32_t *g)
+{
+    for (int32_t c = 0; c + 1 < C; ++c)
+        for (int32_t k = 0; k + 1 < K; ++k)
+            if ((int64_t)g[(c + 1) * K + k + 1] - g[(c + 1) * K + k] < (int64_t)g[c * K + k + 1] - g[c * K + k])
+                return 0;
+    return 1;
+}
+
+/* canonical assignment of counts n[] to the N frames (see R18) */
+static void batched_assign(int32_t N, int32_t C, int32_t K, const uint8_t *cls, const int32_t *n, uint8_t *exits)
+{
+    int32_t level = 0, left = n[0];
+    for (int32_t c = 0; c < C; ++c)
+        for (int32_t x = 0; x < N; ++x) {
+            if ((int32_t)cls[x] != c) continue;
+            while (left == 0 && level + 1 < K) left = n[++level];
+            exits[x] = (uint8_t)level;
+            left -= 1;
+        }
+    /* frames whose class is >= C never occur (validated by the caller) */
+}
+
+/* is count vector a lexicographically smaller than b, read from the top level down? */
+static int batched_lex_less(int32_t K, const int32_t *a, const int32_t *b)
+{
+    for (int32_t k = K - 1; k >= 0; --k)
+        if (a[k] != b[k]) return a[k] < b[k];
+    return 0;
+}
+
+/* Brute force over all K^N plans (tiny N): the plain definition, no R19 needed for G*, C*;
+ * best_counts = the lexicographically smallest count vector among the optimal plans. */
+int oracle_batched_brute(int32_t N, int32_t C, int32_t K, const uint8_t *cls, const int32_t *g,
+                         const int32_t *I, int32_t ncap, int32_t B, int64_t *best_gain, int64_t *best_cost,
+                         int32_t *best_counts, uint8_t *feasible)
+{
+    if (N < 0 || N > 12 || K < 2 || K > 16 || N > ncap) return -1;
+    int64_t total = 1;
+    for (int32_t i = 0; i < N; ++i) total *= K;
+    int32_t plan[16], cnt[16];
+    int have = 0;
+    int64_t bg = 0, bc = 0;
+    int32_t bn[16];
+    for (int64_t code = 0; code < total; ++code) {
+        int64_t r = code;
+        for (int32_t k = 0; k < K; ++k) cnt[k] = 0;
+        int64_t gain = 0;
+        for (int32_t i = 0; i < N; ++i) {
+            plan[i] = (int32_t)(r % K);
+            r /= K;
+            cnt[plan[i]] += 1;
+            gain += g[(int32_t)cls[i] * K + plan[i]];
+        }
+        int64_t cost = 0;
+        for (int32_t k = 0; k < K; ++k) cost += I[k * (ncap + 1) + cnt[k]];
+        if (cost > B) continue;
+        int better = !have || gain > bg || (gain == bg && cost < bc) ||
+                     (gain == bg && cost == bc && batched_lex_less(K, cnt, bn));
+        if (better) {
+            have = 1;
+            bg = gain;
+            bc = cost;
+            for (int32_t k = 0; k < K; ++k) bn[k] = cnt[k];
+        }
+    }
+    if (!have) {
+        int64_t g0 = 0;
+        for (int32_t i = 0; i < N; ++i) g0 += g[(int32_t)cls[i] * K];
+        for (int32_t k = 0; k < K; ++k) bn[k] = k == 0 ? N : 0;
+        bg = g0;
+        bc = I[N];
+    }
+    *best_gain = bg;
+    *best_cost = bc;
+    *feasible = (uint8_t)have;
+    for (int32_t k = 0; k < K; ++k) best_counts[k] = bn[k];
+    return 0;
+}
+
+/* recursive enumeration of the compositions n_0 + ... + n_{K-1} = N */
+typedef struct {
+    int32_t N, C, K, ncap, B;
+    const int32_t *I;
+    const int64_t *P;            /* P[k * (N + 1) + j]: gain of the first j sorted frames at level k */
+    int32_t n[16], bn[16];
+    int have;
+    int64_t bg, bc;
+} batched_ctx;
+
+static void batched_rec(batched_ctx *x, int32_t k, int32_t left)
+{
+    if (k == x->K - 1) {
+        x->n[k] = left;
+        int64_t cost = 0, gain = 0;
+        int32_t s = 0;
+        for (int32_t j = 0; j < x->K; ++j) {
+            cost += x->I[j * (x->ncap + 1) + x->n[j]];
+            gain += x->P[j * (x->N + 1) + s + x->n[j]] - x->P[j * (x->N + 1) + s];
+            s += x->n[j];
+        }
+        if (cost > x->B) return;
+        int better = !x->have || gain > x->bg || (gain == x->bg && cost < x->bc) ||
+                     (gain == x->bg && cost == x->bc && batched_lex_less(x->K, x->n, x->bn));
+        if (better) {
+            x->have = 1;
+            x->bg = gain;
+            x->bc = cost;
+            for (int32_t j = 0; j < x->K; ++j) x->bn[j] = x->n[j];
+        }
+        return;
+    }
+    for (int32_t v = 0; v <= left; ++v) {
+        x->n[k] = v;
+        batched_rec(x, k + 1, left - v);
+    }
+}
+
+/* Exact optimum by count-vector enumeration (R18, R19): one window. */
+int oracle_batched_enum(int32_t N, int32_t C, int32_t K, const uint8_t *cls, const int32_t *g, const int32_t *I,
+                        int32_t ncap, int32_t B, uint8_t *exits, int64_t *best_gain, int64_t *best_cost,
+                        uint8_t *feasible)
+{
+    if (N < 0 || K < 2 || K > 16 || C < 1 || N > ncap) return -1;
+    if (!batched_r19_ok(C, K, g)) return -2;
+    for (int32_t i = 0; i < N; ++i)
+        if ((int32_t)cls[i] >= C) return -1;
+    /* frames in canonical order (class, arrival) and the per-level prefix gains */
+    int32_t *order = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N > 0 ? N : 1));
+    int64_t *P = (int64_t *)malloc(sizeof(int64_t) * (size_t)K * (size_t)(N + 1));
+    int32_t t = 0;
+    for (int32_t c = 0; c < C; ++c)
+        for (int32_t i = 0; i < N; ++i)
+            if ((int32_t)cls[i] == c) order[t++] = i;
+    for (int32_t k = 0; k < K; ++k) {
+        P[k * (N + 1)] = 0;
+        for (int32_t j = 0; j < N; ++j) P[k * (N + 1) + j + 1] = P[k * (N + 1) + j] + g[(int32_t)cls[order[j]] * K + k];
+    }
+    batched_ctx x;
+    memset(&x, 0, sizeof(x));
+    x.N = N;
+    x.C = C;
+    x.K = K;
+    x.ncap = ncap;
+    x.B = B;
+    x.I = I;
+    x.P = P;
+    batched_rec(&x, 0, N);
+    if (!x.have) {
+        int64_t g0 = 0;
+        for (int32_t i = 0; i < N; ++i) g0 += g[(int32_t)cls[i] * K];
+        for (int32_t k = 0; k < K; ++k) x.bn[k] = k == 0 ? N : 0;
+        x.bg = g0;
+        x.bc = I[N];
+    }
+    batched_assign(N, C, K, cls, x.bn, exits);
+    *best_gain = x.bg;
+    *best_cost = x.bc;
+    *feasible = (uint8_t)x.have;
+    free(order);
+    free(P);
+    return 0;
+}
+
+/* windows of a batch (one table pair per window via profile index) */
+int oracle_batched_batch(int32_t num_windows, const int32_t *num_frames, const int32_t *budget,
+                         const int32_t *profile, const int64_t *first_frame, const uint8_t *class_id,
+                         const int32_t *gains, const int64_t *gain_off, const int32_t *C, const int32_t *K,
+                         const int32_t *batch, const int64_t *batch_off, int32_t ncap, uint8_t *exits,
+                         int64_t *best_gain, int64_t *best_cost, uint8_t *feasible)
+{
+    for (int32_t w = 0; w < num_windows; ++w) {
+        const int32_t p = profile[w];
+        int e = oracle_batched_enum(num_frames[w], C[p], K[p], class_id + first_frame[w], gains + gain_off[p],
+                                    batch + batch_off[p], ncap, budget[w], exits + first_frame[w], &best_gain[w],
+                                    &best_cost[w], &feasible[w]);
+        if (e) return e;
+    }
+    return 0;
+}

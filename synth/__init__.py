@@ -34,4 +34,8 @@ from .workloads import (  # noqa: F401
     regular_costs,
     concat_workloads,
     make_long_window,
+    make_batched_config,
+    make_batched_random,
+    supermodular_gain_table,
+    batch_latency_table,
 )

@@ -37,6 +37,10 @@ class Workload:
     profile: np.ndarray                      # int32 [W]  profile index per window
     class_id: np.ndarray                     # uint8 [F]  concatenated per window
     meta: dict = field(default_factory=dict)
+    # NEXT-4 (batched cost): per profile int32 [K * (batch_cap + 1)], I_k(n) = latency of a batch
+    # of n frames at level k (row-major (level, n)); None for the per-frame-cost workloads
+    profiles_batch: Optional[List[np.ndarray]] = None
+    batch_cap: int = 0
 
     @property
     def num_windows(self) -> int:
@@ -307,3 +311,90 @@ def make_long_window(seed: int, N: int, K: int, B: int, c_max: Optional[int] = N
         g, c = _paper_profile(K, cm, C)
     cls = _class_ids(seed, np.array([N], np.int32), np.array([0.35]), window_ids=np.array([seed]))
     return _wl(f"long{seed}", [g], [c], [(C, K)], [N], [B], [0], cls, base_cost, {"seed": seed, "c_max": cm})
+
+
+# ----------------------------------------------------------------------------- NEXT-4 inputs
+def supermodular_gain_table(K: int, C: int = NUM_CLASSES) -> np.ndarray:
+    """NEXT-4 profile: g[c][k] = A_c * H_k (units of 0.001 mAP point), A_c = round(1400 *
+    0.604**(9-c)) (Appendix-B amplitude), H_0 = 0, H_k = round(10 * (0.561 +
+    0.439 (k-1)/(K-2))). Both factors are non-decreasing integers, so the table has increasing
+    differences in the class exactly (reading R19)."""
+    A = [int(math.floor(1400.0 * 0.604 ** (9 - c) + 0.5)) for c in range(C)]
+    H = [0] + [int(math.floor(10.0 * (1.0 if K == 2 else 0.561 + 0.439 * (k - 1) / (K - 2)) + 0.5))
+               for k in range(1, K)]
+    return np.array([[A[c] * H[k] for k in range(K)] for c in range(C)], dtype=np.int32).reshape(-1)
+
+
+def batch_latency_table(K: int, c_max: int, cap: int) -> np.ndarray:
+    """I_k(n) for n = 0..cap: 0 for an empty batch, else ceil(c_k (2 + 3n) / 5) -- a fixed 40 %
+    launch share plus 60 % per frame (a batch of n frames costs less than n singles, the reason
+    the paper batches same-level frames), c_k = ceil(c_max k / (K-1))."""
+    ck = regular_costs(K, c_max)
+    t = np.zeros((K, cap + 1), dtype=np.int64)
+    for k in range(K):
+        for n in range(1, cap + 1):
+            t[k, n] = -((-int(ck[k]) * (2 + 3 * n)) // 5)
+    return t.reshape(-1).astype(np.int32)
+
+
+BATCHED_CONFIGS = {
+    1: dict(W=1, N=30, K=4, B=120),
+    2: dict(W=1024, N=30, K=5, B=1000),
+}
+
+
+def make_batched_config(k: int, num_windows: Optional[int] = None, window_offset: int = 0) -> Workload:
+    """NEXT-4 workload b<k>: the c<k> window shapes and class mix, batched latency tables."""
+    p = BATCHED_CONFIGS[k]
+    W = p["W"] if num_windows is None else num_windows
+    N, K, B = p["N"], p["K"], p["B"]
+    seed = BASE_SEED + 100 + k
+    wid = np.arange(window_offset, window_offset + W, dtype=np.int64)
+    nf = np.full(W, N, dtype=np.int32)
+    cls = _class_ids(seed, nf, np.full(W, 0.35), window_ids=wid)
+    c_max = -((-3 * B) // N)
+    g = supermodular_gain_table(K)
+    wl = _wl(f"b{k}", [g], [np.tile(regular_costs(K, c_max), NUM_CLASSES).astype(np.int32)], [(NUM_CLASSES, K)],
+             nf, np.full(W, B), np.zeros(W), cls, 84, {"config": f"b{k}", "N": N, "K": K, "B": B, "c_max": c_max})
+    wl.profiles_batch = [batch_latency_table(K, c_max, N)]
+    wl.batch_cap = N
+    return wl
+
+
+def make_batched_random(seed: int, W: int, max_frames: int = 8, K: int = 3, C: int = 4, max_budget: int = 40,
+                        linear: bool = False) -> Workload:
+    """Parity set for NEXT-4: random supermodular gains (negative entries allowed), random
+    non-decreasing batch tables (or linear ones, I_k(n) = n c_k, when `linear`), random budgets
+    including infeasible windows (I_0(n) > 0 in some profiles)."""
+    wid = np.arange(W, dtype=np.int64)
+    nf = rand_int(seed, S_TN, wid, 0, max_frames).astype(np.int32)
+    bud = rand_int(seed, S_TBUD, wid, 0, max_budget).astype(np.int32)
+    cap = max_frames
+    gains, costs, batches, shapes = [], [], [], []
+    P = 8
+    for q in range(P):
+        # A_c and H_k non-decreasing integers (possibly negative offsets): g = A_c H_k + r_k
+        A = np.cumsum(rand_int(seed, S_TGAIN * 97 + q, np.arange(C), 0, 3)) - 2
+        H = np.cumsum(rand_int(seed, S_TGAIN * 89 + q, np.arange(K), 0, 3))
+        r = rand_int(seed, S_TGAIN * 83 + q, np.arange(K), -3, 3)
+        g = (A[:, None] * H[None, :] + r[None, :]).astype(np.int32).reshape(-1)
+        ck = rand_int(seed, S_TCOST * 97 + q, np.arange(K), 0, 6)
+        fixed = rand_int(seed, S_TBASE * 97 + q, np.arange(K), 0, 4)
+        t = np.zeros((K, cap + 1), dtype=np.int64)
+        for k in range(K):
+            for n in range(1, cap + 1):
+                t[k, n] = n * ck[k] if linear else fixed[k] + n * ck[k] - (n // 3)
+            t[k] = np.maximum.accumulate(t[k])
+        if not linear and q % 3 == 0:
+            t[0, 1:] += 1                                         # I_0(n) > 0: infeasible windows
+        gains.append(g)
+        costs.append(np.tile(ck, C).astype(np.int32))
+        batches.append(t.reshape(-1).astype(np.int32))
+        shapes.append((C, K))
+    prof = rand_int(seed, S_PROF, wid, 0, P - 1).astype(np.int32)
+    F = int(nf.sum())
+    cls = rand_int(seed, S_CLASS, np.arange(F, dtype=np.int64), 0, C - 1).astype(np.uint8)
+    wl = _wl(f"batched_random_{seed}", gains, costs, shapes, nf, bud, prof, cls, 0)
+    wl.profiles_batch = batches
+    wl.batch_cap = cap
+    return wl
