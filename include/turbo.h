@@ -260,6 +260,27 @@ turbo_status_t turbo_stats(const turbo_shape_t *shape /* host */, const turbo_wi
                            const int32_t *best_gain, const int32_t *best_cost,
                            const uint8_t *feasible, int64_t *stats, turbo_stream_t stream);
 
+/* NEXT-4: exact plans under the paper's batched latency constraint:
+ * cost(plan) = sum_k I_k(n_k), n_k = frames planned at level k, I_k(n) = the latency of a batch of
+ * n frames at level k (latency independent of content :103). Result per window:
+ * larger gain, then smaller cost, then the count vector (n_{K-1}, ..., n_0) lexicographically
+ * smaller, then the canonical assignment -- frames sorted by (class, arrival index) fill level 0,
+ * then 1, ... (readings R18, R19). Preconditions: the profile's gains have increasing
+ * differences in the class, g[c+1][k+1] - g[c+1][k] >= g[c][k+1] - g[c][k] (R19)
+ * and |g| <= 2^24; a window violating them (or with budget < 0) is planned all-zero, feasible = 0,
+ * gain = cost = 0, and status[1] = min such window; a class id >= C sets status[0] like the lookup.
+ * batch_cost (device int32): per profile p a table at p * 16 * (batch_cap + 1), row k (k < K_p) =
+ * I_k(0 .. batch_cap). Host checks (TURBO_ERR_UNSUPPORTED): max_frames <= batch_cap <= 255,
+ * C(max_frames + max_exits - 1, max_exits - 1) <= 2^26 count vectors per window and
+ * (max_frames + 1)^(max_exits - 1) < 2^62. Infeasible windows: all frames at level 0,
+ * feasible = 0, best_gain = sum g[c_x][0], best_cost = I_0(N). Budgets are read from
+ * windows[w].budget (set them on the device, or a1 via turbo_profile_lookup). Stream-ordered. */
+turbo_status_t turbo_batched_plan(const turbo_shape_t *shape /* host */, const turbo_window_t *windows,
+                                  const turbo_profile_t *profiles /* device */, const int32_t *batch_cost,
+                                  int32_t batch_cap, const uint8_t *class_id, int32_t *best_gain,
+                                  int32_t *best_cost, uint8_t *feasible, uint8_t *exit_out, int64_t *status,
+                                  turbo_stream_t stream);
+
 /* Debug / test hook: force a DP kernel variant. variant & 3: 0 = automatic, 1 = fused solve
  * keeps choice planes in shared memory (when they fit the per-CTA maximum), 2 = in HBM;
  * variant & 4: do not stage option tables in shared memory (shuffle broadcast instead).

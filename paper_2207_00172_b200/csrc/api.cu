@@ -554,6 +554,32 @@ turbo_status_t turbo_heuristic_plan(const turbo_shape_t *shape, const turbo_wind
     return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
 }
 
+turbo_status_t turbo_batched_plan(const turbo_shape_t *shape, const turbo_window_t *windows,
+                                  const turbo_profile_t *profiles, const int32_t *batch_cost, int32_t batch_cap,
+                                  const uint8_t *class_id, int32_t *best_gain, int32_t *best_cost, uint8_t *feasible,
+                                  uint8_t *exit_out, int64_t *status, turbo_stream_t stream)
+{
+    if (!shape) return TURBO_ERR_INVALID_ARG;
+    if (shape->num_windows == 0) return TURBO_OK;
+    if (!windows || !profiles || !batch_cost || !best_gain || !best_cost || !feasible || !status)
+        return TURBO_ERR_INVALID_ARG;
+    if (shape->total_frames > 0 && (!class_id || !exit_out)) return TURBO_ERR_INVALID_ARG;
+    if (batch_cap < 0 || batch_cap > 255 || shape->max_frames > batch_cap) return TURBO_ERR_UNSUPPORTED;
+    // count vectors per window: C(N + K - 1, K - 1) at the batch maxima; counts code (N+1)^(K-1)
+    const int64_t N = shape->max_frames, K = shape->max_exits;
+    double vectors = 1.0, code = 1.0;
+    for (int64_t r = 0; r < K - 1; ++r) {
+        vectors = vectors * (double)(N + K - 1 - r) / (double)(r + 1);
+        code *= (double)(N + 1);
+    }
+    if (vectors > (double)(1 << 26) || code >= 4.6e18) return TURBO_ERR_UNSUPPORTED;
+    DeviceInfo d;
+    if (device_info(&d) != cudaSuccess) return TURBO_ERR_CUDA;
+    cudaError_t e = launch_batched(windows, shape->num_windows, profiles, batch_cost, batch_cap, class_id, best_gain,
+                                   best_cost, feasible, exit_out, status, (int32_t)K, d.num_sms, (cudaStream_t)stream);
+    return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
+}
+
 turbo_status_t turbo_bucketize(const float *theta, int64_t num_frames, int32_t num_classes, float bucket_width,
                                uint8_t *class_out, turbo_stream_t stream)
 {

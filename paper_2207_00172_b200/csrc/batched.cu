@@ -1,0 +1,304 @@
+// batched.cu -- NEXT-4: the exact plan under the paper's true, batched latency constraint.
+//
+// PAPER.md:523-525 (§5.2): maximise sum_x P_{kappa_x}^{theta'_x} s.t. f(sum I_kappa) <= T, with f
+// batching the frames that run at the same level (a non-linear GAP). Latency does
+// not depend on frame content, so a plan's cost depends only on its counts
+// n_k = #{x : kappa_x = k}:  cost(n) = sum_k I_k(n_k)  (batch latency table, turbo.h).
+// Readings: R19 -- gains have increasing differences in the class (PAPER.md:535-536,
+// "the hardest frames have the largest marginals"), under which the assortative assignment
+// (frames sorted by (class, arrival) fill level 0, then 1, ...) is an optimal transportation plan
+// for its counts; so the optimum is a maximum over count vectors. R18 -- order: larger gain, then
+// smaller cost, then the count vector read from the top level down lexicographically smaller,
+// then that canonical assignment.
+//
+// B200 mapping: one CTA (256 threads) per window. The class histogram, the canonical positions
+// and the per-level prefix gains P_k(j) (gain of the first j canonical frames at level k) are
+// built in shared memory; then the C(N+K-1, K-1) count vectors are enumerated: each thread
+// unranks prefixes (n_0 .. n_{K-3}) with a binomial table and sweeps the last two levels
+// inline (cost and gain of a vector = 2K shared-memory reads, no global traffic); a 3-key
+// (gain, cost, counts code) argmax reduces over the warp with shuffles and over the CTA in
+// shared memory. Compute-bound on integer ALU + shared loads; tiny inputs, no HBM stream.
+#include "turbo_internal.cuh"
+
+namespace turbo {
+
+constexpr int BT_THREADS = 256;
+constexpr int BT_MAX_N = 255;
+constexpr int BT_MAX_K = 16;
+
+struct BtParams {
+    const turbo_window_t *windows;
+    int32_t num_windows;
+    const turbo_profile_t *profiles;
+    const int32_t *batch;        // [profile][16][cap + 1]
+    int32_t cap;
+    const uint8_t *class_id;
+    int32_t *best_gain;
+    int32_t *best_cost;
+    uint8_t *feasible;
+    uint8_t *exit_out;
+    int64_t *status;
+};
+
+// candidate order: larger gain, then smaller cost, then smaller counts code (R18)
+__device__ __forceinline__ bool bt_better(int32_t g, int32_t c, uint64_t code, int32_t g2, int32_t c2,
+                                          uint64_t code2)
+{
+    return g > g2 || (g == g2 && (c < c2 || (c == c2 && code < code2)));
+}
+
+// dynamic shared memory (kmax = the batch's largest K, cap = batch_cap):
+//   pref  int32 [kmax][cap + 1]   P_k(j), gain of the first j canonical frames at level k
+//   tab   int32 [kmax][cap + 1]   I_k(n)
+//   binom u32   [cap + kmax + 1][kmax]  C(n, r), saturated at 2^31 (counts used stay < 2^26)
+//   pos_cls u8  [cap]             class at canonical position j
+__host__ __device__ inline size_t bt_smem_bytes(int32_t kmax, int32_t cap)
+{
+    return (size_t)2 * kmax * (cap + 1) * 4 + (size_t)(cap + kmax + 1) * kmax * 4 + (size_t)((cap + 15) & ~15);
+}
+
+__global__ void __launch_bounds__(BT_THREADS) batched_kernel(BtParams P, int32_t kmax)
+{
+    extern __shared__ int4 bt_dyn[];
+    const int32_t ST = P.cap + 1;                           // row stride of pref / tab
+    int32_t *pref_s = reinterpret_cast<int32_t *>(bt_dyn);
+    int32_t *tab_s = pref_s + kmax * ST;
+    uint32_t *binom_s = reinterpret_cast<uint32_t *>(tab_s + kmax * ST);
+    uint8_t *pos_cls = reinterpret_cast<uint8_t *>(binom_s + (P.cap + kmax + 1) * kmax);
+#define pref(k, j) pref_s[(k) * ST + (j)]
+#define tab(k, n) tab_s[(k) * ST + (n)]
+#define binom(n, r) binom_s[(n) * kmax + (r)]
+    __shared__ int32_t hist[257];
+    __shared__ int32_t red_g[BT_THREADS / 32], red_c[BT_THREADS / 32];
+    __shared__ uint64_t red_k[BT_THREADS / 32];
+    __shared__ int32_t flag;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+    for (int64_t w = blockIdx.x; w < P.num_windows; w += gridDim.x) {
+        const turbo_window_t win = P.windows[w];
+        const int32_t N = win.num_frames, B = win.budget;
+        const turbo_profile_t pr = P.profiles[win.profile];
+        const int32_t C = pr.num_classes, K = pr.num_exits;
+        const uint8_t *cls = P.class_id + win.first_frame;
+        const int32_t *gt = pr.gain;
+        // ---- validation: class ids (status[0]), R19 and the budget (status[1])
+        if (tid == 0) flag = 0;
+        for (int x = tid; x < 257; x += BT_THREADS) hist[x] = 0;
+        __syncthreads();
+        for (int32_t x = tid; x < N; x += BT_THREADS) {
+            const int32_t c = cls[x];
+            if (c >= C) {
+                atomic_min_i64(&P.status[0], win.first_frame + x);
+                atomicOr(&flag, 1);
+            } else {
+                atomicAdd(&hist[c], 1);
+            }
+        }
+        for (int32_t e = tid; e < (C - 1) * (K - 1); e += BT_THREADS) {
+            const int32_t c = e / (K - 1), k = e - (e / (K - 1)) * (K - 1);
+            const int64_t d1 = (int64_t)__ldg(gt + (c + 1) * K + k + 1) - __ldg(gt + (c + 1) * K + k);
+            const int64_t d0 = (int64_t)__ldg(gt + c * K + k + 1) - __ldg(gt + c * K + k);
+            if (d1 < d0) atomicOr(&flag, 2);
+        }
+        for (int32_t e = tid; e < C * K; e += BT_THREADS) {
+            const int32_t v = __ldg(gt + e);
+            if (v > (1 << 24) || v < -(1 << 24)) atomicOr(&flag, 2);
+        }
+        if (tid == 0 && (B < 0 || N > P.cap || N > BT_MAX_N)) atomicOr(&flag, 2);
+        __syncthreads();
+        if (flag) {
+            if (tid == 0) {
+                P.best_gain[w] = 0;
+                P.best_cost[w] = 0;
+                P.feasible[w] = 0;
+                if (flag & 2) atomic_min_i64(&P.status[1], w);
+            }
+            for (int32_t x = tid; x < N; x += BT_THREADS) P.exit_out[win.first_frame + x] = 0;
+            __syncthreads();
+            continue;
+        }
+        // ---- canonical positions: class start offsets (exclusive prefix of the histogram)
+        if (tid == 0) {
+            int32_t s = 0;
+            for (int32_t c = 0; c < C; ++c) {
+                const int32_t m = hist[c];
+                hist[c] = s;
+                s += m;
+            }
+            hist[C] = s;
+        }
+        __syncthreads();
+        for (int32_t j = tid; j < N; j += BT_THREADS) {             // class of position j
+            int32_t c = 0;
+            while (c + 1 < C && hist[c + 1] <= j) ++c;
+            pos_cls[j] = (uint8_t)c;
+        }
+        // batch table rows and binomials C(n, r) (n <= N + K, r < K)
+        const int32_t *bt = P.batch + (int64_t)win.profile * BT_MAX_K * (P.cap + 1);
+        for (int32_t e = tid; e < K * (N + 1); e += BT_THREADS) {
+            const int32_t k = e / (N + 1), n = e - (e / (N + 1)) * (N + 1);
+            tab(k, n) = __ldg(bt + k * (P.cap + 1) + n);
+        }
+        for (int32_t n = tid; n <= N + K; n += BT_THREADS) {
+            uint64_t v = 1;                                          // C(n, 0), exact while < 2^31
+            for (int32_t r = 0; r < K; ++r) {
+                binom(n, r) = r > n ? 0u : (uint32_t)(v < 0x80000000ull ? v : 0x80000000ull);
+                if (v < 0x80000000ull) v = v * (uint64_t)(n - r) / (uint64_t)(r + 1);
+            }
+        }
+        __syncthreads();
+        // per-level prefix gains over the canonical order (thread k: level k, serial in j)
+        for (int32_t k = tid; k < K; k += BT_THREADS) {
+            int32_t s = 0;
+            pref(k, 0) = 0;
+            for (int32_t j = 0; j < N; ++j) {
+                s += __ldg(gt + (int32_t)pos_cls[j] * K + k);
+                pref(k, j + 1) = s;
+            }
+        }
+        __syncthreads();
+
+        // ---- enumerate the count vectors: prefixes (n_0 .. n_{K-3}), last two levels inline
+        const int32_t KP = K - 2;                                    // prefix parts
+        // #prefixes = sum over left of compositions of (N - left) into KP parts = C(N + KP, KP)
+        const uint64_t n_pref = binom(N + KP, KP);
+        int32_t bg = INT32_MIN, bc = INT32_MAX;
+        uint64_t bk = ~0ull;
+        for (uint64_t r0 = tid; r0 < n_pref; r0 += BT_THREADS) {
+            // unrank r0 into (n_0 .. n_{KP-1}) with sum <= N (lexicographic, weak compositions of
+            // N into KP + 1 parts where the last part -- the two inline levels -- takes the rest)
+            uint64_t r = r0;
+            int32_t left = N, S = 0, cost = 0, gain = 0;
+            uint64_t code = 0, mul = 1;
+            for (int32_t i = 0; i < KP; ++i) {
+                int32_t v = 0;
+                for (;; ++v) {
+                    // compositions of (left - v) into the remaining KP - i parts (incl. the tail)
+                    const uint64_t cnt = binom(left - v + KP - i - 1, KP - i - 1);
+                    if (r < cnt) break;
+                    r -= cnt;
+                }
+                cost += tab(i, v);
+                gain += pref(i, S + v) - pref(i, S);
+                if (i > 0) {                                         // n_0 is implied (sum = N)
+                    code += (uint64_t)v * mul;
+                    mul *= (uint64_t)(N + 1);
+                }
+                S += v;
+                left -= v;
+            }
+            // last two levels: n_{K-2} = v, n_{K-1} = left - v. Code weights: n_k counts
+            // (N+1)^(k-1) for k >= 1 (n_0 is implied), so level K-2 weighs `mul` (0 when K = 2)
+            const int32_t a = K - 2, b = K - 1;
+            const uint64_t wa = a == 0 ? 0 : mul;
+            const uint64_t wb = a == 0 ? 1 : mul * (uint64_t)(N + 1);
+            for (int32_t v = 0; v <= left; ++v) {
+                const int32_t u = left - v;
+                const int32_t c2 = cost + tab(a, v) + tab(b, u);
+                if (c2 > B) continue;
+                const int32_t g2 = gain + (pref(a, S + v) - pref(a, S)) + (pref(b, N) - pref(b, S + v));
+                const uint64_t code2 = code + (uint64_t)v * wa + (uint64_t)u * wb;
+                if (bt_better(g2, c2, code2, bg, bc, bk)) {
+                    bg = g2;
+                    bc = c2;
+                    bk = code2;
+                }
+            }
+        }
+        // ---- argmax over the CTA
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int32_t g2 = __shfl_xor_sync(0xffffffffu, bg, o);
+            const int32_t c2 = __shfl_xor_sync(0xffffffffu, bc, o);
+            const uint64_t k2 = __shfl_xor_sync(0xffffffffu, bk, o);
+            if (bt_better(g2, c2, k2, bg, bc, bk)) {
+                bg = g2;
+                bc = c2;
+                bk = k2;
+            }
+        }
+        if (lane == 0) {
+            red_g[warp] = bg;
+            red_c[warp] = bc;
+            red_k[warp] = bk;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int x = 1; x < BT_THREADS / 32; ++x)
+                if (bt_better(red_g[x], red_c[x], red_k[x], bg, bc, bk)) {
+                    bg = red_g[x];
+                    bc = red_c[x];
+                    bk = red_k[x];
+                }
+            const bool feas = bk != ~0ull;
+            const int32_t g0 = pref(0, N);
+            P.best_gain[w] = feas ? bg : g0;
+            P.best_cost[w] = feas ? bc : tab(0, N);
+            P.feasible[w] = feas ? 1 : 0;
+            // decode the counts into block boundaries S_k (reuse hist[0..K])
+            int32_t rest = N, S = 0;
+            uint64_t code = feas ? bk : 0;
+            int32_t cnt[BT_MAX_K];
+            for (int32_t k = 1; k < K; ++k) {
+                cnt[k] = (int32_t)(code % (uint64_t)(N + 1));
+                code /= (uint64_t)(N + 1);
+                rest -= cnt[k];
+            }
+            cnt[0] = rest;
+            for (int32_t k = 0; k < K; ++k) {                        // level blocks [S_k, S_k+1)
+                hist[k] = S;
+                S += cnt[k];
+            }
+            hist[K] = S;
+        }
+        __syncthreads();
+        // ---- exits: frame x's canonical position -> its level block
+        for (int32_t x = tid; x < N; x += BT_THREADS) {
+            const int32_t c = cls[x];
+            int32_t before = 0;                                      // same-class frames before x
+            for (int32_t y = 0; y < x; ++y) before += (cls[y] == c) ? 1 : 0;
+            int32_t start = 0;                                       // frames of smaller classes
+            for (int32_t j = 0; j < N && pos_cls[j] < c; ++j) ++start;
+            const int32_t posx = start + before;
+            int32_t k = 0;
+            while (k + 1 < K && hist[k + 1] <= posx) ++k;
+            P.exit_out[win.first_frame + x] = (uint8_t)k;
+        }
+        __syncthreads();
+    }
+#undef pref
+#undef tab
+#undef binom
+}
+
+cudaError_t launch_batched(const turbo_window_t *windows, int32_t num_windows, const turbo_profile_t *profiles,
+                           const int32_t *batch, int32_t cap, const uint8_t *class_id, int32_t *best_gain,
+                           int32_t *best_cost, uint8_t *feasible, uint8_t *exit_out, int64_t *status, int32_t kmax,
+                           int num_sms, cudaStream_t stream)
+{
+    if (num_windows <= 0) return cudaSuccess;
+    const size_t smem = bt_smem_bytes(kmax, cap);
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    BtParams P;
+    P.windows = windows;
+    P.num_windows = num_windows;
+    P.profiles = profiles;
+    P.batch = batch;
+    P.cap = cap;
+    P.class_id = class_id;
+    P.best_gain = best_gain;
+    P.best_cost = best_cost;
+    P.feasible = feasible;
+    P.exit_out = exit_out;
+    P.status = status;
+    int64_t blocks = num_windows;
+    if (blocks > (int64_t)num_sms * 64) blocks = (int64_t)num_sms * 64;
+    note_launch();
+    batched_kernel<<<(unsigned)blocks, BT_THREADS, smem, stream>>>(P, kmax);
+    return cudaGetLastError();
+}
+
+}  // namespace turbo

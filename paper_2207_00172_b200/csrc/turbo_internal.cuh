@@ -120,6 +120,10 @@ __host__ __device__ inline bool dp_kernel_fixed_k(int kmin, int kmax)
     return kmin == kmax && (kmin == 4 || kmin == 5 || kmin == 6 || kmin == 8);
 }
 
+cudaError_t launch_batched(const turbo_window_t *windows, int32_t num_windows, const turbo_profile_t *profiles,
+                           const int32_t *batch, int32_t cap, const uint8_t *class_id, int32_t *best_gain,
+                           int32_t *best_cost, uint8_t *feasible, uint8_t *exit_out, int64_t *status, int32_t kmax,
+                           int num_sms, cudaStream_t stream);
 // every kernel launch of the library is counted (turbo_launch_count)
 void note_launch();
 

@@ -64,7 +64,7 @@ assert WINDOW_DTYPE.itemsize == 48
 
 EXPORTS = ["turbo_mckp_workspace", "turbo_profile_lookup", "turbo_mckp_plan", "turbo_backtrack",
            "turbo_mckp_solve", "turbo_mckp_solve_workspace", "turbo_schedule", "turbo_heuristic_plan", "turbo_stats",
-           "turbo_bucketize", "turbo_batches",
+           "turbo_bucketize", "turbo_batches", "turbo_batched_plan",
            "turbo_debug_set_variant", "turbo_debug_trace", "turbo_launch_count",
            "turbo_status_string", "turbo_abi_version"]
 
@@ -92,6 +92,7 @@ def load(path: Optional[str] = None):
     lib.turbo_heuristic_plan.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.turbo_bucketize.argtypes = [vp, i64, i32, ctypes.c_float, vp, vp]
     lib.turbo_batches.argtypes = [vp, vp, vp, vp, vp, vp]
+    lib.turbo_batched_plan.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp]
     lib.turbo_debug_set_variant.argtypes = [i32]
     lib.turbo_debug_trace.argtypes = [vp, i64]
     lib.turbo_launch_count.argtypes = []
@@ -191,6 +192,25 @@ def heuristic_plan(shape, windows_dev, opt_gain, opt_cost, gain_out, cost_out, f
            load().turbo_heuristic_plan(ctypes.addressof(shape), _ptr(windows_dev), _ptr(opt_gain), _ptr(opt_cost),
                                        _ptr(gain_out), _ptr(cost_out), _ptr(feasible), _ptr(exit_out), _ptr(steps),
                                        _stream(stream)))
+
+
+def batched_plan(shape, windows_dev, profiles_dev, batch_cost, batch_cap, class_id, best_gain, best_cost, feasible,
+                 exit_out, status, stream=None):
+    """NEXT-4: exact plans under the batched latency tables (turbo.h turbo_batched_plan)."""
+    _check("turbo_batched_plan",
+           load().turbo_batched_plan(ctypes.addressof(shape), _ptr(windows_dev), _ptr(profiles_dev), _ptr(batch_cost),
+                                     int(batch_cap), _ptr(class_id), _ptr(best_gain), _ptr(best_cost), _ptr(feasible),
+                                     _ptr(exit_out), _ptr(status), _stream(stream)))
+
+
+def batch_cost_table(profiles_batch, profiles_shape, cap: int, device="cuda"):
+    """Device layout of the batch latency tables: profile p at p * 16 * (cap + 1), row k = I_k(0..cap)."""
+    import torch
+    P = len(profiles_batch)
+    t = np.zeros((max(P, 1), 16, cap + 1), dtype=np.int32)
+    for p, (tab, (C, K)) in enumerate(zip(profiles_batch, profiles_shape)):
+        t[p, :K] = np.asarray(tab, dtype=np.int32).reshape(K, cap + 1)
+    return torch.as_tensor(t.reshape(-1), device=device)
 
 
 def bucketize(theta, class_out, num_classes: int = 10, bucket_width: float = 0.1, stream=None):
