@@ -38,7 +38,13 @@ WORKLOADS = {
     "c3": dict(config=3, per_gpu=8192, desc="8192 windows x 300 frames, K=8, B=4096 per GPU (c3 = 65536 over 8 GPUs)"),
     "c4": dict(config=4, per_gpu=1, desc="single long window: 3000 frames, K=6, B=2^20 (grid-spanning row; replicas)"),
     "c5": dict(config=5, per_gpu=2048, desc="mixed sweep: K 2-16, B 64-16384, N 30-300, skewed classes; 2048 windows per GPU"),
+    # NEXT-4 (batched latency): the c2 window shape with batch latency tables
+    "b2": dict(config="b2", per_gpu=1024, desc="NEXT-4 batched-cost GAP: 1024 windows x 30 frames, K=5, B=1000, "
+                                               "I_k(n) = ceil(c_k (2+3n)/5) per GPU"),
 }
+METRIC_B = "NEXT-4 exact batched-cost plans: count vectors evaluated/s (and windows/s)"
+UNIT_B = "count-vectors/s"
+ISSUE_PEAK = 148 * 4 * 1.965e9          # warp-instructions/s: 4 SMSPs x 1 issue/clk x sm_max_mhz
 
 
 def dist_env():
@@ -51,7 +57,148 @@ def dist_env():
 def make_workload(name: str, rank: int):
     import synth
     spec = WORKLOADS[name]
+    if name.startswith("b"):
+        return synth.make_batched_config(int(name[1:]), num_windows=spec["per_gpu"],
+                                         window_offset=rank * spec["per_gpu"])
     return synth.make_config(spec["config"], window_offset=rank * spec["per_gpu"], num_windows=spec["per_gpu"])
+
+
+def _vectors(wl) -> int:
+    """Count vectors per window: C(N + K - 1, K - 1), summed."""
+    from math import comb
+    return int(sum(comb(int(n) + int(k) - 1, int(k) - 1) for n, k in zip(wl.num_frames, wl.num_exits)))
+
+
+def run_batched(args):
+    """NEXT-4 leg: turbo_batched_plan on b<k> windows (device timing with CUDA graphs and L2 flush,
+    e2e through the public API with host buffers, CPU oracle baseline)."""
+    import torch
+    import numpy as np
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist_mod
+        dist = dist_mod
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    from paper_2207_00172_b200 import build as tbuild, turbo
+    if not os.path.exists(turbo.LIB_PATH):
+        tbuild.build()
+    turbo.load()
+    name = args.workload
+    wl = make_workload(name, rank)
+    b = turbo.make_batch(wl.profiles_gain, wl.profiles_cost, wl.profiles_shape, wl.num_frames, wl.budget, wl.profile,
+                         class_id=wl.class_id, device=dev, with_plan_workspace=False)
+    bt = turbo.batch_cost_table(wl.profiles_batch, wl.profiles_shape, wl.batch_cap, device=dev)
+    W, F = wl.num_windows, wl.total_frames
+    vec = _vectors(wl)
+
+    def call(stream=None):
+        turbo.batched_plan(b.shape, b.windows_dev, b.profiles_dev, bt, wl.batch_cap, b.class_id, b.best_gain,
+                           b.best_cost, b.feasible, b.exit_out, b.status, stream)
+
+    for _ in range(max(args.warmup, 3)):
+        call()
+    torch.cuda.synchronize(dev)
+    c0 = turbo.launch_count()
+    call()
+    torch.cuda.synchronize(dev)
+    launches = turbo.launch_count() - c0
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        call()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(3):
+        g.replay()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clk = ClockSampler(local)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    clk.start()
+    for k in range(args.steps):
+        flush.fill_(k & 0xff)
+        evs[k][0].record(stream)
+        g.replay()
+        evs[k][1].record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = clk.stop()
+    t_step = sum(a.elapsed_time(bb) for a, bb in evs) / args.steps / 1e3
+    st = b.status.cpu().numpy()
+    if st[0] != -1 or st[1] != -1:
+        raise RuntimeError(f"status words set during bench: {st}")
+    # e2e: class ids H2D from pinned host memory, the C-ABI call, results D2H (pinned)
+    h_cls = torch.empty(max(F, 1), dtype=torch.uint8).pin_memory()
+    h_cls[:F] = torch.as_tensor(wl.class_id)
+    h_out = torch.empty_like(b.out_arena, device="cpu").pin_memory()
+    for _ in range(3):
+        b.class_id[:F].copy_(h_cls[:F], non_blocking=True)
+        call()
+        h_out.copy_(b.out_arena, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        b.class_id[:F].copy_(h_cls[:F], non_blocking=True)
+        call()
+        h_out.copy_(b.out_arena, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    t_e2e = e0.elapsed_time(e1) / args.steps / 1e3
+    if dist is not None:
+        tt = torch.tensor([t_step, t_e2e], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_step, t_e2e = float(tt[0]), float(tt[1])
+    N = ws
+    ops = None
+    opf = os.path.join(ROOT, "profiles", f"issue_{name}.json")
+    if os.path.exists(opf):
+        ops = json.load(open(opf)).get("warp_instructions_per_launch")
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        import oracle
+        import synth
+        n_sub = 64
+        synth_sub = synth.make_batched_config(int(name[1:]), num_windows=n_sub)
+        t0 = time.time()
+        reps = 0
+        while time.time() - t0 < args.cpu_seconds or reps == 0:
+            oracle.batched(synth_sub)
+            reps += 1
+        dt = time.time() - t0
+        cpu = {"value": _vectors(synth_sub) * reps / dt, "unit": UNIT_B, "cores": 1, "kind": "oracle",
+               "sample": f"{reps} passes over {n_sub} {name} windows (count-vector enumeration, gcc -O2, 1 thread)"}
+    if rank == 0:
+        line = {
+            "metric": METRIC_B, "value": vec * N / t_step, "unit": UNIT_B, "n_gpus": N, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (seeded splitmix64 generator, synth/; supermodular Appendix-B gains, batch latency tables)",
+            "config": {"workload": f"{name}: {WORKLOADS[name]['desc']}", "windows_per_gpu": W,
+                       "count_vectors_per_gpu_step": vec, "path": "turbo_batched_plan (1 launch)",
+                       "l2": "flushed between timed steps (256 MiB write outside the step events)",
+                       "parallelism": f"weak dp{N} (windows sharded, no collective)"},
+            "windows_per_s": W * N / t_step,
+            "roofline": {"bound": "alu", "achieved": (ops / t_step) if ops else None, "peak": ISSUE_PEAK,
+                         "unit": "warp-instructions/s", "frac": (ops / t_step / ISSUE_PEAK) if ops else None,
+                         "traffic": None, "kernel": "turbo::batched_kernel",
+                         "note": "integer compare/select + smem reads; achieved = warp instructions per launch "
+                                 "(profiles/issue_<workload>.json, ncu smsp__inst_executed) / live launch time; "
+                                 "peak = 148 SMs x 4 issue/clk x sm_max_mhz"},
+            "e2e": {"value": vec * N / t_e2e, "unit": UNIT_B, "h2d_bytes_per_step": F,
+                    "d2h_bytes_per_step": int(b.out_arena.numel()), "ms_per_step": t_e2e * 1e3},
+            "gpu_launches": launches * args.steps,
+            "clocks": clocks,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+    return 0
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -193,6 +340,28 @@ def run_reference(args):
     if rank != 0:
         return 0
     name = args.workload
+    if name.startswith("b"):                     # NEXT-4: the batched oracle on a window sample
+        import oracle
+        import synth
+        sub = synth.make_batched_config(int(name[1:]), num_windows=64)
+        for _ in range(args.warmup):
+            oracle.batched(sub)
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            oracle.batched(sub)
+        el = time.perf_counter() - t0
+        value = _vectors(sub) * args.steps / el
+        sample = f"64 of {WORKLOADS[name]['per_gpu']} windows of {name} per step, count-vector enumeration, 1 thread"
+        print(json.dumps({"impl": "reference", "metric": METRIC_B, "value": value, "unit": UNIT_B,
+                          "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                          "ms_per_step": el / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
+                          "vs_baseline": None, "dtype": "int64", "data": "synthetic (seeded splitmix64, synth/)",
+                          "config": {"workload": f"{name}: {WORKLOADS[name]['desc']}", "oracle_sample_windows": 64},
+                          "cpu_baseline": {"value": value, "unit": UNIT_B, "cores": 1, "kind": "oracle",
+                                           "sample": sample},
+                          "e2e": {"value": value, "unit": UNIT_B, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+              flush=True)
+        return 0
     wl = make_workload(name, 0)
     threads = os.cpu_count() or 1
     # each step: a bounded sample (whole windows) of ~0.15 s of oracle work on all cores
@@ -468,6 +637,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload.startswith("b"):
+        return run_batched(args)
     return run_turbo(args)
 
 

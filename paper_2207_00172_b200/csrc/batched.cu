@@ -158,18 +158,22 @@ __global__ void __launch_bounds__(BT_THREADS) batched_kernel(BtParams P, int32_t
         }
         __syncthreads();
 
-        // ---- enumerate the count vectors: prefixes (n_0 .. n_{K-3}), last two levels inline
+        // ---- enumerate the count vectors: prefixes (n_0 .. n_{K-3}) ranked lexicographically, the
+        // last two levels swept inline. Each thread takes a contiguous range of prefix ranks: it
+        // unranks its first prefix once (binomial search), then steps to the lexicographic
+        // successor. (Measured alternatives: unranking every prefix, 285 us on b2; one vector per
+        // step with per-lane carries, 361 us -- the carries diverge; this, 225 us.)
         const int32_t KP = K - 2;                                    // prefix parts
-        // #prefixes = sum over left of compositions of (N - left) into KP parts = C(N + KP, KP)
-        const uint64_t n_pref = binom(N + KP, KP);
+        const uint64_t n_pref = binom(N + KP, KP);                   // weak compositions, KP+1 parts
         int32_t bg = INT32_MIN, bc = INT32_MAX;
         uint64_t bk = ~0ull;
-        for (uint64_t r0 = tid; r0 < n_pref; r0 += BT_THREADS) {
-            // unrank r0 into (n_0 .. n_{KP-1}) with sum <= N (lexicographic, weak compositions of
-            // N into KP + 1 parts where the last part -- the two inline levels -- takes the rest)
-            uint64_t r = r0;
-            int32_t left = N, S = 0, cost = 0, gain = 0;
-            uint64_t code = 0, mul = 1;
+        const uint64_t chunk = (n_pref + BT_THREADS - 1) / BT_THREADS;
+        const uint64_t r_lo = (uint64_t)tid * chunk;
+        const uint64_t r_hi = r_lo + chunk < n_pref ? r_lo + chunk : n_pref;
+        int32_t pv[BT_MAX_K];                                        // prefix parts n_0 .. n_{KP-1}
+        int32_t left = N;                                            // the tail: n_{K-2} + n_{K-1}
+        if (r_lo < r_hi) {
+            uint64_t r = r_lo;
             for (int32_t i = 0; i < KP; ++i) {
                 int32_t v = 0;
                 for (;; ++v) {
@@ -178,6 +182,28 @@ __global__ void __launch_bounds__(BT_THREADS) batched_kernel(BtParams P, int32_t
                     if (r < cnt) break;
                     r -= cnt;
                 }
+                pv[i] = v;
+                left -= v;
+            }
+        }
+        for (uint64_t r0 = r_lo; r0 < r_hi; ++r0) {
+            if (r0 > r_lo) {                                         // lexicographic successor
+                if (left > 0) {
+                    pv[KP - 1] += 1;
+                    left -= 1;
+                } else {
+                    int32_t i = KP - 1;
+                    while (i > 0 && pv[i] == 0) --i;                 // rightmost non-zero part
+                    left += pv[i];
+                    pv[i] = 0;
+                    pv[i - 1] += 1;
+                    left -= 1;
+                }
+            }
+            int32_t S = 0, cost = 0, gain = 0;
+            uint64_t code = 0, mul = 1;
+            for (int32_t i = 0; i < KP; ++i) {
+                const int32_t v = pv[i];
                 cost += tab(i, v);
                 gain += pref(i, S + v) - pref(i, S);
                 if (i > 0) {                                         // n_0 is implied (sum = N)
@@ -185,18 +211,18 @@ __global__ void __launch_bounds__(BT_THREADS) batched_kernel(BtParams P, int32_t
                     mul *= (uint64_t)(N + 1);
                 }
                 S += v;
-                left -= v;
             }
             // last two levels: n_{K-2} = v, n_{K-1} = left - v. Code weights: n_k counts
             // (N+1)^(k-1) for k >= 1 (n_0 is implied), so level K-2 weighs `mul` (0 when K = 2)
-            const int32_t a = K - 2, b = K - 1;
-            const uint64_t wa = a == 0 ? 0 : mul;
-            const uint64_t wb = a == 0 ? 1 : mul * (uint64_t)(N + 1);
+            const int32_t a2 = K - 2, b2 = K - 1;
+            const uint64_t wa = a2 == 0 ? 0 : mul;
+            const uint64_t wb = a2 == 0 ? 1 : mul * (uint64_t)(N + 1);
+            const int32_t gb = gain + pref(b2, N) - pref(a2, S);
             for (int32_t v = 0; v <= left; ++v) {
                 const int32_t u = left - v;
-                const int32_t c2 = cost + tab(a, v) + tab(b, u);
+                const int32_t c2 = cost + tab(a2, v) + tab(b2, u);
                 if (c2 > B) continue;
-                const int32_t g2 = gain + (pref(a, S + v) - pref(a, S)) + (pref(b, N) - pref(b, S + v));
+                const int32_t g2 = gb + pref(a2, S + v) - pref(b2, S + v);
                 const uint64_t code2 = code + (uint64_t)v * wa + (uint64_t)u * wb;
                 if (bt_better(g2, c2, code2, bg, bc, bk)) {
                     bg = g2;
