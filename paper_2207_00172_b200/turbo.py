@@ -49,7 +49,7 @@ class Shape(ctypes.Structure):
                 ("total_frames", ctypes.c_int64), ("total_options", ctypes.c_int64),
                 ("total_cells", ctypes.c_int64), ("workspace_bytes", ctypes.c_int64),
                 ("max_budget_small", ctypes.c_int32), ("num_big", ctypes.c_int32),
-                ("grid_scratch_offset", ctypes.c_int64), ("ordered", ctypes.c_int32), ("reserved2", ctypes.c_int32),
+                ("grid_scratch_offset", ctypes.c_int64), ("ordered", ctypes.c_int32), ("cls_order", ctypes.c_int32),
                 ("reserved3", ctypes.c_int64),
                 ("cls_count", ctypes.c_int32 * 4), ("cls_max_budget", ctypes.c_int32 * 4),
                 ("cls_max_frames", ctypes.c_int32 * 4), ("cls_max_options", ctypes.c_int32 * 4),
