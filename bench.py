@@ -437,10 +437,10 @@ def run_turbo(args):
             turbo.mckp_plan(b.shape, b.windows_dev, b.opt_gain, b.opt_cost, b.workspace, b.best_gain,
                             b.best_cost, b.feasible, b.status)
 
-    def step():
+    def step(reset: bool = True):
         stream = torch.cuda.current_stream(dev)
-        b.status.fill_(-1)
-        b.stats.zero_()
+        if reset:                    # stats = 0, status = -1: one device-to-device copy
+            turbo.reset_outputs(b)
         if path == "schedule":
             dominant()
             return
@@ -524,6 +524,7 @@ def run_turbo(args):
     # ---- e2e through the C ABI with HOST buffers (pinned), H2D inputs + D2H results inside
     F = int(b.shape.total_frames)
     # host buffers (pinned) mirroring the device input / output arenas: one copy each way
+    turbo.reset_outputs(b)           # the host input image carries the initial stats / status
     h_in = torch.empty_like(b.in_arena, device="cpu").pin_memory()
     h_in.copy_(b.in_arena)
     h_out = torch.empty_like(b.out_arena, device="cpu").pin_memory()
@@ -532,8 +533,8 @@ def run_turbo(args):
 
     def e2e_step():
         # the public API, called eagerly (no graph): H2D inputs, the C-ABI calls, D2H results
-        b.in_arena.copy_(h_in, non_blocking=True)
-        step()
+        b.in_arena.copy_(h_in, non_blocking=True)     # inputs + initial stats/status
+        step(reset=False)
         if dist is not None:
             dist.all_reduce(b.stats)
         h_out.copy_(b.out_arena, non_blocking=True)

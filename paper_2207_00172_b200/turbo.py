@@ -274,8 +274,22 @@ class Batch:
     status: object
     stats: object
     solve_ws: object
-    in_arena: object = None      # [capacity | class_id] (one H2D per step)
+    in_arena: object = None      # [capacity | class_id | stats | status] (one H2D per step)
     out_arena: object = None     # [stats | status | best_gain | best_cost | feasible | exit_out] (one D2H)
+    reset: object = None         # device copy of the initial [stats = 0 | status = -1] (one D2D reset)
+
+
+def _reset_template(arena, offs):
+    """Initial [stats | status] bytes (zeros, then -1) on the device: one D2D copy resets both."""
+    t = arena[offs[2]: offs[4]].clone()
+    t.view(-1)[:] = 0
+    t[offs[3] - offs[2]:].view(-1).fill_(255)      # status int64 = -1
+    return t
+
+
+def reset_outputs(b, stream=None):
+    """stats = 0, status = -1 with one device-to-device copy (the step's only reset op)."""
+    b.in_arena[b.in_arena.numel() - b.reset.numel():].copy_(b.reset, non_blocking=True)
 
 
 def make_batch(profiles_gain: List[np.ndarray], profiles_cost: List[np.ndarray], profiles_shape: List[tuple],
@@ -310,30 +324,32 @@ def make_batch(profiles_gain: List[np.ndarray], profiles_cost: List[np.ndarray],
     profiles_dev = torch.as_tensor(pbytes.copy(), device=dev)
     windows_dev = torch.as_tensor(wins.view(np.uint8).copy(), device=dev)
     F = int(shape.total_frames)
-    # inputs in one device arena [capacity int32 W | class_id u8 F] and outputs in another
-    # [stats int64 181 | status int64 2 | best_gain int32 W | best_cost int32 W | feasible u8 W |
-    # exit_out u8 F]: one host<->device copy each way per step (sub-buffers 16-B aligned)
+    # One device arena, 16-B aligned sections:
+    #   [capacity int32 W | class_id u8 F | stats int64 181 | status int64 2 |
+    #    best_gain int32 W | best_cost int32 W | feasible u8 W | exit_out u8 F]
+    # in_arena = the first four sections (ONE host->device copy per step carries the inputs AND the
+    # initial stats (0) / status (-1)); out_arena = stats .. exit_out (ONE device->host copy).
     def _carve(arena, sizes):
-        views, off = [], 0
+        views, off, offs = [], 0, []
         for nbytes, dt in sizes:
             views.append(arena[off: off + nbytes].view(dt))
+            offs.append(off)
             off += (nbytes + 15) & ~15
-        return views
-    def _total(sizes):
-        return sum((n + 15) & ~15 for n, _ in sizes)
-    in_sizes = [(4 * max(W, 1), torch.int32), (max(F, 1), torch.uint8)]
-    in_arena = torch.zeros(_total(in_sizes), dtype=torch.uint8, device=dev)
-    cap_v, cls = _carve(in_arena, in_sizes)
+        return views, offs, off
+    sizes = [(4 * max(W, 1), torch.int32), (max(F, 1), torch.uint8), (8 * STATS_WORDS, torch.int64),
+             (8 * STATUS_WORDS, torch.int64), (4 * max(W, 1), torch.int32), (4 * max(W, 1), torch.int32),
+             (max(W, 1), torch.uint8), (max(F, 1), torch.uint8)]
+    total = sum((n + 15) & ~15 for n, _ in sizes)
+    arena = torch.zeros(total, dtype=torch.uint8, device=dev)
+    (cap_v, cls, st_v, status_v, bg_v, bc_v, fe_v, ex_v), offs, _ = _carve(arena, sizes)
+    in_arena = arena[: offs[4]]
+    out_arena = arena[offs[2]:]
     if class_id is not None and F:
         cls[:F] = torch.as_tensor(np.ascontiguousarray(class_id, dtype=np.uint8), device=dev)
     cap = None
     if capacity is not None:
         cap = cap_v
         cap[:W] = torch.as_tensor(np.ascontiguousarray(capacity, dtype=np.int32), device=dev)
-    out_sizes = [(8 * STATS_WORDS, torch.int64), (8 * STATUS_WORDS, torch.int64), (4 * max(W, 1), torch.int32),
-                 (4 * max(W, 1), torch.int32), (max(W, 1), torch.uint8), (max(F, 1), torch.uint8)]
-    out_arena = torch.zeros(_total(out_sizes), dtype=torch.uint8, device=dev)
-    st_v, status_v, bg_v, bc_v, fe_v, ex_v = _carve(out_arena, out_sizes)
     status_v.fill_(-1)
     nopt = max(int(shape.total_options), 4)
     ws_bytes = int(shape.workspace_bytes) if with_plan_workspace else 0
@@ -346,7 +362,7 @@ def make_batch(profiles_gain: List[np.ndarray], profiles_cost: List[np.ndarray],
                  workspace=torch.empty(max(ws_bytes, 16), dtype=torch.uint8, device=dev) if ws_bytes else None,
                  best_gain=bg_v, best_cost=bc_v, feasible=fe_v, exit_out=ex_v, status=status_v, stats=st_v,
                  solve_ws=torch.empty(solve_bytes, dtype=torch.uint8, device=dev) if solve_bytes else None,
-                 in_arena=in_arena, out_arena=out_arena)
+                 in_arena=in_arena, out_arena=out_arena, reset=_reset_template(arena, offs))
 
 
 def batch_from_workload(wl, device="cuda", with_plan_workspace: bool = True) -> Batch:
