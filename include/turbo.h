@@ -269,7 +269,8 @@ turbo_status_t turbo_stats(const turbo_shape_t *shape /* host */, const turbo_wi
  * smaller, then the canonical assignment -- frames sorted by (class, arrival index) fill level 0,
  * then 1, ... (readings R18, R19). Preconditions: the profile's gains have increasing
  * differences in the class, g[c+1][k+1] - g[c+1][k] >= g[c][k+1] - g[c][k] (R19)
- * and |g| <= 2^24; a window violating them (or with budget < 0) is planned all-zero, feasible = 0,
+ * and |g| <= 2^24, sum over the window's frames of |g| per level <= 2^30, batch latencies in [0, 2^26];
+ * a window violating them (or with budget < 0) is planned all-zero, feasible = 0,
  * gain = cost = 0, and status[1] = min such window; a class id >= C sets status[0] like the lookup.
  * batch_cost (device int32): per profile p a table at p * 16 * (batch_cap + 1), row k (k < K_p) =
  * I_k(0 .. batch_cap). Host checks (TURBO_ERR_UNSUPPORTED): max_frames <= batch_cap <= 255,

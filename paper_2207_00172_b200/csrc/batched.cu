@@ -69,6 +69,7 @@ __global__ void __launch_bounds__(BT_THREADS) batched_kernel(BtParams P, int32_t
 #define tab(k, n) tab_s[(k) * ST + (n)]
 #define binom(n, r) binom_s[(n) * kmax + (r)]
     __shared__ int32_t hist[257];
+    __shared__ int32_t qsh[BT_MAX_K][257];                  // Q_k(c): gain of all smaller classes
     __shared__ int32_t red_g[BT_THREADS / 32], red_c[BT_THREADS / 32];
     __shared__ uint64_t red_k[BT_THREADS / 32];
     __shared__ int32_t flag;
@@ -147,14 +148,43 @@ __global__ void __launch_bounds__(BT_THREADS) batched_kernel(BtParams P, int32_t
             }
         }
         __syncthreads();
-        // per-level prefix gains over the canonical order (thread k: level k, serial in j)
+        // per-level prefix gains over the canonical order, P_k(j) = Q_k(c) + (j - start_c) g[c][k]
+        // with c the class of position j-1 and Q_k(c) = sum_{c' < c} m_c' g[c'][k] (a short serial
+        // pass over the classes per level, then every (k, j) in parallel)
         for (int32_t k = tid; k < K; k += BT_THREADS) {
-            int32_t s = 0;
-            pref(k, 0) = 0;
-            for (int32_t j = 0; j < N; ++j) {
-                s += __ldg(gt + (int32_t)pos_cls[j] * K + k);
-                pref(k, j + 1) = s;
+            int64_t q = 0, qa = 0;
+            for (int32_t c = 0; c < C; ++c) {
+                qsh[k][c] = (int32_t)q;
+                const int64_t gv = __ldg(gt + c * K + k);
+                q += (int64_t)(hist[c + 1] - hist[c]) * gv;
+                qa += (int64_t)(hist[c + 1] - hist[c]) * (gv < 0 ? -gv : gv);
             }
+            if (qa > (1ll << 30)) atomicOr(&flag, 2);              // every partial sum fits int32
+        }
+        for (int32_t e = tid; e < K * (N + 1); e += BT_THREADS) {
+            const int32_t t = tab(e / (N + 1), e - (e / (N + 1)) * (N + 1));
+            if (t < 0 || t > (1 << 26)) atomicOr(&flag, 2);         // batch latencies (range)
+        }
+        __syncthreads();
+        if (flag) {                                                 // range violation: rejected
+            if (tid == 0) {
+                P.best_gain[w] = 0;
+                P.best_cost[w] = 0;
+                P.feasible[w] = 0;
+                atomic_min_i64(&P.status[1], w);
+            }
+            for (int32_t x = tid; x < N; x += BT_THREADS) P.exit_out[win.first_frame + x] = 0;
+            __syncthreads();
+            continue;
+        }
+        for (int32_t e = tid; e < K * (N + 1); e += BT_THREADS) {
+            const int32_t k = e / (N + 1), j = e - (e / (N + 1)) * (N + 1);
+            int32_t v = 0;
+            if (j > 0) {
+                const int32_t c = pos_cls[j - 1];
+                v = qsh[k][c] + (j - hist[c]) * __ldg(gt + c * K + k);
+            }
+            pref(k, j) = v;
         }
         __syncthreads();
 
