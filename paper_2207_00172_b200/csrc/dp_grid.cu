@@ -175,6 +175,119 @@ struct GridCtx {
     long long *trace;           // [GRID_MAX_CTAS][8] cycle counters (debug bit 2)
 };
 
+// a5 of the long window by the WHOLE CTA (512 threads, the rest of the GPU is idle): thread q is
+// a candidate prefix of up to D-1 choices (q = 0 the empty one, then the K one-frame prefixes,
+// ...), D the deepest level whose candidates fit the CTA; each thread reads the choices along its
+// own prefix (loads issued together), the realised deepest candidate -- exactly one thread --
+// posts its exits and cost to shared memory, one CTA barrier per round. D frames per HBM round
+// trip (K = 6: 4 instead of the warp walk's 2). Costs are loaded a round ahead.
+template <int K>
+struct CtaWalkGeom {
+    static constexpr int NT = 512;
+    static constexpr int count(int d) { return d == 0 ? 0 : count(d - 1) * K + 1; }   // sum_{j<d} K^j
+    static constexpr int pick(int d) { return (d < 8 && count(d + 1) <= NT) ? pick(d + 1) : d; }
+    static constexpr int D = pick(1);
+};
+
+template <int K, class CostF>
+__device__ __forceinline__ void backtrack_cta_spec(int32_t N, int32_t b, const uint32_t *__restrict__ gch,
+                                                   int32_t gtiles, CostF cost, uint8_t *__restrict__ exit_g,
+                                                   long long *slot /* smem, >= 4 words */)
+{
+    constexpr int CB = (K <= 4) ? 2 : 4;
+    constexpr int RPT = 32 / CB;
+    constexpr uint32_t CMASK = (1u << CB) - 1u;
+    constexpr int D = CtaWalkGeom<K>::D;
+    const int tid = threadIdx.x, lane = tid & 31;
+    int d = -1;
+    uint32_t dig = 0;
+    {
+        int q = tid, pw = 1;
+#pragma unroll
+        for (int dd = 0; dd < D; ++dd) {
+            if (d < 0) {
+                if (q < pw) {
+                    d = dd;
+                    int r = q;
+                    for (int j = dd - 1; j >= 0; --j) {
+                        dig |= (uint32_t)(r % K) << (4 * j);
+                        r /= K;
+                    }
+                } else {
+                    q -= pw;
+                }
+            }
+            pw *= K;
+        }
+    }
+    auto choice = [&](int32_t i, int32_t cell) -> int32_t {
+        const int32_t t = cell / (32 * RPT);
+        const int32_t jr = (cell >> 5) & (RPT - 1);
+        const uint32_t word = gch[((int64_t)i * gtiles + t) * 32 + (cell & 31)];
+        return (int32_t)((word >> choice_shift(jr, CB)) & CMASK);
+    };
+    auto load_costs = [&](int32_t i0, int32_t (&pcv)[D], int32_t (&lcv)[K]) {
+#pragma unroll
+        for (int j = 0; j < D - 1; ++j)
+            pcv[j] = (j < d && i0 + j < N) ? cost(i0 + j, (int)((dig >> (4 * j)) & 15u)) : 0;
+        pcv[D - 1] = 0;
+        const bool last = d >= 0 && i0 + d < N;
+#pragma unroll
+        for (int k = 0; k < K; ++k) lcv[k] = last ? cost(i0 + d, k) : 0;
+    };
+    int32_t pcA[D], lcA[K], pcB[D], lcB[K];
+    auto round = [&](int32_t i, int par, const int32_t (&pcv)[D], const int32_t (&lcv)[K], int32_t (&pcn)[D],
+                     int32_t (&lcn)[K]) -> bool {
+        const int32_t dm = min(D, N - i);
+        if (i + D < N) load_costs(i + D, pcn, lcn);
+        int32_t kv[D];
+        int32_t bj = b, bd = b;
+        bool neg = false;
+        const bool deep = d >= 0 && d == dm - 1;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            kv[j] = choice(min(i + j, N - 1), max(bj, 0));    // unconditional: all loads in flight
+            if (j <= d) neg |= bj < 0;
+            if (j == d) bd = bj;
+            if (j < D - 1 && j < d) bj -= pcv[j];
+        }
+        bool on = deep && !neg;
+        int32_t kd = 0;
+#pragma unroll
+        for (int j = 0; j < D; ++j) {
+            if (j < d) on = on && kv[j] == (int32_t)((dig >> (4 * j)) & 15u);
+            if (j == d) kd = kv[j];
+        }
+        int32_t lk = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) lk = (k == kd) ? lcv[k] : lk;
+        if (on) {                                            // exactly one thread of the CTA
+            slot[2 * par] = (long long)(dig | ((uint32_t)kd << (4 * (d < 0 ? 0 : d))));
+            slot[2 * par + 1] = (long long)((b - bd) + lk);
+        }
+        __syncthreads();
+        const uint32_t packed = (uint32_t)slot[2 * par];
+        const int32_t step = (int32_t)slot[2 * par + 1];
+        if (tid == 0) {
+#pragma unroll
+            for (int j = 0; j < D; ++j)
+                if (j < dm) exit_g[i + j] = (uint8_t)((packed >> (4 * j)) & 15u);
+        }
+        b -= step;
+        return i + D < N;
+    };
+    (void)lane;
+    load_costs(0, pcA, lcA);
+    int par = 0;
+    for (int32_t i = 0; i < N; i += 2 * D) {
+        if (!round(i, par, pcA, lcA, pcB, lcB)) break;
+        par ^= 1;
+        if (!round(i + D, par, pcB, lcB, pcA, lcA)) break;
+        par ^= 1;
+    }
+    __syncthreads();
+}
+
 template <int K, int MODE>
 __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, int32_t *bufA, int32_t *bufB,
                            long long *red, GridCtx X, int &step_base, unsigned long long *stage_in,
@@ -495,9 +608,9 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
     // ---- a5 (solve): CTA 0's warp 0 walks the HBM choice planes
     if (!feas) {
         for (int32_t i = j * nthr + tid; i < N; i += NP * nthr) P.exit_out[ff + i] = 0;
-    } else if (j == 0 && warp == 0) {
+    } else if (j == 0) {                               // CTA 0, all threads (the grid is idle)
         auto cost = [&](int32_t i, int32_t k) -> int32_t { return __ldg(oc + (int64_t)i * K + k); };
-        backtrack_warp_spec<K, DP_SOLVE_GLOBAL>(N, Cst, nullptr, gch, 0, gtiles, cost, P.exit_out + ff, nullptr, lane);
+        backtrack_cta_spec<K>(N, Cst, gch, gtiles, cost, P.exit_out + ff, red + 8);
     }
 }
 
