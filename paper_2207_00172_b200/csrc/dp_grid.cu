@@ -516,11 +516,15 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
                     if (trace && gtid == 0) X.trace[j * 8 + 4] += clock64() - cw;
                     ++uses;
                     // unpack and check the tags in one pass (a stale word just repeats the load)
+                    // (two tagged words per 16-byte load, two values per 8-byte store)
                     bool stale = false;
-                    for (int32_t x = gtid; x < hl8; x += gn) {
-                        const unsigned long long u = stage_in[x];
-                        stale |= (uint32_t)(u >> 32) != (uint32_t)(sb + f);
-                        cur[H - hl8 + x] = (int32_t)(uint32_t)u;
+                    const ulonglong2 *in2 = reinterpret_cast<const ulonglong2 *>(stage_in);
+                    int2 *out2 = reinterpret_cast<int2 *>(cur + H - hl8);
+                    for (int32_t x = gtid; x < hl8 / 2; x += gn) {
+                        const ulonglong2 u = in2[x];
+                        stale |= ((uint32_t)(u.x >> 32) != (uint32_t)(sb + f)) |
+                                 ((uint32_t)(u.y >> 32) != (uint32_t)(sb + f));
+                        out2[x] = make_int2((int32_t)(uint32_t)u.x, (int32_t)(uint32_t)u.y);
                     }
                     ok = !(group ? named_sync_or(1, gn, stale) : __syncthreads_or(stale));
                 }
