@@ -177,9 +177,9 @@ def stats(num_frames, class_id, exits, best_gain, best_cost, feasible) -> np.nda
     return out
 
 
-def run(wl, mode: str = "table", threads: Optional[int] = None) -> dict:
-    """The whole path a1..a6 on one workload."""
-    bud = budget(wl.capacity, wl.num_frames, wl.base_cost)
+def run(wl, mode: str = "table", threads: Optional[int] = None, budgets=None) -> dict:
+    """The whole path a1..a6 on one workload (budgets given: the capacity = NULL path, a1 skipped)."""
+    bud = budget(wl.capacity, wl.num_frames, wl.base_cost) if budgets is None else _i32(budgets)
     og, oc, fo, bad = lookup(wl)
     K = wl.num_exits
     exits, bg, bc, fe = plan(wl.num_frames, bud, K, og, oc, mode, threads)

@@ -365,10 +365,21 @@ def make_batch(profiles_gain: List[np.ndarray], profiles_cost: List[np.ndarray],
                  in_arena=in_arena, out_arena=out_arena, reset=_reset_template(arena, offs))
 
 
-def batch_from_workload(wl, device="cuda", with_plan_workspace: bool = True) -> Batch:
-    """Device batch for a synth.Workload (budgets derived on device by a1 from capacity)."""
+def batch_from_workload(wl, device="cuda", with_plan_workspace: bool = True, null_capacity: bool = False) -> Batch:
+    """Device batch for a synth.Workload (budgets derived on device by a1 from capacity; with
+    null_capacity the calls get capacity = NULL and plan the windows' own budget fields)."""
     return make_batch(wl.profiles_gain, wl.profiles_cost, wl.profiles_shape, wl.num_frames, wl.budget,
-                      wl.profile, wl.class_id, wl.capacity, wl.base_cost, device, with_plan_workspace)
+                      wl.profile, wl.class_id, None if null_capacity else wl.capacity, wl.base_cost, device,
+                      with_plan_workspace)
+
+
+def set_device_budgets(b: Batch, budgets: np.ndarray):
+    """Overwrite turbo_window_t.budget of the DEVICE window array (the layout bound stays as sized):
+    what a caller does when it derives budgets itself and passes capacity = NULL."""
+    import torch
+    wins = b.windows_dev.cpu().numpy().view(WINDOW_DTYPE).copy()
+    wins["budget"] = np.asarray(budgets, dtype=np.int32)
+    b.windows_dev.copy_(torch.as_tensor(wins.view(np.uint8)))
 
 
 def run_path(b: Batch, fused=True, stream=None, with_stats: bool = True, reset: bool = True):

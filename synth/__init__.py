@@ -38,4 +38,5 @@ from .workloads import (  # noqa: F401
     make_batched_random,
     supermodular_gain_table,
     batch_latency_table,
+    with_budget_edges,
 )

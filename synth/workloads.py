@@ -398,3 +398,34 @@ def make_batched_random(seed: int, W: int, max_frames: int = 8, K: int = 3, C: i
     wl.profiles_batch = batches
     wl.batch_cap = cap
     return wl
+
+
+# ----------------------------------------------------------------------------- a1 edge inputs
+S_EDGE_MODE, S_EDGE_VAL = 40, 41
+
+
+def with_budget_edges(wl: Workload, seed: int) -> Workload:
+    """Copy of `wl` whose capacities exercise every branch of a1 (reading R3):
+    the layout bound stays wl.budget, while the capacity handed to the path is drawn per window:
+      25 %  capacity in [N u0 - 100, N u0]   -> a1 clamps (budget 0; exactly 0 when = N u0)
+      10 %  capacity in [-1000, N u0]        -> deep clamp, some capacities negative
+      35 %  capacity = N u0 + U{0..B_bound}  -> device budget below (or at) the layout bound
+      30 %  unchanged (capacity = N u0 + B_bound, the exact fit)
+    Inputs only: no budget is computed here (the code under test derives it)."""
+    W = wl.num_windows
+    wid = np.arange(W, dtype=np.int64)
+    u = rand_uniform(seed, S_EDGE_MODE, wid)
+    nu0 = wl.num_frames.astype(np.int64) * int(wl.base_cost)
+    bb = wl.budget.astype(np.int64)
+    r = rand_uniform(seed, S_EDGE_VAL, wid)
+    cap = wl.capacity.astype(np.int64).copy()
+    m1 = u < 0.25
+    cap[m1] = nu0[m1] - np.floor(r[m1] * 101).astype(np.int64)
+    m2 = (u >= 0.25) & (u < 0.35)
+    cap[m2] = -1000 + np.floor(r[m2] * (nu0[m2] + 1001)).astype(np.int64)
+    m3 = (u >= 0.35) & (u < 0.70)
+    cap[m3] = nu0[m3] + np.floor(r[m3] * (bb[m3] + 1)).astype(np.int64)
+    out = Workload(f"{wl.name}+edges{seed}", wl.profiles_gain, wl.profiles_cost, wl.profiles_shape,
+                   wl.num_frames.copy(), wl.budget.copy(), cap.astype(np.int32), wl.base_cost, wl.profile.copy(),
+                   wl.class_id.copy(), dict(wl.meta))
+    return out

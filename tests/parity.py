@@ -8,12 +8,17 @@ import numpy as np
 import oracle
 
 
-def gpu_run(wl, fused=True, variant=0, with_stats=True):
+def gpu_run(wl, fused=True, variant=0, with_stats=True, device_budgets=None):
+    """device_budgets: run with capacity = NULL after writing these budgets into the device
+    windows (the layout bound stays wl.budget)."""
     import torch
     from paper_2207_00172_b200 import turbo
     turbo.debug_set_variant(variant)
     try:
-        b = turbo.batch_from_workload(wl, with_plan_workspace=not fused or (variant & 3) == 2)
+        b = turbo.batch_from_workload(wl, with_plan_workspace=not fused or (variant & 3) == 2,
+                                      null_capacity=device_budgets is not None)
+        if device_budgets is not None:
+            turbo.set_device_budgets(b, device_budgets)
         turbo.run_path(b, fused=fused, with_stats=with_stats)
         torch.cuda.synchronize()
         out = turbo.results(b)
@@ -24,8 +29,9 @@ def gpu_run(wl, fused=True, variant=0, with_stats=True):
     return out
 
 
-def oracle_run(wl, mode="table", threads=None):
-    return oracle.run(wl, mode=mode, threads=threads)
+def oracle_run(wl, mode="table", threads=None, budgets=None):
+    """budgets: plan these budgets directly (the capacity = NULL path) instead of a1."""
+    return oracle.run(wl, mode=mode, threads=threads, budgets=budgets)
 
 
 def compare(wl, got, want, check_options=True, windows=None):
