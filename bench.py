@@ -37,7 +37,8 @@ WORKLOADS = {
     "c2": dict(config=2, per_gpu=1024, desc="1024 streams x 1 s windows at 30 fps (N=30), K=5, B=1000 per GPU"),
     "c3": dict(config=3, per_gpu=8192, desc="8192 windows x 300 frames, K=8, B=4096 per GPU (c3 = 65536 over 8 GPUs)"),
     "c4": dict(config=4, per_gpu=1, desc="single long window: 3000 frames, K=6, B=2^20 (grid-spanning row; replicas)"),
-    "c5": dict(config=5, per_gpu=2048, desc="mixed sweep: K 2-16, B 64-16384, N 30-300, skewed classes; 2048 windows per GPU"),
+    "c5": dict(config=5, per_gpu=16384, desc="mixed sweep: K 2-16, B 64-16384, N 30-300, skewed classes; "
+                                           "16384 windows (the whole config) per GPU"),
     # NEXT-4 (batched latency): the c2 window shape with batch latency tables
     "b2": dict(config="b2", per_gpu=1024, desc="NEXT-4 batched-cost GAP: 1024 windows x 30 frames, K=5, B=1000, "
                                                "I_k(n) = ceil(c_k (2+3n)/5) per GPU"),
@@ -54,13 +55,60 @@ def dist_env():
     return ws, rank, local
 
 
-def make_workload(name: str, rank: int):
+def make_workload(name: str, rank: int, world: int = 1, scaling: str = "weak"):
+    """The rank's windows. weak: per_gpu windows at offset rank * per_gpu (per-GPU work fixed).
+    strong: the config's whole window set (BASELINE.json), split into contiguous work-balanced
+    ranges (shard.py) -- the same total work at every N."""
     import synth
     spec = WORKLOADS[name]
     if name.startswith("b"):
         return synth.make_batched_config(int(name[1:]), num_windows=spec["per_gpu"],
                                          window_offset=rank * spec["per_gpu"])
+    if scaling == "strong":
+        from paper_2207_00172_b200.shard import shard_ranges, work_per_window
+        whole = synth.CONFIGS[spec["config"]]["W"] if spec["config"] in synth.CONFIGS else 16384
+        full = synth.make_config(spec["config"])
+        assert full.num_windows == whole
+        lo, hi = shard_ranges(work_per_window(full.num_frames, full.budget, full.num_exits), world)[rank]
+        return synth.make_config(spec["config"], window_offset=lo, num_windows=hi - lo)
     return synth.make_config(spec["config"], window_offset=rank * spec["per_gpu"], num_windows=spec["per_gpu"])
+
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def measure_smem_peak(dev) -> dict:
+    """The shared-memory roofline denominator, measured live on this GPU: the library's
+    conflict-free 32-bit LDS stream kernel (turbo_debug_smem_stream) on every SM, CUDA events,
+    best of 5 after warm-up, 1 and 2 CTAs (1024 threads) per SM."""
+    import torch
+    from paper_2207_00172_b200 import turbo
+    sink = torch.zeros(4096, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    best, best_cfg = 0.0, None
+    for ctas in (1, 2):
+        iters = 6000 // ctas
+        for _ in range(2):
+            turbo.smem_stream(iters, ctas, sink)
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            nbytes = turbo.smem_stream(iters, ctas, sink)
+            e1.record(stream)
+            e1.synchronize()
+            gbs = nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9
+            if gbs > best:
+                best, best_cfg = gbs, ctas
+    return {"gbs": best, "ctas_per_sm": best_cfg,
+            "how": "turbo_debug_smem_stream: conflict-free ld.shared.u32 stream, 1024 threads x {1,2} CTAs per SM "
+                   "on every SM, CUDA events, best of 5 (burst)"}
 
 
 def _vectors(wl) -> int:
@@ -416,7 +464,7 @@ def run_turbo(args):
     turbo.load()
 
     name = args.workload
-    wl = make_workload(name, rank)
+    wl = make_workload(name, rank, ws, args.scaling)
     path = args.path
     if path == "auto":      # one fused launch unless long windows need the grid kernel
         path = "solve" if _has_long_windows(wl) else "schedule"
@@ -489,8 +537,18 @@ def run_turbo(args):
         g_dp.replay()
     torch.cuda.synchronize(dev)
 
+    g_lk = torch.cuda.CUDAGraph()                        # a2 gather alone (HBM roofline)
+    with torch.cuda.graph(g_lk):
+        turbo.profile_lookup(b.shape, b.profiles_dev, b.windows_dev, b.class_id, b.capacity, b.base_cost,
+                             b.opt_gain, b.opt_cost, b.status)
+    for _ in range(3):
+        g_lk.replay()
+    torch.cuda.synchronize(dev)
+    turbo.reset_outputs(b)
+
     evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     evd = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    evl = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clk = ClockSampler(local)
     if dist is not None:
         dist.barrier()
@@ -511,10 +569,17 @@ def run_turbo(args):
         evd[k][0].record(stream)
         g_dp.replay()
         evd[k][1].record(stream)
+    for k in range(args.steps):
+        flush.fill_(k & 0xff)
+        evl[k][0].record(stream)
+        g_lk.replay()
+        evl[k][1].record(stream)
     torch.cuda.synchronize(dev)
     clocks = clk.stop()
     t_step = sum(a.elapsed_time(bb) for a, bb in evs) / args.steps / 1e3          # s per step (this rank)
     t_dp = sum(a.elapsed_time(bb) for a, bb in evd) / args.steps / 1e3
+    t_lk = sum(a.elapsed_time(bb) for a, bb in evl) / args.steps / 1e3
+    turbo.reset_outputs(b)                               # (the lookup graph left status untouched)
 
     # correctness of the timed run (cheap, rank-local): no status errors
     st = b.status.cpu().numpy()
@@ -560,10 +625,16 @@ def run_turbo(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_step, t_dp, t_e2e = tt.tolist()
     N = ws
-    total_cells = cells * N
+    if dist is not None:           # whole-job totals (strong-scaling shards differ in size)
+        tot = torch.tensor([cells, W], dtype=torch.float64, device=dev)
+        dist.all_reduce(tot)
+        total_cells, W_total = int(tot[0].item()), int(tot[1].item())
+    else:
+        total_cells, W_total = cells, W
     value = total_cells / t_step
 
-    # ---- roofline of the dominant kernel (the DP): shared-memory bound
+    # ---- roofline of the dominant kernel (the DP): shared-memory bound, against the MEASURED
+    # smem stream rate of this GPU (derived 148 x 128 B/clk x sm_max_mhz kept beside it)
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -572,8 +643,17 @@ def run_turbo(args):
         pass
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
-    smem_peak = nsm * 128 * sm_max * 1e6 / 1e9                   # GB/s: 32 banks x 4 B per clock per SM
+    smem_derived = nsm * 128 * sm_max * 1e6 / 1e9                # GB/s: 32 banks x 4 B per clock per SM
+    smem_meas = measure_smem_peak(dev)
+    smem_peak = smem_meas["gbs"]
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs (measured)" if "hbm_gbs" in peaks else "fallback 6650 GB/s (profiling guide)"
     Kw = wl.num_exits.astype(np.int64)
+    # HBM streams: the a2 gather (class ids in, option tables out, window records) and the
+    # choice planes the timed call writes to HBM (0 when they stay in shared memory)
+    F = int(b.shape.total_frames)
+    lk_bytes = int((wl.num_frames.astype(np.int64) * (1 + 8 * Kw)).sum()) + 48 * W + 4 * W
+    plane_bytes = turbo.mckp_plane_bytes(b.shape, b.windows_host, path != "plan")
     alg_bytes = int((wl.num_frames.astype(np.int64) * (wl.budget.astype(np.int64) + 1) * (4 * Kw + 4)).sum())
     achieved = alg_bytes / t_dp / 1e9
     traffic = None
@@ -586,35 +666,55 @@ def run_turbo(args):
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "int32", "data": "synthetic (seeded splitmix64 generator, synth/; paper-calibrated profiles)",
         "config": {"workload": f"{name}: {WORKLOADS[name]['desc']}", "windows_per_gpu": W,
                    "cells_per_gpu_step": cells, "path": {"schedule": "turbo_schedule (a1-a6 in one launch)", "solve": "lookup + solve (a3-a5 fused) + stats",
                             "plan": "lookup + plan + backtrack + stats"}[path],
                    "l2": "flushed between timed steps (256 MiB write outside the step events)",
-                   "parallelism": f"weak dp{N} (windows sharded, NCCL allreduce of stats)"},
-        "windows_per_s": W * N / t_step,
+                   "parallelism": f"{args.scaling} dp{N} (windows sharded, NCCL allreduce of stats)",
+                   "windows_total": W_total},
+        "windows_per_s": W_total / t_step,
         "dp_ms": t_dp * 1e3,
         "dp_cell_updates_per_s": total_cells / t_dp,
         "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
                      "frac": achieved / smem_peak, "traffic": traffic,
+                     "peak_source": "measured live (" + smem_meas["how"] + ")",
+                     "peak_derived": smem_derived, "frac_of_derived": achieved / smem_derived,
                      "kernel": ("turbo::dp_cta_kernel (" + {"schedule": "turbo_schedule", "solve": "turbo_mckp_solve",
                                                             "plan": "turbo_mckp_plan"}[path] + ")"
                                 + (f"; timed as the whole call, {launches_dominant} launches (DP per row class,"
                                    " walks of HBM planes, long-window grid kernel)" if launches_dominant > 1 else "")),
                      "note": "algorithmic smem bytes = cells x (4K+4) per launch (SURVEY.md 8(d)); "
-                             "peak = SMs x 128 B/clk x sm_max_mhz (MEASURED_PEAKS.json), derived"},
+                             "peak = measured smem stream rate; peak_derived = SMs x 128 B/clk x sm_max_mhz"},
+        "hbm": {"peak": hbm_peak, "unit": "GB/s", "peak_source": hbm_src,
+                "lookup": {"kernel": "turbo::lookup_kernel (turbo_profile_lookup, timed alone)",
+                           "bytes": lk_bytes, "ms": t_lk * 1e3, "achieved": lk_bytes / t_lk / 1e9,
+                           "frac": lk_bytes / t_lk / 1e9 / hbm_peak,
+                           "note": "bytes = sum_w N_w (1 + 8 K_w) + 52 W (class ids, int32 option tables, "
+                                   "window records + capacity); not on the timed path of turbo_schedule"},
+                "choice_planes": {"bytes": plane_bytes, "achieved": plane_bytes / t_dp / 1e9,
+                                  "frac": plane_bytes / t_dp / 1e9 / hbm_peak,
+                                  "note": "choice planes the timed DP call writes to HBM (turbo_mckp_plane_bytes) "
+                                          "over the DP call's time"}},
         "e2e": {"value": total_cells / t_e2e, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": t_e2e * 1e3},
         "gpu_launches": launches_per_step * args.steps,
         "clocks": clocks,
     }
     if rank == 0 and not args.no_cpu_baseline:
-        rate, reps, el = oracle_rate(wl, args.cpu_seconds, os.cpu_count() or 1)
-        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": os.cpu_count() or 1, "kind": "oracle",
-                                "sample": f"{reps} passes over the rank-0 {name} windows ({wl.num_windows} windows, "
-                                          f"{cells} cells each), {el:.1f} s, table DP, gcc -O2, "
-                                          f"{os.cpu_count()} threads"}
+        nthr = os.cpu_count() or 1
+        sub = sample_for_oracle(wl, 2.5e8 * nthr * args.cpu_seconds / 10.0)
+        rate, reps, el = oracle_rate(sub, args.cpu_seconds, nthr)
+        sub1 = sample_for_oracle(wl, 2.5e8 * args.cpu_seconds / 20.0)
+        rate1, reps1, el1 = oracle_rate(sub1, args.cpu_seconds / 2.0, 1)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": nthr, "kind": "oracle",
+                                "value_1core": rate1, "cpu_model": cpu_model(),
+                                "sample": f"all cores: {reps} passes over {sub.num_windows} of the rank-0 {name} windows "
+                                          f"({sub.total_cells} cells per pass), {el:.1f} s, {nthr} threads; "
+                                          f"1 core: {reps1} passes over {sub1.num_windows} windows "
+                                          f"({sub1.total_cells} cells), {el1:.1f} s; table DP + reconstruction, "
+                                          f"gcc -O2"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -633,6 +733,9 @@ def main():
     ap.add_argument("--path", choices=["auto", "schedule", "solve", "plan"], default="auto",
                     help="auto: schedule unless long windows; schedule: one fused a1..a6 launch; solve: lookup, "
                          "solve, stats; plan: 4 launches")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: per-GPU windows fixed (per_gpu of the workload); strong: the config's whole "
+                         "window set split over the ranks by work (shard.py)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()

@@ -118,8 +118,9 @@ typedef struct {
 
 /* Rows longer than this many cells (budget_bound + 1) are planned by the long-window kernel:
  * one cooperative grid of CTAs per window, each CTA owning a contiguous budget segment, with
- * neighbour halos exchanged through an L2 ring. Costs in such a window
- * must not exceed TURBO_BIG_MAX_COST cells (else the window is rejected, status[1]). */
+ * neighbour halos exchanged through an L2 ring. Option costs up to
+ * TURBO_BIG_MAX_COST cells travel in the halo; a window with a larger cost is rejected
+ * (status[1], reading R17). */
 #define TURBO_BIG_CELLS 24576
 #define TURBO_BIG_MAX_COST 4096
 
@@ -139,9 +140,11 @@ typedef struct {
  * 177 sum best_cost; 178 #windows; 179 #frames; 180 #infeasible windows. */
 
 /* ---------------------------------------------------------------------------
- * Host-only sizing (no device access). Validates the host copies of profiles and
- * windows, fills windows_host[w].first_option / choice_offset / num_exits /
- * budget_bound, and fills *shape (including workspace_bytes).
+ * Host-only sizing (no device access). Not a step of the method: it lays out the buffers the
+ * steps of PAPER.md:519-525 (§5.2) need -- option blocks, bit-packed choice planes, the long-window
+ * scratch -- and the launch shape (row-size classes, serving order). Validates the host copies of
+ * profiles and windows, fills windows_host[w].first_option / choice_offset / num_exits /
+ * budget_bound / order, and fills *shape (including workspace_bytes).
  * profiles_host: host array of num_profiles descriptors (gain/cost pointers are
  *   not dereferenced here). windows_host: host array, modified in place.
  * Errors: INVALID_ARG (null, K or C out of range, profile index out of range,
@@ -166,7 +169,9 @@ turbo_status_t turbo_profile_lookup(const turbo_shape_t *shape /* host */,
                                     int64_t *status, turbo_stream_t stream);
 
 /* ---------------------------------------------------------------------------
- * a3 + a4: for every window, the suffix max-plus DP over frames N-1..0,
+ * a3 + a4 (§5.2 max / s.t., solved exactly = the paper's "upper", PAPER.md:858
+ * §6.4; reading R1 f = sum; tie-break R7 / SPEC.md:275): for every window, the suffix max-plus DP
+ * over frames N-1..0,
  *   S_N[b] = 0,  S_i[b] = max_{k : c_ik <= b} g_ik + S_{i+1}[b - c_ik]   (b = 0..B),
  * with the per-cell smallest maximising k written bit-packed to the workspace
  * (2 bits for K <= 4, 4 bits otherwise); then G* = S_0[B],
@@ -181,7 +186,9 @@ turbo_status_t turbo_mckp_plan(const turbo_shape_t *shape /* host */, const turb
                                int64_t *status, turbo_stream_t stream);
 
 /* ---------------------------------------------------------------------------
- * a5: plan reconstruction from the choice planes of turbo_mckp_plan:
+ * a5 ("execute each frame according to the plan": the plan kappa_x of every frame;
+ * forward walk = the lexicographic tie-break R7): plan reconstruction from the choice planes of
+ * turbo_mckp_plan:
  *   b = C*; for i = 0..N-1: k_i = choice_i[b]; exit_out[first_frame + i] = k_i; b -= c_{i,k_i}.
  * Infeasible or rejected windows get all-zero exits. exit_out: u8 [total_frames]. */
 turbo_status_t turbo_backtrack(const turbo_shape_t *shape /* host */, const turbo_window_t *windows,
@@ -203,6 +210,13 @@ turbo_status_t turbo_mckp_solve(const turbo_shape_t *shape /* host */, const tur
  * choice plane fits in shared memory). Host only. */
 turbo_status_t turbo_mckp_solve_workspace(const turbo_shape_t *shape, size_t *bytes /* host, out */);
 
+/* Host only (measurement): bytes of choice planes one call writes to HBM -- turbo_mckp_plan
+ * (fused = 0: every window) or turbo_mckp_solve / turbo_schedule (fused = 1: the windows whose
+ * planes do not stay in shared memory, and every long window). windows_host: the sized host
+ * array of turbo_mckp_workspace. The denominator of the choice-plane HBM stream's roofline. */
+turbo_status_t turbo_mckp_plane_bytes(const turbo_shape_t *shape, const turbo_window_t *windows_host,
+                                      int32_t fused, int64_t *hbm_bytes /* host, out */);
+
 /* ---------------------------------------------------------------------------
  * The whole path a1..a6 in ONE launch (one CTA per window): a1 budget from capacity (when
  * capacity != NULL, written back to windows[w].budget), a2 option rows read straight from
@@ -210,8 +224,11 @@ turbo_status_t turbo_mckp_solve_workspace(const turbo_shape_t *shape, size_t *by
  * status[0] and gives a zero row, exactly as turbo_profile_lookup), a3..a5 as
  * turbo_mckp_solve, a6 ACCUMULATED into stats (int64[181], caller zeroes it).
  * Outputs are bit-identical to lookup -> solve -> stats. Workspace as turbo_mckp_solve
- * (turbo_mckp_solve_workspace() bytes). Returns TURBO_ERR_UNSUPPORTED when one window's
- * option table (max_frames x max_exits x 8 B) exceeds 48 KiB; use the separate calls then. */
+ * (turbo_mckp_solve_workspace() bytes). Windows of every size are served: rows up to
+ * TURBO_BIG_CELLS cells by one launch per row-size class, longer rows by the long-window grid
+ * kernel with a1, a2 and a6 fused into it as well. Returns TURBO_ERR_UNSUPPORTED (before any
+ * launch) only when a launch cannot fit the device (a long row too large for the grid's shared
+ * memory, about 1.8M cells on 148 SMs). */
 turbo_status_t turbo_schedule(const turbo_shape_t *shape /* host */, const turbo_profile_t *profiles,
                               turbo_window_t *windows, const uint8_t *class_id,
                               const int32_t *capacity /* nullable */, int32_t base_cost,
@@ -255,7 +272,10 @@ turbo_status_t turbo_batches(const turbo_shape_t *shape /* host */, const turbo_
 
 /* ---------------------------------------------------------------------------
  * a6 (per GPU): ACCUMULATES the plan statistics into stats (int64[181], layout
- * above; caller zeroes it). The cross-GPU sum (one allreduce over NVLink) is done by
+ * above; caller zeroes it): the per-exit usage and per-difficulty-class x exit histograms and
+ * the totals the paper's scheduler evaluation reports per run (accuracy gain, GPU time of the
+ * chosen enhancement, infeasible windows; PAPER.md:561-562 §6, :858 §6.4). Not part of the
+ * optimisation itself. The cross-GPU sum (one allreduce over NVLink) is done by
  * the caller's communicator, not inside the library. */
 turbo_status_t turbo_stats(const turbo_shape_t *shape /* host */, const turbo_window_t *windows,
                            const uint8_t *class_id, const uint8_t *exit_out,
@@ -297,6 +317,13 @@ turbo_status_t turbo_debug_set_variant(int32_t variant);
  * needed in production. Returns TURBO_ERR_UNSUPPORTED unless the library was built with
  * TURBO_TRACE defined (the marks are compiled out of production builds). */
 turbo_status_t turbo_debug_trace(int64_t *trace, int64_t words);
+/* Measurement hook (not a step of the method): the shared-memory roofline denominator. Launches
+ * ctas_per_sm (1 or 2) x SMs CTAs of 1024 threads, each thread issuing iters x 32 conflict-free
+ * 32-bit shared loads (one 128-B wavefront per warp instruction, the DP's access type);
+ * *bytes_out (host) = bytes the launch reads. The caller times the launch (CUDA events) and
+ * divides. sink: device, >= 4 KB, never meaningfully written. */
+turbo_status_t turbo_debug_smem_stream(int32_t iters, int32_t ctas_per_sm, void *sink, double *bytes_out,
+                                       turbo_stream_t stream);
 /* Kernels this library has launched so far in the process (all threads and devices; graph
  * capture counts the captured launches once). Lets a caller count the kernels of a call. */
 int64_t turbo_launch_count(void);

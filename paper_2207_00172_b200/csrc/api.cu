@@ -76,19 +76,18 @@ static int32_t dp_pad_words(const turbo_shape_t *s)
 
 // Per-device streams and events used to run the row-size class launches concurrently.
 struct ForkJoin {
-    std::mutex mu;
     cudaStream_t streams[TURBO_NUM_CLASSES];
     cudaEvent_t fork;
     cudaEvent_t join[TURBO_NUM_CLASSES];
 };
 
+// Per calling THREAD and device: concurrent callers (or one thread capturing a graph while another
+// launches eagerly) never share a library stream. The streams live as long as the process.
 static ForkJoin *fork_join_for_device()
 {
-    static std::mutex mu;
-    static ForkJoin *per_dev[64] = {nullptr};
+    thread_local ForkJoin *per_dev[64] = {nullptr};
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
-    std::lock_guard<std::mutex> lk(mu);
     if (!per_dev[dev]) {
         ForkJoin *fj = new ForkJoin();
         for (int c = 0; c < TURBO_NUM_CLASSES; ++c) {
@@ -329,7 +328,17 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int kind, const DpParam
 {
     DeviceInfo d;
     if (device_info(&d) != cudaSuccess) return TURBO_ERR_CUDA;
-    if (kind == RUN_SCHEDULE && shape->num_big > 0) return TURBO_ERR_UNSUPPORTED;
+    // long windows (the grid kernel) are validated first: nothing is launched unless every launch
+    // of the call can run
+    const int grid_mode = kind == RUN_PLAN ? DP_PLAN : DP_SOLVE_GLOBAL;
+    if (shape->num_big > 0) {
+        const cudaError_t ge = check_dp_grid(shape, grid_mode, d.num_sms, d.smem_per_cta_optin);
+        if (ge != cudaSuccess) {
+            cudaGetLastError();
+            return ge == cudaErrorInvalidConfiguration || ge == cudaErrorCooperativeLaunchTooLarge
+                       ? TURBO_ERR_UNSUPPORTED : TURBO_ERR_CUDA;
+        }
+    }
     DpParams Ps[TURBO_NUM_CLASSES];
     turbo_shape_t shapes[TURBO_NUM_CLASSES];
     int modes[TURBO_NUM_CLASSES];
@@ -361,8 +370,9 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int kind, const DpParam
         P.ordered = (shape->ordered && !dp_kernel_fixed_k(shapes[c].min_exits, shapes[c].max_exits)) ? 1 : 0;
         P.cls_first = 0;
         for (int c2 = 0; c2 < c; ++c2) P.cls_first += shape->cls_count[c2];
-        if (dp_smem_bytes(P, dp_warps_per_window(&shapes[c])) > (size_t)d.smem_per_cta_optin)
-            return TURBO_ERR_UNSUPPORTED;
+        const cudaError_t ce = check_dp(&shapes[c], modes[c], P, d.smem_per_cta_optin);   // incl. static smem
+        if (ce == cudaErrorInvalidConfiguration) return TURBO_ERR_UNSUPPORTED;
+        if (ce != cudaSuccess) return TURBO_ERR_CUDA;
     }
     DpLaunch info;
     cudaError_t e = cudaSuccess;
@@ -395,28 +405,28 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int kind, const DpParam
         // caller's stream with events -- stream-ordered for the caller and capturable in graphs.
         ForkJoin *fj = fork_join_for_device();
         if (!fj) return TURBO_ERR_CUDA;
-        std::lock_guard<std::mutex> lk(fj->mu);
         e = cudaEventRecord(fj->fork, (cudaStream_t)stream);
         int order = shape->cls_order, seen = 0;                     // a permutation, else 0 1 2 3
         for (int i = 0; i < TURBO_NUM_CLASSES; ++i) seen |= 1 << ((order >> (4 * i)) & 15);
         if (seen != (1 << TURBO_NUM_CLASSES) - 1) order = 0x3210;
         for (int i = 0; i < TURBO_NUM_CLASSES && e == cudaSuccess; ++i) {
-            const int c = (order >> (4 * i)) & 15;                     // heaviest window first
+            const int c = (order >> (4 * i)) & 15;
             if (c >= TURBO_NUM_CLASSES || !shape->cls_count[c]) continue;
             if ((e = cudaStreamWaitEvent(fj->streams[c], fj->fork, 0)) != cudaSuccess) break;
-            if ((e = launch_dp(&shapes[c], modes[c], Ps[c], d.num_sms, d.smem_per_sm, d.smem_per_cta_optin,
-                               fj->streams[c], &info)) != cudaSuccess)
-                break;
-            if ((e = launch_walk(c, fj->streams[c])) != cudaSuccess) break;
-            if ((e = cudaEventRecord(fj->join[c], fj->streams[c])) != cudaSuccess) break;
-            e = cudaStreamWaitEvent((cudaStream_t)stream, fj->join[c], 0);
+            // every forked stream is joined back below, also when a launch on it fails (an unjoined
+            // stream would break the caller's graph capture)
+            e = launch_dp(&shapes[c], modes[c], Ps[c], d.num_sms, d.smem_per_sm, d.smem_per_cta_optin,
+                          fj->streams[c], &info);
+            if (e == cudaSuccess) e = launch_walk(c, fj->streams[c]);
+            cudaError_t je = cudaEventRecord(fj->join[c], fj->streams[c]);
+            if (je == cudaSuccess) je = cudaStreamWaitEvent((cudaStream_t)stream, fj->join[c], 0);
+            if (e == cudaSuccess) e = je;
         }
     }
     if (e == cudaSuccess && shape->num_big > 0) {          // long windows: the whole grid per window
         DpParams P = base;
         P.grid_scratch_offset = shape->grid_scratch_offset;
-        e = launch_dp_grid(shape, kind == RUN_PLAN ? DP_PLAN : DP_SOLVE_GLOBAL, P, d.num_sms, d.smem_per_cta_optin,
-                           (cudaStream_t)stream);
+        e = launch_dp_grid(shape, grid_mode, P, d.num_sms, d.smem_per_cta_optin, (cudaStream_t)stream);
     }
     if (e == cudaErrorInvalidConfiguration || e == cudaErrorCooperativeLaunchTooLarge) {
         cudaGetLastError();
@@ -488,6 +498,29 @@ turbo_status_t turbo_backtrack(const turbo_shape_t *shape, const turbo_window_t 
                                      reinterpret_cast<const uint8_t *>(workspace), best_cost, feasible, exit_out,
                                      d.num_sms, (cudaStream_t)stream);
     return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
+}
+
+turbo_status_t turbo_mckp_plane_bytes(const turbo_shape_t *shape, const turbo_window_t *windows_host,
+                                      int32_t fused, int64_t *hbm_bytes)
+{
+    if (!shape || !hbm_bytes || (shape->num_windows > 0 && !windows_host)) return TURBO_ERR_INVALID_ARG;
+    bool hbm_class[TURBO_NUM_CLASSES + 1];
+    for (int c = 0; c < TURBO_NUM_CLASSES; ++c) {
+        hbm_class[c] = !fused;
+        if (fused && shape->cls_count[c]) {
+            const turbo_shape_t cs = class_shape(shape, c);
+            hbm_class[c] = solve_mode(&cs) == DP_SOLVE_GLOBAL;
+        }
+    }
+    hbm_class[TURBO_NUM_CLASSES] = true;                 // long windows: always HBM planes
+    int64_t total = 0;
+    for (int32_t w = 0; w < shape->num_windows; ++w) {
+        const turbo_window_t &win = windows_host[w];
+        const int rc = std::min(row_class((int64_t)win.budget_bound + 1), TURBO_NUM_CLASSES);
+        if (hbm_class[rc]) total += choice_plane_bytes(win.num_frames, win.budget_bound, win.num_exits);
+    }
+    *hbm_bytes = total;
+    return TURBO_OK;
 }
 
 turbo_status_t turbo_mckp_solve_workspace(const turbo_shape_t *shape, size_t *bytes)

@@ -15,6 +15,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdlib>
+#include <algorithm>
 #include <mutex>
 
 #include "dp_kernel.cuh"
@@ -288,10 +289,27 @@ __device__ __forceinline__ void backtrack_cta_spec(int32_t N, int32_t b, const u
     __syncthreads();
 }
 
+// a6 of a rejected long window (turbo_schedule): all frames at level 0, G* = C* = 0, infeasible
+// (the same counts the CTA kernels give a rejected window)
+__device__ __forceinline__ void reject_stats(const DpParams &P, uint32_t *hist, int64_t ff, int32_t N, int tid,
+                                             int nthr)
+{
+    for (int x = tid; x < 176; x += nthr) hist[x] = 0;
+    __syncthreads();
+    for (int32_t i = tid; i < N; i += nthr) {
+        const uint32_t cls = P.class_id[ff + i];
+        atomicAdd(&hist[0], 1u);
+        if (cls < 10) atomicAdd(&hist[16 + cls * 16], 1u);
+    }
+    __syncthreads();
+    flush_window_stats(P, hist, 0, 0, false, N, tid, nthr);
+    __syncthreads();
+}
+
 template <int K, int MODE>
 __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, int32_t *bufA, int32_t *bufB,
                            long long *red, GridCtx X, int &step_base, unsigned long long *stage_in,
-                           unsigned long long *stage_out, uint64_t *mbar, uint32_t *mbar_uses)
+                           unsigned long long *stage_out, uint64_t *mbar, uint32_t *mbar_uses, uint32_t *hist)
 {
     constexpr int CB = (K <= 4) ? 2 : 4;
     constexpr int RPT = 32 / CB;
@@ -303,10 +321,36 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
     const turbo_window_t *win = P.windows + w;
     const int64_t ff = win->first_frame;
     const int32_t N = win->num_frames;
-    const int32_t B = win->budget;
+    int32_t B = win->budget;
     const int32_t Bb = win->budget_bound;
     const int32_t *__restrict__ og = P.opt_gain + win->first_option;
     const int32_t *__restrict__ oc = P.opt_cost + win->first_option;
+    // turbo_schedule (P.fuse): a1 budget from the capacity, a2 options straight from the frame's
+    // class and the profile (a class >= C reads as a zero row and sets status[0], as the lookup)
+    const bool fuse = P.fuse != 0;
+    int32_t prof_C = 0;
+    const int32_t *prof_g = nullptr, *prof_c = nullptr;
+    if (fuse) {
+        const turbo_profile_t *prof = P.profiles + win->profile;
+        prof_C = prof->num_classes;
+        prof_g = prof->gain;
+        prof_c = prof->cost;
+        if (P.capacity != nullptr) {       // a1 (reading R3): max(0, capacity - m u0)
+            const int64_t b = (int64_t)P.capacity[w] - (int64_t)N * (int64_t)P.base_cost;
+            B = (int32_t)(b < 0 ? 0 : (b > 0x7fffffffll ? 0x7fffffff : b));
+            if (blockIdx.x == 0 && threadIdx.x == 0) P.windows_rw[w].budget = B;
+        }
+    }
+    auto opt_g = [&](int32_t i, int32_t k) -> int32_t {
+        if (!fuse) return __ldg(og + (int64_t)i * K + k);
+        const int32_t cls = P.class_id[ff + i];
+        return cls < prof_C ? __ldg(prof_g + cls * K + k) : 0;
+    };
+    auto opt_c = [&](int32_t i, int32_t k) -> int32_t {
+        if (!fuse) return __ldg(oc + (int64_t)i * K + k);
+        const int32_t cls = P.class_id[ff + i];
+        return cls < prof_C ? __ldg(prof_c + cls * K + k) : 0;
+    };
     uint32_t *__restrict__ gch = reinterpret_cast<uint32_t *>(P.workspace + win->choice_offset);
     const int32_t gtiles = (int32_t)(((Bb + 32) >> 5) + RPT - 1) / RPT;
     const int32_t nrows = (B + 32) >> 5;
@@ -324,9 +368,10 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
         long long bad = 0, cmax = 0, g0 = 0, c0 = 0, asum = 0;
         for (int32_t i = j * nthr + tid; i < N; i += NP * nthr) {
             int32_t m = 0;
+            if (fuse && (int32_t)P.class_id[ff + i] >= prof_C) atomic_min_i64(&P.status[0], ff + i);
             for (int k = 0; k < K; ++k) {
-                const int32_t g = __ldg(og + (int64_t)i * K + k);
-                const int32_t c = __ldg(oc + (int64_t)i * K + k);
+                const int32_t g = opt_g(i, k);
+                const int32_t c = opt_c(i, k);
                 const int32_t a = g < 0 ? -g : g;
                 m = a > m ? a : m;
                 bad |= (c < 0) || (c >= (1 << 30)) || (g > (1 << 24)) || (g < -(1 << 24));
@@ -370,6 +415,7 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
         }
         if (MODE != DP_PLAN)
             for (int32_t i = j * nthr + tid; i < N; i += NP * nthr) P.exit_out[ff + i] = 0;
+        if (fuse && j == 0) reject_stats(P, hist, ff, N, tid, nthr);
         return;
     }
     const int32_t hl = cmax;                        // halo length actually needed (<= H)
@@ -386,8 +432,8 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
 
     int32_t my_g = 0, my_c = 0;                       // lane k < K: option k of the next frame (raw)
     if (N > 0 && lane < K) {
-        my_g = __ldg(og + (int64_t)(N - 1) * K + lane);
-        my_c = __ldg(oc + (int64_t)(N - 1) * K + lane);
+        my_g = opt_g(N - 1, lane);
+        my_c = opt_c(N - 1, lane);
     }
     int32_t *cur = bufA, *nxt = bufB;
     const int32_t t_first = seg_lo / (32 * RPT);
@@ -443,8 +489,8 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
             cc[k] = __shfl_sync(0xffffffffu, my_c, k);
         }
         if (i > 0 && lane < K) {                       // consumed one frame later (no stall here)
-            my_g = __ldg(og + (int64_t)(i - 1) * K + lane);
-            my_c = __ldg(oc + (int64_t)(i - 1) * K + lane);
+            my_g = opt_g(i - 1, lane);
+            my_c = opt_c(i - 1, lane);
         }
         const long long c_step = trace ? clock64() : 0;
         if (mine) {
@@ -496,8 +542,10 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
                     // back-pressure: the consumer must have taken the slot's previous content; the
                     // last value seen usually still proves it, so the L2 poll is rare
                     if (f >= D && con_seen < slot_step - D + 1 &&
-                        !wait_at_least(&X.con[j + 1], slot_step - D + 1, con_seen))
+                        !wait_at_least(&X.con[j + 1], slot_step - D + 1, con_seen)) {
                         atomic_min_i64(&status[1], w);
+                        atomicOr(reinterpret_cast<unsigned long long *>(&X.misc[7]), 1ull);   // window failed
+                    }
                     unsigned long long *dst = X.ring + ((int64_t)(slot_step % D) * GRID_MAX_CTAS + j) * H;
                     tma_store_1d(dst, stg, hl8 * 8);
                     if (trace) X.trace[j * 8 + 2] += clock64() - c0;
@@ -532,7 +580,10 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
                     }
                     ok = !(group ? named_sync_or(1, gn, stale) : __syncthreads_or(stale));
                 }
-                if (!ok && gtid == 0) atomic_min_i64(&status[1], w);
+                if (!ok && gtid == 0) {
+                    atomic_min_i64(&status[1], w);
+                    atomicOr(reinterpret_cast<unsigned long long *>(&X.misc[7]), 1ull);   // window failed
+                }
                 if (trace && gtid == 0) {
                     X.trace[j * 8 + 0] += attempt - 1;
                     X.trace[j * 8 + 1] += clock64() - c0;
@@ -604,6 +655,19 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
     cnt = block_sum_ll(cnt, red, tid, nthr);
     if (tid == 0 && cnt) atomicAdd(reinterpret_cast<unsigned long long *>(&X.misc[6]), (unsigned long long)cnt);
     grid.sync();
+    if (*((volatile long long *)&X.misc[7]) != 0) {
+        // a halo or back-pressure wait timed out (status[1] is set): the rows may be corrupt, so
+        // the window is reported as rejected -- all-zero exits, G* = C* = 0, feasible = 0
+        if (j == 0 && tid == 0) {
+            P.best_gain[w] = 0;
+            P.best_cost[w] = 0;
+            P.feasible[w] = 0;
+        }
+        if (MODE != DP_PLAN)
+            for (int32_t i = j * nthr + tid; i < N; i += NP * nthr) P.exit_out[ff + i] = 0;
+        if (fuse && j == 0) reject_stats(P, hist, ff, N, tid, nthr);
+        return;
+    }
     const bool feas = RB > VALID_MIN_R;
     const int32_t G = feas ? (RB >> 4) : (int32_t)g0_sum;
     const int32_t Cst = feas ? (int32_t)*((volatile long long *)&X.misc[6]) : (int32_t)c0_sum;
@@ -617,8 +681,23 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
     if (!feas) {
         for (int32_t i = j * nthr + tid; i < N; i += NP * nthr) P.exit_out[ff + i] = 0;
     } else if (j == 0) {                               // CTA 0, all threads (the grid is idle)
-        auto cost = [&](int32_t i, int32_t k) -> int32_t { return __ldg(oc + (int64_t)i * K + k); };
+        auto cost = [&](int32_t i, int32_t k) -> int32_t { return opt_c(i, k); };
         backtrack_cta_spec<K>(N, Cst, gch, gtiles, cost, P.exit_out + ff, red + 8);
+    }
+    if (fuse && j == 0) {
+        // a6 of the long window (turbo_schedule): CTA 0 bins the plan it just wrote (an infeasible
+        // plan is all zero) and adds the window's totals to the per-GPU vector
+        for (int x = tid; x < 176; x += nthr) hist[x] = 0;
+        __syncthreads();
+        for (int32_t i = tid; i < N; i += nthr) {
+            const uint32_t k = feas ? (P.exit_out[ff + i] & 15u) : 0u;
+            const uint32_t cls = P.class_id[ff + i];
+            atomicAdd(&hist[k], 1u);
+            if (cls < 10) atomicAdd(&hist[16 + cls * 16 + k], 1u);
+        }
+        __syncthreads();
+        flush_window_stats(P, hist, G, Cst, feas, N, tid, nthr);
+        __syncthreads();
     }
 }
 
@@ -627,13 +706,13 @@ template <int K, int MODE>
 __device__ __noinline__ void grid_window_call(const DpParams &P, cg::grid_group &grid, int64_t w, int32_t *bufA,
                                               int32_t *bufB, long long *red, GridCtx X, int &step_base,
                                               unsigned long long *stage_in, unsigned long long *stage_out,
-                                              uint64_t *mbar, uint32_t *mbar_uses)
+                                              uint64_t *mbar, uint32_t *mbar_uses, uint32_t *hist)
 {
-    grid_window<K, MODE>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar, mbar_uses);
+    grid_window<K, MODE>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar, mbar_uses, hist);
 }
 
 template <int KSEL, int MODE>
-__global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg_max, int32_t tag_base)
+__global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg_max, int32_t span)
 {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ int4 smem_raw[];
@@ -644,6 +723,7 @@ __global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg
     unsigned long long *stage_out = stage_in + TURBO_BIG_MAX_COST;          // two stages (parity)
     uint64_t *mbar = reinterpret_cast<uint64_t *>(stage_out + 2 * TURBO_BIG_MAX_COST);
     uint32_t *mbar_uses = reinterpret_cast<uint32_t *>(mbar + 1);           // completed halo loads
+    __shared__ uint32_t ghist[176];                                         // a6 of turbo_schedule
     if (threadIdx.x == 0) {
         mbar_init(mbar, 1);
         *mbar_uses = 0;
@@ -654,18 +734,37 @@ __global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg
     X.pub = flags;
     X.con = flags + GRID_MAX_CTAS;
     X.misc = reinterpret_cast<long long *>(flags + 2 * GRID_MAX_CTAS);
-    X.ring = reinterpret_cast<unsigned long long *>(flags + grid_flags_words());
+    unsigned long long *hdr = reinterpret_cast<unsigned long long *>(flags + grid_flags_words());
+    X.ring = reinterpret_cast<unsigned long long *>(flags + grid_flags_words() + GRID_HEADER_WORDS);
     X.trace = reinterpret_cast<long long *>(flags + 2 * GRID_MAX_CTAS + 64);
-    int step_base = tag_base;          // ring tags of this launch never repeat an earlier launch's
+    // Ring tags continue from the epoch stored in this workspace (every CTA reads it before the
+    // first grid barrier; CTA 0 advances it after the last one), so a ring word left by an earlier
+    // launch -- or an earlier replay of a captured graph -- never carries a tag this launch expects.
+    // A fresh workspace (no magic) or an epoch about to wrap clears the ring first.
+    int step_base;
+    {
+        const unsigned long long magic = ld_relaxed_u64(hdr);
+        const int epoch = ld_relaxed_gpu(reinterpret_cast<const int *>(hdr + 1));
+        const bool clear = magic != GRID_MAGIC || epoch < 1 || (int64_t)epoch + span >= (1ll << 30);
+        if (clear) {
+            const int64_t words = (int64_t)GRID_RING_DEPTH * GRID_MAX_CTAS * TURBO_BIG_MAX_COST;
+            for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < words;
+                 x += (int64_t)gridDim.x * blockDim.x)
+                X.ring[x] = 0ull;
+        }
+        step_base = clear ? 1 : epoch;
+        grid.sync();                   // ring cleared; every CTA has read the header
+    }
     for (int64_t w = 0; w < P.num_windows; ++w) {
         if ((int64_t)P.windows[w].budget_bound + 1 <= TURBO_BIG_CELLS) continue;
         if (KSEL != 0) {
             grid_window<(KSEL > 0 ? KSEL : 2), MODE>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar,
-                                                     mbar_uses);
+                                                     mbar_uses, ghist);
         } else {
             switch (P.windows[w].num_exits) {
 #define TURBO_K_CASE(KK) \
-    case KK: grid_window_call<KK, MODE>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar, mbar_uses); \
+    case KK: grid_window_call<KK, MODE>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar, mbar_uses, \
+                                        ghist);                                                                  \
         break;
                 TURBO_K_CASE(2) TURBO_K_CASE(3) TURBO_K_CASE(4) TURBO_K_CASE(5) TURBO_K_CASE(6)
                 TURBO_K_CASE(7) TURBO_K_CASE(8) TURBO_K_CASE(9) TURBO_K_CASE(10) TURBO_K_CASE(11)
@@ -677,6 +776,10 @@ __global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg
         grid.sync();                                   // every CTA done with this window
         if (blockIdx.x == 0 && threadIdx.x < 8) X.misc[threadIdx.x] = 0;
         grid.sync();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {         // the next launch on this workspace continues here
+        st_relaxed_u32(reinterpret_cast<int *>(hdr + 1), step_base);
+        st_relaxed_u64(hdr, GRID_MAGIC);
     }
 }
 
@@ -696,48 +799,64 @@ static dp_grid_kernel_t pick_grid(int kmin, int kmax)
     }
 }
 
-cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams &P0, int num_sms,
-                           int smem_per_cta_max, cudaStream_t stream)
+// Launch geometry of the long-window kernel: CTAs, segment cells, dynamic shared memory; and the
+// host-only checks (shared memory incl. the kernel's static part, cooperative residency) that
+// run_dp performs before launching anything.
+static cudaError_t grid_geometry(const turbo_shape_t *shape, int mode, int num_sms, int smem_per_cta_max,
+                                 dp_grid_kernel_t *kern_out, int *np_out, int32_t *seg_out, size_t *smem_out)
 {
-    DpParams P = P0;
     const int NP = num_sms < GRID_MAX_CTAS ? num_sms : GRID_MAX_CTAS;
     int32_t seg = (int32_t)(((int64_t)shape->max_budget + 1 + NP - 1) / NP);
     seg = (seg + 511) & ~511;
     if (seg < TURBO_BIG_MAX_COST) seg = TURBO_BIG_MAX_COST;
     const size_t smem = 128 + (size_t)8 * (TURBO_BIG_MAX_COST + seg) + (size_t)24 * TURBO_BIG_MAX_COST + 16;
-    if (smem > (size_t)smem_per_cta_max) return cudaErrorInvalidConfiguration;
     dp_grid_kernel_t kern = mode == DP_PLAN ? pick_grid<DP_PLAN>(shape->min_exits, shape->max_exits)
                                             : pick_grid<DP_SOLVE_GLOBAL>(shape->min_exits, shape->max_exits);
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+    if (e != cudaSuccess) return e;
+    if (smem + fa.sharedSizeBytes > (size_t)smem_per_cta_max) return cudaErrorInvalidConfiguration;
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     int occ = 0;
     e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, GRID_THREADS, smem);
     if (e != cudaSuccess) return e;
     if (occ < 1) return cudaErrorCooperativeLaunchTooLarge;
+    *kern_out = kern;
+    *np_out = NP;
+    *seg_out = seg;
+    *smem_out = smem;
+    return cudaSuccess;
+}
+
+cudaError_t check_dp_grid(const turbo_shape_t *shape, int mode, int num_sms, int smem_per_cta_max)
+{
+    dp_grid_kernel_t kern;
+    int NP;
+    int32_t seg;
+    size_t smem;
+    return grid_geometry(shape, mode, num_sms, smem_per_cta_max, &kern, &NP, &seg, &smem);
+}
+
+cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams &P0, int num_sms,
+                           int smem_per_cta_max, cudaStream_t stream)
+{
+    DpParams P = P0;
+    dp_grid_kernel_t kern;
+    int NP;
+    int32_t seg;
+    size_t smem;
+    cudaError_t e = grid_geometry(shape, mode, num_sms, smem_per_cta_max, &kern, &NP, &seg, &smem);
+    if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(P.workspace + P.grid_scratch_offset, 0, (size_t)grid_flags_words() * 4, stream);
     if (e != cudaSuccess) return e;
-    // ring tags: a per-process epoch advanced past every step this launch can take, so a stale
-    // ring word from an earlier launch can never carry a matching tag (the ring is cleared when
-    // the epoch wraps)
-    static std::mutex mu;
-    int32_t tag_base;
-    {
-        std::lock_guard<std::mutex> lk(mu);
-        static int64_t epoch = 1;
-        const int64_t span = (int64_t)shape->num_big * shape->max_frames + 2;
-        if (epoch + span >= (1ll << 30)) {
-            e = cudaMemsetAsync(P.workspace + P.grid_scratch_offset, 0, (size_t)grid_scratch_bytes(), stream);
-            if (e != cudaSuccess) return e;
-            epoch = 1;
-        }
-        tag_base = (int32_t)epoch;
-        epoch += span;
-    }
+    // ring tags this launch can consume (the epoch itself lives in the workspace header)
+    int32_t span = (int32_t)std::min<int64_t>((int64_t)shape->num_big * shape->max_frames + 2, 1 << 29);
     {
         const char *dbg = getenv("TURBO_GRID_DEBUG");      // 1: no halo exchange (timing only)
         P.debug = dbg ? atoi(dbg) : 0;
     }
-    void *args[] = {(void *)&P, (void *)&seg, (void *)&tag_base};
+    void *args[] = {(void *)&P, (void *)&seg, (void *)&span};
     note_launch();
     return cudaLaunchCooperativeKernel((const void *)kern, dim3(NP), dim3(GRID_THREADS), args, smem, stream);
 }

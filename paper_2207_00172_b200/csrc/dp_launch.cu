@@ -75,6 +75,46 @@ size_t dp_smem_bytes(const DpParams &P, int nwarps)
                              P.cst_words);
 }
 
+// The kernel a class launch uses, and its dynamic-smem ceiling (the per-CTA opt-in maximum minus
+// the kernel's static smem). Host-only queries: run_dp calls this for every class BEFORE any launch.
+static cudaError_t resolve_dp(const turbo_shape_t *shape, int mode, const DpParams &P, int smem_per_cta_max,
+                              dp_kernel_t *kern_out, size_t *dyn_max_out)
+{
+    const bool osm = P.osm != 0;
+    // (HBM choice planes are always walked by a separate kernel: DP_SOLVE_GLOBAL never gets here)
+    if (mode == DP_SOLVE_GLOBAL) return cudaErrorInvalidValue;
+    dp_kernel_t kern = P.fuse                  ? dp_kernel_schedule(shape->min_exits, shape->max_exits, mode, osm)
+                       : mode == DP_PLAN         ? dp_kernel_plan(shape->min_exits, shape->max_exits, osm)
+                                                 : dp_kernel_solve_smem(shape->min_exits, shape->max_exits, osm);
+    static std::mutex amu;
+    static std::map<const void *, size_t> static_smem;
+    size_t st_bytes = 0;
+    {
+        std::lock_guard<std::mutex> lk(amu);
+        auto it = static_smem.find((const void *)kern);
+        if (it == static_smem.end()) {
+            cudaFuncAttributes fa;
+            cudaError_t e = cudaFuncGetAttributes(&fa, kern);
+            if (e != cudaSuccess) return e;
+            it = static_smem.emplace((const void *)kern, fa.sharedSizeBytes).first;
+        }
+        st_bytes = it->second;
+    }
+    if ((size_t)smem_per_cta_max <= st_bytes) return cudaErrorInvalidConfiguration;
+    *kern_out = kern;
+    *dyn_max_out = (size_t)smem_per_cta_max - st_bytes;
+    return cudaSuccess;
+}
+
+cudaError_t check_dp(const turbo_shape_t *shape, int mode, const DpParams &P, int smem_per_cta_max)
+{
+    dp_kernel_t kern = nullptr;
+    size_t dyn_max = 0;
+    cudaError_t e = resolve_dp(shape, mode, P, smem_per_cta_max, &kern, &dyn_max);
+    if (e != cudaSuccess) return e;
+    return dp_smem_bytes(P, dp_warps_per_window(shape)) > dyn_max ? cudaErrorInvalidConfiguration : cudaSuccess;
+}
+
 cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P0, int num_sms, int smem_per_sm,
                       int smem_per_cta_max, cudaStream_t stream, DpLaunch *info)
 {
@@ -84,30 +124,10 @@ cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P0, 
     const int G = dp_warps_per_window(shape);
     P.warps_per_cta = G;
     const size_t need = dp_smem_bytes(P, G);
-
-    const bool osm = P.osm != 0;
-    // (HBM choice planes are always walked by a separate kernel: DP_SOLVE_GLOBAL never gets here)
-    if (mode == DP_SOLVE_GLOBAL) return cudaErrorInvalidValue;
-    dp_kernel_t kern = P.fuse                  ? dp_kernel_schedule(shape->min_exits, shape->max_exits, mode, osm)
-                       : mode == DP_PLAN         ? dp_kernel_plan(shape->min_exits, shape->max_exits, osm)
-                                                 : dp_kernel_solve_smem(shape->min_exits, shape->max_exits, osm);
-    // the dynamic-smem ceiling is the per-CTA opt-in maximum minus the kernel's static smem
-    static std::mutex amu;
-    static std::map<const void *, size_t> static_smem;
-    size_t st_bytes = 0;
-    cudaError_t e = cudaSuccess;
-    {
-        std::lock_guard<std::mutex> lk(amu);
-        auto it = static_smem.find((const void *)kern);
-        if (it == static_smem.end()) {
-            cudaFuncAttributes fa;
-            e = cudaFuncGetAttributes(&fa, kern);
-            if (e != cudaSuccess) return e;
-            it = static_smem.emplace((const void *)kern, fa.sharedSizeBytes).first;
-        }
-        st_bytes = it->second;
-    }
-    const size_t dyn_max = (size_t)smem_per_cta_max - st_bytes;
+    dp_kernel_t kern = nullptr;
+    size_t dyn_max = 0;
+    cudaError_t e = resolve_dp(shape, mode, P, smem_per_cta_max, &kern, &dyn_max);
+    if (e != cudaSuccess) return e;
     if (need > dyn_max) return cudaErrorInvalidConfiguration;
     e = prepare(kern, dyn_max);
     if (e != cudaSuccess) return e;

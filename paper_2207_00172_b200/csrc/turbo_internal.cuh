@@ -140,14 +140,25 @@ cudaError_t launch_lookup(const turbo_profile_t *profiles, turbo_window_t *windo
 cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P, int num_sms, int smem_per_sm,
                       int smem_per_cta_max, cudaStream_t stream, DpLaunch *info);
 int dp_warps_per_window(const turbo_shape_t *shape);
+// host-only validation (no launch): the class kernel fits its shared memory / the long-window
+// kernel fits shared memory and the cooperative grid fits the device
+cudaError_t check_dp(const turbo_shape_t *shape, int mode, const DpParams &P, int smem_per_cta_max);
+cudaError_t check_dp_grid(const turbo_shape_t *shape, int mode, int num_sms, int smem_per_cta_max);
 
 // long-window (grid) kernel: scratch = flags (pub/con per CTA + misc) + halo ring
 constexpr int GRID_MAX_CTAS = 256;
 constexpr int GRID_RING_DEPTH = 8;
+// scratch = [flags: cleared by every launch][header: persists across launches][halo ring]
 __host__ __device__ constexpr int64_t grid_flags_words() { return 2 * GRID_MAX_CTAS + 64 + 16 * GRID_MAX_CTAS; }
+// header (64 B): {magic u64, tag epoch i32}. The ring's step tags continue from the epoch stored in the
+// workspace itself, so tags never repeat within a workspace -- also across CUDA-graph replays, whose
+// kernel arguments are frozen at capture (the kernel advances the epoch on the device).
+constexpr int64_t GRID_HEADER_WORDS = 16;
+constexpr unsigned long long GRID_MAGIC = 0x7475726230677264ull;   // "turb0grd"
 __host__ __device__ constexpr int64_t grid_scratch_bytes()
 {
-    return 4 * grid_flags_words() + 8 * (int64_t)GRID_RING_DEPTH * GRID_MAX_CTAS * TURBO_BIG_MAX_COST;
+    return 4 * (grid_flags_words() + GRID_HEADER_WORDS) +
+           8 * (int64_t)GRID_RING_DEPTH * GRID_MAX_CTAS * TURBO_BIG_MAX_COST;
 }
 cudaError_t launch_heuristic(const turbo_shape_t *shape, const turbo_window_t *windows, const int32_t *opt_gain,
                              const int32_t *opt_cost, int32_t *gain_out, int32_t *cost_out, uint8_t *feasible,

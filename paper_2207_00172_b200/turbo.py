@@ -63,9 +63,9 @@ WINDOW_DTYPE = np.dtype([("first_frame", "<i8"), ("first_option", "<i8"), ("choi
 assert WINDOW_DTYPE.itemsize == 48
 
 EXPORTS = ["turbo_mckp_workspace", "turbo_profile_lookup", "turbo_mckp_plan", "turbo_backtrack",
-           "turbo_mckp_solve", "turbo_mckp_solve_workspace", "turbo_schedule", "turbo_heuristic_plan", "turbo_stats",
+           "turbo_mckp_solve", "turbo_mckp_solve_workspace", "turbo_mckp_plane_bytes", "turbo_schedule", "turbo_heuristic_plan", "turbo_stats",
            "turbo_bucketize", "turbo_batches", "turbo_batched_plan",
-           "turbo_debug_set_variant", "turbo_debug_trace", "turbo_launch_count",
+           "turbo_debug_set_variant", "turbo_debug_trace", "turbo_debug_smem_stream", "turbo_launch_count",
            "turbo_status_string", "turbo_abi_version"]
 
 _lib = None
@@ -87,6 +87,7 @@ def load(path: Optional[str] = None):
     lib.turbo_backtrack.argtypes = [vp, vp, vp, vp, sz, vp, vp, vp, vp]
     lib.turbo_mckp_solve.argtypes = [vp, vp, vp, vp, vp, sz, vp, vp, vp, vp, vp, vp]
     lib.turbo_mckp_solve_workspace.argtypes = [vp, vp]
+    lib.turbo_mckp_plane_bytes.argtypes = [vp, vp, i32, vp]
     lib.turbo_stats.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.turbo_schedule.argtypes = [vp, vp, vp, vp, vp, i32, vp, sz, vp, vp, vp, vp, vp, vp, vp]
     lib.turbo_heuristic_plan.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
@@ -95,6 +96,7 @@ def load(path: Optional[str] = None):
     lib.turbo_batched_plan.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp]
     lib.turbo_debug_set_variant.argtypes = [i32]
     lib.turbo_debug_trace.argtypes = [vp, i64]
+    lib.turbo_debug_smem_stream.argtypes = [i32, i32, vp, vp, vp]
     lib.turbo_launch_count.argtypes = []
     lib.turbo_launch_count.restype = i64
     lib.turbo_status_string.restype = ctypes.c_char_p
@@ -163,6 +165,15 @@ def mckp_solve_workspace(shape) -> int:
     out = ctypes.c_size_t(0)
     _check("turbo_mckp_solve_workspace",
            load().turbo_mckp_solve_workspace(ctypes.addressof(shape), ctypes.addressof(out)))
+    return int(out.value)
+
+
+def mckp_plane_bytes(shape, windows_host: np.ndarray, fused: bool) -> int:
+    """Choice-plane bytes one call writes to HBM (turbo.h turbo_mckp_plane_bytes; host only)."""
+    out = ctypes.c_int64(0)
+    _check("turbo_mckp_plane_bytes",
+           load().turbo_mckp_plane_bytes(ctypes.addressof(shape), windows_host.ctypes.data, int(bool(fused)),
+                                         ctypes.addressof(out)))
     return int(out.value)
 
 
@@ -235,6 +246,16 @@ def stats(shape, windows_dev, class_id, exit_out, best_gain, best_cost, feasible
 
 def debug_set_variant(v: int):
     _check("turbo_debug_set_variant", load().turbo_debug_set_variant(int(v)))
+
+
+def smem_stream(iters: int, ctas_per_sm: int, sink, stream=None) -> float:
+    """Launch the shared-memory stream kernel (turbo.h turbo_debug_smem_stream); returns the bytes
+    it reads (the caller times the launch)."""
+    out = ctypes.c_double(0.0)
+    _check("turbo_debug_smem_stream",
+           load().turbo_debug_smem_stream(int(iters), int(ctas_per_sm), _ptr(sink), ctypes.addressof(out),
+                                          _stream(stream)))
+    return float(out.value)
 
 
 def launch_count() -> int:

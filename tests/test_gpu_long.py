@@ -20,7 +20,7 @@ def _lib():
     turbo.load()
 
 
-@pytest.mark.parametrize("fused", [True, False], ids=["solve", "plan+backtrack"])
+@pytest.mark.parametrize("fused", [True, False, "all"], ids=["solve", "plan+backtrack", "schedule"])
 def test_long_window_paper_profile(fused):
     wl = synth.make_long_window(3, N=120, K=6, B=40000)
     compare(wl, gpu_run(wl, fused), oracle_run(wl))
@@ -43,6 +43,49 @@ def test_mixed_batch_routes_small_and_long_windows():
     wl = synth.concat_workloads(parts)
     for fused in (True, False):
         compare(wl, gpu_run(wl, fused), oracle_run(wl))
+    # turbo_schedule: the long windows go to the grid kernel with a1/a2/a6 fused into it
+    compare(wl, gpu_run(wl, "all"), oracle_run(wl), check_options=False)
+
+
+@pytest.mark.parametrize("fused", [True, False, "all"], ids=["solve", "plan+backtrack", "schedule"])
+def test_long_windows_a1_edges(fused):
+    """a1 on long windows: clamped (budget 0), under-bound and exact-fit capacities."""
+    parts = [synth.make_long_window(40 + s, N=20 + 7 * s, K=4 + s, B=30000 + 999 * s, c_max=600, random_rows=True)
+             for s in range(6)]
+    wl = synth.with_budget_edges(synth.concat_workloads(parts), seed=3)
+    want = oracle_run(wl)
+    assert (want["budget"] < wl.budget).any()
+    compare(wl, gpu_run(wl, fused), want, check_options=fused != "all")
+
+
+@pytest.mark.parametrize("fused", [True, "all"], ids=["lookup+solve+stats", "schedule"])
+def test_graph_replay_with_changed_inputs(fused):
+    """A captured graph replayed with NEW class ids must plan the new inputs (the halo
+    ring tags continue on the device across replays, so a slot of an earlier replay is never taken
+    for the current one). Short long windows (N <= 2 x ring depth) are the exposed case."""
+    import dataclasses
+    import torch
+    from paper_2207_00172_b200 import turbo
+    parts = [synth.make_long_window(70 + s, N=6 + 3 * s, K=5, B=28000 + 500 * s, c_max=900, random_rows=True)
+             for s in range(4)]
+    wl = synth.concat_workloads(parts)
+    variants = [wl]
+    for v in range(1, 3):
+        rng = np.random.default_rng(v)
+        variants.append(dataclasses.replace(wl, class_id=rng.integers(0, 10, wl.total_frames).astype(np.uint8)))
+    b = turbo.batch_from_workload(wl)
+    turbo.run_path(b, fused=fused)               # warm-up (kernel attributes) before capture
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        turbo.run_path(b, fused=fused)
+    for rep in range(6):
+        cur = variants[rep % 3]
+        b.class_id[: cur.total_frames].copy_(torch.as_tensor(cur.class_id))
+        g.replay()
+        torch.cuda.synchronize()
+        got = turbo.results(b)
+        compare(cur, got, oracle_run(cur), check_options=fused != "all")
 
 
 def test_long_window_cost_above_halo_cap_is_rejected():
