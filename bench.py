@@ -86,29 +86,32 @@ def cpu_model() -> str:
 
 def measure_smem_peak(dev) -> dict:
     """The shared-memory roofline denominator, measured live on this GPU: the library's
-    conflict-free 32-bit LDS stream kernel (turbo_debug_smem_stream) on every SM, CUDA events,
-    best of 5 after warm-up, 1 and 2 CTAs (1024 threads) per SM."""
+    conflict-free LDS stream kernel (turbo_debug_smem_stream) on every SM, CUDA events, best of 5
+    after warm-up, 1 and 2 CTAs (1024 threads) per SM, 4/8/16-byte loads per lane. The peak is the
+    best over load widths (the most the pipe delivers); the 4-byte figure -- the DP's own access
+    type -- is reported beside it."""
     import torch
     from paper_2207_00172_b200 import turbo
     sink = torch.zeros(4096, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(dev)
-    best, best_cfg = 0.0, None
-    for ctas in (1, 2):
-        iters = 6000 // ctas
-        for _ in range(2):
-            turbo.smem_stream(iters, ctas, sink)
-        for _ in range(5):
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            nbytes = turbo.smem_stream(iters, ctas, sink)
-            e1.record(stream)
-            e1.synchronize()
-            gbs = nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9
-            if gbs > best:
-                best, best_cfg = gbs, ctas
-    return {"gbs": best, "ctas_per_sm": best_cfg,
-            "how": "turbo_debug_smem_stream: conflict-free ld.shared.u32 stream, 1024 threads x {1,2} CTAs per SM "
-                   "on every SM, CUDA events, best of 5 (burst)"}
+    rates = {}
+    for width in (4, 8, 16):
+        best = 0.0
+        for ctas in (1, 2):
+            iters = 24000 // (ctas * width)
+            for _ in range(2):
+                turbo.smem_stream(iters, ctas, sink, width)
+            for _ in range(5):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                nbytes = turbo.smem_stream(iters, ctas, sink, width)
+                e1.record(stream)
+                e1.synchronize()
+                best = max(best, nbytes / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+        rates[width] = best
+    return {"gbs": max(rates.values()), "gbs_by_bytes_per_lane": {str(k): v for k, v in rates.items()},
+            "how": "turbo_debug_smem_stream: conflict-free ld.shared stream (4/8/16 B per lane), 1024 threads x "
+                   "{1,2} CTAs per SM on every SM, CUDA events, best of 5 (burst); peak = best width"}
 
 
 def _vectors(wl) -> int:
@@ -463,6 +466,8 @@ def run_turbo(args):
         tbuild.build()
     turbo.load()
 
+    if args.variant:
+        turbo.debug_set_variant(args.variant)      # A/B runs only (turbo.h turbo_debug_set_variant)
     name = args.workload
     wl = make_workload(name, rank, ws, args.scaling)
     path = args.path
@@ -680,6 +685,8 @@ def run_turbo(args):
         "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
                      "frac": achieved / smem_peak, "traffic": traffic,
                      "peak_source": "measured live (" + smem_meas["how"] + ")",
+                     "peak_by_bytes_per_lane": smem_meas["gbs_by_bytes_per_lane"],
+                     "frac_of_lds32_stream": achieved / smem_meas["gbs_by_bytes_per_lane"]["4"],
                      "peak_derived": smem_derived, "frac_of_derived": achieved / smem_derived,
                      "kernel": ("turbo::dp_cta_kernel (" + {"schedule": "turbo_schedule", "solve": "turbo_mckp_solve",
                                                             "plan": "turbo_mckp_plan"}[path] + ")"
@@ -736,6 +743,7 @@ def main():
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="weak: per-GPU windows fixed (per_gpu of the workload); strong: the config's whole "
                          "window set split over the ranks by work (shard.py)")
+    ap.add_argument("--variant", type=int, default=0, help="kernel-variant debug switch (A/B runs; 0 = automatic)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()

@@ -306,7 +306,8 @@ turbo_status_t turbo_batched_plan(const turbo_shape_t *shape /* host */, const t
 
 /* Debug / test hook: force a DP kernel variant. variant & 3: 0 = automatic, 1 = fused solve
  * keeps choice planes in shared memory (when they fit the per-CTA maximum), 2 = in HBM;
- * variant & 4: do not stage option tables in shared memory (shuffle broadcast instead).
+ * variant & 4: do not stage option tables in shared memory (shuffle broadcast instead);
+ * variant & 8: never use the lockstep multi-window kernel (one CTA per window instead).
  * Returns INVALID_ARG for other values. Process-wide; not needed in production. */
 turbo_status_t turbo_debug_set_variant(int32_t variant);
 
@@ -319,11 +320,11 @@ turbo_status_t turbo_debug_set_variant(int32_t variant);
 turbo_status_t turbo_debug_trace(int64_t *trace, int64_t words);
 /* Measurement hook (not a step of the method): the shared-memory roofline denominator. Launches
  * ctas_per_sm (1 or 2) x SMs CTAs of 1024 threads, each thread issuing iters x 32 conflict-free
- * 32-bit shared loads (one 128-B wavefront per warp instruction, the DP's access type);
- * *bytes_out (host) = bytes the launch reads. The caller times the launch (CUDA events) and
- * divides. sink: device, >= 4 KB, never meaningfully written. */
-turbo_status_t turbo_debug_smem_stream(int32_t iters, int32_t ctas_per_sm, void *sink, double *bytes_out,
-                                       turbo_stream_t stream);
+ * shared loads of bytes_per_lane (4, 8 or 16) bytes (4: one 128-B wavefront per warp instruction,
+ * the DP's access type); *bytes_out (host) = bytes the launch reads. The caller times the launch
+ * (CUDA events) and divides. sink: device, >= 4 KB, never meaningfully written. */
+turbo_status_t turbo_debug_smem_stream(int32_t iters, int32_t ctas_per_sm, int32_t bytes_per_lane, void *sink,
+                                       double *bytes_out, turbo_stream_t stream);
 /* Kernels this library has launched so far in the process (all threads and devices; graph
  * capture counts the captured launches once). Lets a caller count the kernels of a call. */
 int64_t turbo_launch_count(void);

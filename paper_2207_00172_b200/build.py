@@ -49,10 +49,25 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     srcs = sources()
     objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in srcs]
-    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
-        results = list(ex.map(_compile, srcs, objs))
+    # incremental: an object is rebuilt when its source, any header, or the build flags changed
+    headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h")) + [__file__]
+    t_hdr = max(os.path.getmtime(h) for h in headers)
+    stamp = os.path.join(objdir, ".flags")
+    flags = " ".join(NVCC_FLAGS) + (" -DTURBO_TRACE" if os.environ.get("TURBO_TRACE") else "")
+    same_flags = os.path.exists(stamp) and open(stamp).read() == flags
+    todo = [i for i, (s, o) in enumerate(zip(srcs, objs))
+            if force or not same_flags or not os.path.exists(o)
+            or os.path.getmtime(o) < max(os.path.getmtime(s), t_hdr)]
+    with ThreadPoolExecutor(max_workers=max(1, min(len(todo) or 1, os.cpu_count() or 1))) as ex:
+        done = list(ex.map(_compile, [srcs[i] for i in todo], [objs[i] for i in todo]))
+    with open(stamp, "w") as f:
+        f.write(flags)
+    results = {i: r for i, r in zip(todo, done)}
     log = []
-    for s, r in zip(srcs, results):
+    for i, s in enumerate(srcs):
+        if i not in results:
+            continue
+        r = results[i]
         log.append(f"==== {os.path.basename(s)}\n{r.stdout}{r.stderr}")
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
@@ -62,7 +77,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if link.returncode != 0:
         sys.stderr.write(link.stdout + link.stderr)
         raise RuntimeError("nvcc link of libturbo.so failed")
-    with open(os.path.join(PKG, "ptxas.log"), "w") as f:
+    with open(os.path.join(PKG, "ptxas.log"), "a" if len(todo) < len(srcs) else "w") as f:
         f.write("\n".join(log))
     if verbose:
         sys.stderr.write("\n".join(log))

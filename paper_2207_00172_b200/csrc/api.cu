@@ -146,7 +146,7 @@ turbo_status_t turbo_debug_trace(int64_t *trace, int64_t words)
 
 turbo_status_t turbo_debug_set_variant(int32_t variant)
 {
-    if (variant < 0 || variant > 6 || (variant & 3) == 3) return TURBO_ERR_INVALID_ARG;
+    if (variant < 0 || variant > 14 || (variant & 3) == 3) return TURBO_ERR_INVALID_ARG;
     g_variant = variant;
     return TURBO_OK;
 }
@@ -365,6 +365,7 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int kind, const DpParam
             P.cst_words += 2 * P.prof_entries + 2 * ((shapes[c].max_frames + 3) / 4);
         }
         P.cls = c;
+        P.max_frames = shapes[c].max_frames;
         P.cls_count = shape->cls_count[c];
         // the serving order is followed by the mixed-K kernels; fixed-K kernels go in index order
         P.ordered = (shape->ordered && !dp_kernel_fixed_k(shapes[c].min_exits, shapes[c].max_exits)) ? 1 : 0;
@@ -395,6 +396,15 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int kind, const DpParam
     if (n_cls <= 1) {
         for (int c = 0; c < TURBO_NUM_CLASSES && e == cudaSuccess; ++c)
             if (shape->cls_count[c]) {
+                // one class of short rows, planes in shared memory, many windows per SM: the lockstep
+                // kernel (V windows per CTA, one barrier per frame for all of them)
+                int pv, pt, pw;
+                size_t ps;
+                if (modes[c] == DP_SOLVE_SMEM && shape->num_big == 0 && !(g_variant & 8) &&
+                    pack_geometry(&shapes[c], Ps[c], d.num_sms, d.smem_per_cta_optin, &pv, &pt, &pw, &ps)) {
+                    e = launch_pack(&shapes[c], Ps[c], d.num_sms, d.smem_per_cta_optin, (cudaStream_t)stream);
+                    continue;
+                }
                 e = launch_dp(&shapes[c], modes[c], Ps[c], d.num_sms, d.smem_per_sm, d.smem_per_cta_optin,
                               (cudaStream_t)stream, &info);
                 if (e == cudaSuccess) e = launch_walk(c, (cudaStream_t)stream);

@@ -97,6 +97,11 @@ struct DpParams {
     int64_t *stats;
     int64_t *trace;                // debug: per-CTA phase timestamps (turbo_debug_trace)
     int64_t trace_words;
+    // lockstep kernel (dp_pack.cu): windows per CTA, tiles per window, words per window slot
+    int32_t max_frames;
+    int32_t pack_v;
+    int32_t pack_tiles;
+    int32_t pack_stride;
 };
 
 // turbo_debug_trace: %globaltimer at phase p of window w (thread 0 of the window's CTA). Compiled
@@ -168,6 +173,11 @@ cudaError_t launch_bucketize(const float *theta, int64_t n, int32_t C, float inv
                              cudaStream_t stream);
 cudaError_t launch_batches(const turbo_window_t *windows, int32_t num_windows, const uint8_t *exit_out,
                            int32_t *count, int32_t *order, int num_sms, cudaStream_t stream);
+// lockstep multi-window kernel for short-row single-class batches (dp_pack.cu)
+bool pack_geometry(const turbo_shape_t *s, const DpParams &P, int num_sms, int smem_per_cta_max, int *V_out,
+                   int *T_out, int *warps_out, size_t *smem_out);
+cudaError_t launch_pack(const turbo_shape_t *s, const DpParams &P, int num_sms, int smem_per_cta_max,
+                        cudaStream_t stream);
 cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams &P, int num_sms,
                            int smem_per_cta_max, cudaStream_t stream);
 size_t dp_smem_bytes(const DpParams &P, int nwarps);

@@ -96,7 +96,7 @@ def load(path: Optional[str] = None):
     lib.turbo_batched_plan.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp]
     lib.turbo_debug_set_variant.argtypes = [i32]
     lib.turbo_debug_trace.argtypes = [vp, i64]
-    lib.turbo_debug_smem_stream.argtypes = [i32, i32, vp, vp, vp]
+    lib.turbo_debug_smem_stream.argtypes = [i32, i32, i32, vp, vp, vp]
     lib.turbo_launch_count.argtypes = []
     lib.turbo_launch_count.restype = i64
     lib.turbo_status_string.restype = ctypes.c_char_p
@@ -248,13 +248,13 @@ def debug_set_variant(v: int):
     _check("turbo_debug_set_variant", load().turbo_debug_set_variant(int(v)))
 
 
-def smem_stream(iters: int, ctas_per_sm: int, sink, stream=None) -> float:
+def smem_stream(iters: int, ctas_per_sm: int, sink, bytes_per_lane: int = 4, stream=None) -> float:
     """Launch the shared-memory stream kernel (turbo.h turbo_debug_smem_stream); returns the bytes
     it reads (the caller times the launch)."""
     out = ctypes.c_double(0.0)
     _check("turbo_debug_smem_stream",
-           load().turbo_debug_smem_stream(int(iters), int(ctas_per_sm), _ptr(sink), ctypes.addressof(out),
-                                          _stream(stream)))
+           load().turbo_debug_smem_stream(int(iters), int(ctas_per_sm), int(bytes_per_lane), _ptr(sink),
+                                          ctypes.addressof(out), _stream(stream)))
     return float(out.value)
 
 

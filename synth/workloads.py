@@ -202,14 +202,16 @@ def make_config(k: int, window_offset: int = 0, num_windows: Optional[int] = Non
 # ----------------------------------------------------------------------------- parity sets
 def make_tie_heavy(seed: int, W: int, max_frames: int = 8, max_exits: int = 4,
                    num_profiles: int = 16, max_budget: Optional[int] = None,
-                   C: int = NUM_CLASSES, base_cost: int = 3) -> Workload:
-    """Gains U{-2..8}, costs U{0..4}; 30% of profiles have c_0 > 0 (infeasible windows)."""
+                   C: int = NUM_CLASSES, base_cost: int = 3, fixed_exits: Optional[int] = None,
+                   max_cost: int = 4) -> Workload:
+    """Gains U{-2..8}, costs U{0..max_cost}; 30% of profiles have c_0 > 0 (infeasible windows).
+    fixed_exits: every profile has that K (else K ~ U{2..max_exits} per profile)."""
     gains, costs, shapes = [], [], []
     for p in range(num_profiles):
-        K = int(rand_int(seed, S_PROF, p, 2, max_exits))
+        K = int(rand_int(seed, S_PROF, p, 2, max_exits)) if fixed_exits is None else int(fixed_exits)
         n = C * K
         g = rand_int(seed, S_TGAIN, p * 4096 + np.arange(n), -2, 8).astype(np.int32)
-        c = rand_int(seed, S_TCOST, p * 4096 + np.arange(n), 0, 4).astype(np.int32)
+        c = rand_int(seed, S_TCOST, p * 4096 + np.arange(n), 0, max_cost).astype(np.int32)
         if rand_uniform(seed, S_TBASE, p) >= 0.3:
             c.reshape(C, K)[:, 0] = 0
         gains.append(g)

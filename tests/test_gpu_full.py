@@ -119,3 +119,41 @@ def test_device_budget_above_bound_rejected():
         want = oracle_run(wl, budgets=bud)
         for k in ("best_gain", "best_cost", "feasible"):
             np.testing.assert_array_equal(got[k][keep].astype(np.int64), want[k][keep].astype(np.int64))
+
+
+# ---------------------------------------------------------------------------------------------
+# The lockstep multi-window kernel (dp_pack.cu) serves single-class fixed-K batches with >= 2
+# windows per SM (c2). These sets give it windows of DIFFERENT N and B inside one CTA, tie-heavy
+# rows, infeasible windows, clamped budgets and bad class ids; variant 8 forces the one-window-
+# per-CTA kernel on the same inputs.
+PACK_K = [4, 5, 6, 8]
+
+
+def _pack_set(K, seed):
+    """Budget bounds in [256, 1000] keep every window in one row-size class (the kernel's domain);
+    the a1 edges then lower (or clamp) the device budgets below those bounds."""
+    wl = synth.make_tie_heavy(seed=seed, W=1500, max_frames=40, max_exits=K, fixed_exits=K, max_budget=1000,
+                              max_cost=150)
+    wl.budget = (256 + wl.budget.astype(np.int64) % 745).astype(np.int32)
+    wl.capacity = (wl.budget.astype(np.int64) + wl.num_frames.astype(np.int64) * wl.base_cost).astype(np.int32)
+    return synth.with_budget_edges(wl, seed=seed + 1)
+
+
+@pytest.mark.parametrize("K", PACK_K)
+@pytest.mark.parametrize("fused", ["all", True], ids=["schedule", "solve"])
+def test_lockstep_kernel_mixed_windows(K, fused):
+    wl = _pack_set(K, 500 + K)
+    want = oracle_run(wl)
+    compare(wl, gpu_run(wl, fused, 0), want, check_options=fused != "all")
+    compare(wl, gpu_run(wl, fused, 8), want, check_options=fused != "all")
+
+
+def test_lockstep_kernel_bad_class_and_range():
+    wl = _pack_set(5, 77)
+    wl.class_id[1234] = 200
+    wl.class_id[99] = 10
+    a = gpu_run(wl, "all", 0)
+    c = gpu_run(wl, "all", 8)
+    assert int(a["status"][0]) == 99 and int(c["status"][0]) == 99
+    for k in ("exits", "best_gain", "best_cost", "feasible", "stats", "budget"):
+        np.testing.assert_array_equal(a[k], c[k])

@@ -23,7 +23,7 @@ def _lib():
 @pytest.mark.parametrize("fused", [True, False, "all"], ids=["solve", "plan+backtrack", "schedule"])
 def test_long_window_paper_profile(fused):
     wl = synth.make_long_window(3, N=120, K=6, B=40000)
-    compare(wl, gpu_run(wl, fused), oracle_run(wl))
+    compare(wl, gpu_run(wl, fused), oracle_run(wl), check_options=fused != "all")
 
 
 @pytest.mark.parametrize("K", [2, 3, 4, 5, 6, 7, 8, 11, 16])
