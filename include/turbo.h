@@ -307,7 +307,8 @@ turbo_status_t turbo_batched_plan(const turbo_shape_t *shape /* host */, const t
 /* Debug / test hook: force a DP kernel variant. variant & 3: 0 = automatic, 1 = fused solve
  * keeps choice planes in shared memory (when they fit the per-CTA maximum), 2 = in HBM;
  * variant & 4: do not stage option tables in shared memory (shuffle broadcast instead);
- * variant & 8: never use the lockstep multi-window kernel (one CTA per window instead).
+ * variant & 8: use the lockstep multi-window kernel (dp_pack.cu; V windows per CTA) for
+ * single-class short-row batches instead of one CTA per window.
  * Returns INVALID_ARG for other values. Process-wide; not needed in production. */
 turbo_status_t turbo_debug_set_variant(int32_t variant);
 

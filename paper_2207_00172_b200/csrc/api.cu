@@ -396,11 +396,12 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int kind, const DpParam
     if (n_cls <= 1) {
         for (int c = 0; c < TURBO_NUM_CLASSES && e == cudaSuccess; ++c)
             if (shape->cls_count[c]) {
-                // one class of short rows, planes in shared memory, many windows per SM: the lockstep
-                // kernel (V windows per CTA, one barrier per frame for all of them)
+                // opt-in (variant & 8): the lockstep kernel (V windows per CTA, one barrier per frame
+                // for all of them). Measured slower on c2 (42.7 vs 37.2 us): the shared
+                // per-frame barrier drains and refills the whole SM's shared-memory pipe every frame
                 int pv, pt, pw;
                 size_t ps;
-                if (modes[c] == DP_SOLVE_SMEM && shape->num_big == 0 && !(g_variant & 8) &&
+                if (modes[c] == DP_SOLVE_SMEM && shape->num_big == 0 && (g_variant & 8) &&
                     pack_geometry(&shapes[c], Ps[c], d.num_sms, d.smem_per_cta_optin, &pv, &pt, &pw, &ps)) {
                     e = launch_pack(&shapes[c], Ps[c], d.num_sms, d.smem_per_cta_optin, (cudaStream_t)stream);
                     continue;

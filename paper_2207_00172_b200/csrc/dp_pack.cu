@@ -170,36 +170,107 @@ __global__ void __launch_bounds__(1024, 1) dp_pack_kernel(DpParams P)
     int32_t own[RPT];
 #pragma unroll
     for (int r = 0; r < RPT; ++r) own[r] = 0;
-    for (int32_t f = 0; f < maxN; ++f) {
-        bool first = true;
-        for (int q = warp; q < nq; q += nwarps) {
-            const int v = q / T, t = q - (q / T) * T;
-            const int32_t i = ws[v].N - 1 - f;
-            const int32_t nt = ws[v].ntiles;
-            if (i >= 0 && t < nt) {
-                const int2 *o = opts(v) + i * K;
+    if (nq <= nwarps) {
+        // one task per warp (the launch shape makes this the normal case): the task's addresses are
+        // fixed for the whole window, the next frame's options are loaded before the barrier
+        const int v = warp / T, t = warp - (warp / T) * T;
+        const bool has = warp < nq && !ws[v].bad && t < ws[v].ntiles;
+        const int32_t N = has ? ws[v].N : 0;
+        const int32_t nt = has ? ws[v].ntiles : 1;
+        const int32_t b_lo = t * RPT * 32;
+        int32_t *const ra = rowA(has ? v : 0), *const rb = rowB(has ? v : 0);
+        const int2 *const ov = opts(has ? v : 0);
+        uint32_t *pl = planes(has ? v : 0) + ((int64_t)(N > 0 ? N - 1 : 0) * nt + t) * 32 + lane;
+        int2 on[K];
+        if (N > 0) {
+#pragma unroll
+            for (int k = 0; k < K; ++k) on[k] = ov[(N - 1) * K + k];
+        }
+        for (int32_t f = 0; f < maxN; ++f) {
+            if (f < N) {
                 int32_t gp[K], cc[K];
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
-                    const int2 x = o[k];
-                    gp[k] = x.x;
-                    cc[k] = x.y;
+                    gp[k] = on[k].x;
+                    cc[k] = on[k].y;
+                }
+                if (f + 1 < N) {                             // frame i - 1's options, used after the barrier
+#pragma unroll
+                    for (int k = 0; k < K; ++k) on[k] = ov[(N - 2 - f) * K + k];
                 }
                 int32_t cmax = cc[0];
 #pragma unroll
                 for (int k = 1; k < K; ++k) cmax = max(cmax, cc[k]);
-                const int32_t *cur = (f & 1) ? rowB(v) : rowA(v);
-                int32_t *nxt = (f & 1) ? rowA(v) : rowB(v);
-                if (first)
-                    dp_tile<K, DP_SOLVE_SMEM, true>(P, t, i, nt * RPT, nt, 0, cur, nxt, planes(v), nullptr, gp, cc,
-                                                    cmax, false, lane, own);
-                else
-                    dp_tile<K, DP_SOLVE_SMEM, false>(P, t, i, nt * RPT, nt, 0, cur, nxt, planes(v), nullptr, gp, cc,
-                                                     cmax, false, lane, own);
+                const int32_t *cur = (f & 1) ? rb : ra;
+                int32_t *nxt = (f & 1) ? ra : rb;
+                int32_t key[RPT];
+                if (cmax <= b_lo + pad) {                    // every shift inside the -inf pad
+                    const int32_t *src = cur + b_lo + lane;
+                    if (cc[0] == 0) {
+#pragma unroll
+                        for (int r = 0; r < RPT; ++r) key[r] = own[r] + gp[0];
+                    } else {
+#pragma unroll
+                        for (int r = 0; r < RPT; ++r) key[r] = src[r * 32 - cc[0]] + gp[0];
+                    }
+#pragma unroll
+                    for (int k = 1; k < K; ++k) {
+                        const int32_t *s = src - cc[k];
+#pragma unroll
+                        for (int r = 0; r < RPT; ++r) key[r] = max_plus(s[r * 32], gp[k], key[r]);
+                    }
+                } else {
+                    tile_keys<K, RPT>(cur, b_lo, RPT, pad, gp, cc, lane, key);
+                }
+                int32_t *dst = nxt + b_lo + lane;
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) {
+                    const int32_t x = key[r] & ~15;
+                    own[r] = x;
+                    dst[r * 32] = x;
+                }
+                *pl = pack_choices<RPT, CB>(key);
+                pl -= nt * 32;
             }
-            first = false;
+            __syncthreads();                                 // frame f of every window visible
         }
-        __syncthreads();                                     // frame f of every window visible
+    } else {
+        for (int32_t f = 0; f < maxN; ++f) {
+            bool first = true;
+            int v = warp / T, t = warp - (warp / T) * T;
+            for (int q = warp; q < nq; q += nwarps) {
+                const int32_t i = ws[v].N - 1 - f;
+                const int32_t nt = ws[v].ntiles;
+                if (i >= 0 && t < nt && !ws[v].bad) {
+                    const int2 *o = opts(v) + i * K;
+                    int32_t gp[K], cc[K];
+#pragma unroll
+                    for (int k = 0; k < K; ++k) {
+                        const int2 x = o[k];
+                        gp[k] = x.x;
+                        cc[k] = x.y;
+                    }
+                    int32_t cmax = cc[0];
+#pragma unroll
+                    for (int k = 1; k < K; ++k) cmax = max(cmax, cc[k]);
+                    const int32_t *cur = (f & 1) ? rowB(v) : rowA(v);
+                    int32_t *nxt = (f & 1) ? rowA(v) : rowB(v);
+                    if (first)
+                        dp_tile<K, DP_SOLVE_SMEM, true>(P, t, i, nt * RPT, nt, 0, cur, nxt, planes(v), nullptr, gp,
+                                                        cc, cmax, false, lane, own);
+                    else
+                        dp_tile<K, DP_SOLVE_SMEM, false>(P, t, i, nt * RPT, nt, 0, cur, nxt, planes(v), nullptr, gp,
+                                                         cc, cmax, false, lane, own);
+                }
+                first = false;
+                t += nwarps;                                 // next task: q + nwarps
+                while (t >= T) {
+                    t -= T;
+                    ++v;
+                }
+            }
+            __syncthreads();                                 // frame f of every window visible
+        }
     }
 
     // ---- a4 / a5 / a6: warp v finishes window v (the pipe is idle now: walks run at latency)

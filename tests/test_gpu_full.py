@@ -123,9 +123,9 @@ def test_device_budget_above_bound_rejected():
 
 # ---------------------------------------------------------------------------------------------
 # The lockstep multi-window kernel (dp_pack.cu) serves single-class fixed-K batches with >= 2
-# windows per SM (c2). These sets give it windows of DIFFERENT N and B inside one CTA, tie-heavy
-# rows, infeasible windows, clamped budgets and bad class ids; variant 8 forces the one-window-
-# per-CTA kernel on the same inputs.
+# windows per SM when variant bit 8 is set (opt-in). These sets give it windows of DIFFERENT N and B
+# inside one CTA, tie-heavy rows, infeasible windows, clamped budgets and bad class ids; variant 0
+# runs the one-window-per-CTA kernel on the same inputs.
 PACK_K = [4, 5, 6, 8]
 
 
