@@ -146,7 +146,7 @@ turbo_status_t turbo_debug_trace(int64_t *trace, int64_t words)
 
 turbo_status_t turbo_debug_set_variant(int32_t variant)
 {
-    if (variant < 0 || variant > 14 || (variant & 3) == 3) return TURBO_ERR_INVALID_ARG;
+    if (variant < 0 || variant > 63 || (variant & 3) == 3) return TURBO_ERR_INVALID_ARG;
     g_variant = variant;
     return TURBO_OK;
 }
@@ -366,6 +366,11 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int kind, const DpParam
         }
         P.cls = c;
         P.max_frames = shapes[c].max_frames;
+        // mixed-K plan-mode launches of the short-row classes run the runtime-K body (several CTAs
+        // of different K per SM would thrash the instruction cache with fifteen unrolled bodies);
+        // the longest rows (one CTA per SM) keep the K-specific bodies
+        P.generic = (modes[c] == DP_PLAN && !dp_kernel_fixed_k(shapes[c].min_exits, shapes[c].max_exits) &&
+                     (c < TURBO_NUM_CLASSES - 1 || (g_variant & 16)) && !(g_variant & 32)) ? 1 : 0;
         P.cls_count = shape->cls_count[c];
         // the serving order is followed by the mixed-K kernels; fixed-K kernels go in index order
         P.ordered = (shape->ordered && !dp_kernel_fixed_k(shapes[c].min_exits, shapes[c].max_exits)) ? 1 : 0;

@@ -773,6 +773,201 @@ __device__ __noinline__ void dp_window_call(const DpParams &P, int64_t w, int32_
     dp_window<K, MODE, OSM, FUSE>(P, w, rowA, rowB, sch, cst, opt_s, red, hist, warp, nwarps, lane);
 }
 
+// Generic-K body of the mixed-K kernel in plan mode (choice planes to HBM; the walk runs in its own
+// kernel). K is a runtime value: ONE body per choice width (CB = 2 for K <= 4, 4 otherwise) instead
+// of fifteen unrolled ones. Measured on c5: with windows of 15 different K sharing an SM, the
+// per-K bodies thrash the instruction cache (ncu: 37 "no instruction" stalls per issued
+// instruction in the short-row launch) -- these windows are latency-bound, so the option loop
+// that is not unrolled costs nothing there. Same recurrence, packed keys and outputs as dp_window.
+template <int CB, bool OSM, bool FUSE>
+__device__ __noinline__ void dp_window_gen(const DpParams &P, int64_t w, const int K, int32_t *__restrict__ rowA,
+                                           int32_t *__restrict__ rowB, int2 *__restrict__ opt_s,
+                                           int64_t *__restrict__ red, int warp, int nwarps, int lane)
+{
+    constexpr int RPT = 32 / CB;
+    const bool inplace = (nwarps == 1);
+    const int tid = warp * 32 + lane;
+    const int nthr = nwarps * 32;
+    const turbo_window_t *win = P.windows + w;
+    const int64_t ff = win->first_frame;
+    const int64_t fo = win->first_option;
+    const int32_t N = win->num_frames;
+    int32_t B = win->budget;
+    const int32_t Bb = win->budget_bound;
+    const int32_t *__restrict__ og = P.opt_gain + fo;
+    const int32_t *__restrict__ oc = P.opt_cost + fo;
+    int32_t prof_C = 0;
+    const int32_t *prof_g = nullptr, *prof_c = nullptr;
+    if (FUSE) {
+        const turbo_profile_t *prof = P.profiles + win->profile;
+        prof_C = prof->num_classes;
+        prof_g = prof->gain;
+        prof_c = prof->cost;
+        if (P.capacity != nullptr) {     // a1 (reading R3): B_w = max(0, capacity_w - m_w u0)
+            const int64_t b = (int64_t)P.capacity[w] - (int64_t)N * (int64_t)P.base_cost;
+            B = (int32_t)(b < 0 ? 0 : (b > 0x7fffffffll ? 0x7fffffff : b));
+            if (tid == 0) P.windows_rw[w].budget = B;
+        }
+    }
+    auto load_opt = [&](int32_t i, int32_t k, int32_t &g, int32_t &c) {
+        if (FUSE) {                      // a2: the profile row of the frame's class (zero row for >= C)
+            const int32_t cls = P.class_id[ff + i];
+            g = cls < prof_C ? __ldg(prof_g + cls * K + k) : 0;
+            c = cls < prof_C ? __ldg(prof_c + cls * K + k) : 0;
+        } else {
+            g = __ldg(og + (int64_t)i * K + k);
+            c = __ldg(oc + (int64_t)i * K + k);
+        }
+    };
+    // ---- prologue: stage options (OSM), validate, sums for the infeasible report (reading R8)
+    bool bad = (B < 0) || (B > Bb);
+    if (OSM) {
+        for (int32_t o = tid; o < N * K; o += nthr) {
+            const int32_t i = o / K, k = o - (o / K) * K;
+            int32_t g, c;
+            load_opt(i, k, g, c);
+            bad |= (c < 0) || (c >= (1 << 30)) || (g > (1 << 24)) || (g < -(1 << 24));
+            opt_s[o] = make_int2((g << 4) | (15 - k), c);
+        }
+        bad = nwarps > 1 ? __syncthreads_or(bad) : __any_sync(0xffffffffu, bad);
+    }
+    if (warp == 0) {
+        int64_t abs_sum = 0, g0_sum = 0, c0_sum = 0;
+        for (int32_t i = lane; i < N; i += 32) {
+            int32_t m = 0;
+            if (FUSE && (int32_t)P.class_id[ff + i] >= prof_C) atomic_min_i64(&P.status[0], ff + i);
+            for (int k = 0; k < K; ++k) {
+                int32_t g, c;
+                if (OSM) {
+                    const int2 v = opt_s[i * K + k];
+                    g = v.x >> 4;
+                    c = v.y;
+                } else {
+                    load_opt(i, k, g, c);
+                    bad |= (c < 0) || (c >= (1 << 30)) || (g > (1 << 24)) || (g < -(1 << 24));
+                }
+                m = max(m, g < 0 ? -g : g);
+                if (k == 0) {
+                    g0_sum += g;
+                    c0_sum += c;
+                }
+            }
+            abs_sum += m;
+        }
+        abs_sum = warp_sum_i64(abs_sum);
+        g0_sum = warp_sum_i64(g0_sum);
+        c0_sum = warp_sum_i64(c0_sum);
+        bad = __any_sync(0xffffffffu, bad) || abs_sum >= GAIN_RANGE_LIMIT || c0_sum >= 0x7fffffffll;
+        if (lane == 0) {
+            red[0] = bad ? 1 : 0;
+            red[1] = g0_sum;
+            red[2] = c0_sum;
+            red[3] = 0;
+        }
+    }
+    const int32_t ntiles = (((B + 32) >> 5) + RPT - 1) / RPT;
+    const int32_t nrows = ntiles * RPT;
+    for (int32_t x = tid; x < nrows * 32; x += nthr) rowA[x] = 0;          // S_N = 0
+    if (nwarps > 1) __syncthreads(); else __syncwarp();
+    if (red[0]) {
+        if (tid == 0) {
+            P.best_gain[w] = 0;
+            P.best_cost[w] = 0;
+            P.feasible[w] = 0;
+            atomic_min_i64(&P.status[1], w);
+        }
+        return;
+    }
+    const int32_t gtiles = (int32_t)(((Bb + 32) >> 5) + RPT - 1) / RPT;
+    uint32_t *__restrict__ gch = reinterpret_cast<uint32_t *>(P.workspace + win->choice_offset);
+    // !OSM: lane q K + k holds option k of the q-th frame of a chunk of CH = 32 / K frames, the next
+    // chunk loaded while this one is consumed (as dp_window)
+    const int CH = 32 / K;
+    const int lq = lane / K, lk = lane - (lane / K) * K;
+    int32_t a_gp = 0, a_c = 0, b_g = 0, b_c = 0;
+    auto load_raw = [&](int32_t hi, int32_t &g, int32_t &c) {
+        const int32_t i = hi - lq;
+        g = 0;
+        c = 0;
+        if (lq < CH && i >= 0) load_opt(i, lk, g, c);
+    };
+    if (!OSM && N > 0) {
+        int32_t g, c;
+        load_raw(N - 1, g, c);
+        a_gp = (g << 4) | (15 - lk);
+        a_c = c;
+        load_raw(N - 1 - CH, b_g, b_c);
+    }
+    int32_t *__restrict__ cur = rowA;
+    int32_t *__restrict__ nxt = inplace ? rowA : rowB;
+    const int32_t t0 = inplace ? ntiles - 1 : warp;
+    const int32_t dt = inplace ? -1 : nwarps;
+    const int32_t pad = P.pad_words;
+    for (int32_t i = N - 1; i >= 0; --i) {
+        const int32_t f = N - 1 - i;
+        const int q = f % CH;
+        if (!OSM && q == 0 && f > 0) {
+            a_gp = (b_g << 4) | (15 - lk);
+            a_c = b_c;
+            load_raw(i - CH, b_g, b_c);
+        }
+        for (int32_t t = t0; t >= 0 && t < ntiles; t += dt) {
+            const int32_t b_lo = t * RPT * 32;
+            int32_t key[RPT];
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) key[r] = NEG_R;
+            for (int k = 0; k < K; ++k) {
+                int32_t g, c;
+                if (OSM) {
+                    const int2 v = opt_s[i * K + k];
+                    g = v.x;
+                    c = v.y;
+                } else {
+                    g = __shfl_sync(0xffffffffu, a_gp, q * K + k);
+                    c = __shfl_sync(0xffffffffu, a_c, q * K + k);
+                }
+                if (c <= b_lo + pad) {
+                    const int32_t *__restrict__ s = cur + (b_lo + lane - c);
+#pragma unroll
+                    for (int r = 0; r < RPT; ++r) key[r] = max_plus(s[r * 32], g, key[r]);
+                } else if (c < b_lo + RPT * 32) {
+#pragma unroll
+                    for (int r = 0; r < RPT; ++r) {
+                        const int32_t idx = b_lo + r * 32 + lane - c;
+                        const int32_t v = idx < 0 ? NEG_R : cur[idx < 0 ? 0 : idx];
+                        key[r] = max_plus(v, g, key[r]);
+                    }
+                }
+            }
+            if (inplace) __syncwarp();                      // all reads of this tile done
+            int32_t *__restrict__ dst = nxt + b_lo + lane;
+#pragma unroll
+            for (int r = 0; r < RPT; ++r) dst[r * 32] = key[r] & ~15;
+            gch[((int64_t)i * gtiles + t) * 32 + lane] = pack_choices<RPT, CB>(key);
+        }
+        if (nwarps > 1) __syncthreads(); else __syncwarp();
+        int32_t *tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+    }
+    // ---- a4: G* = S_0[B], C* = #{b <= B : S_0[b] < G*}
+    const int32_t RB = cur[B];
+    const bool feas = RB > VALID_MIN_R;
+    int32_t cnt = 0;
+    for (int32_t b = tid; b <= B; b += nthr) cnt += cur[b] < RB ? 1 : 0;
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (nwarps > 1) {
+        if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(&red[3]), (unsigned long long)cnt);
+        __syncthreads();
+        cnt = (int32_t)red[3];
+    }
+    if (tid == 0) {
+        P.best_gain[w] = feas ? (RB >> 4) : (int32_t)red[1];
+        P.best_cost[w] = feas ? cnt : (int32_t)red[2];
+        P.feasible[w] = feas ? 1 : 0;
+    }
+}
+
 // smem layout per CTA: [red: 8 x int64][pad][rowA][pad][rowB (G > 1)][options (OSM) | costs]
 // [choice planes (solve smem)]. The pads (pad_words of -inf below each row buffer) are written
 // once and never overwritten.
@@ -806,6 +1001,15 @@ __global__ void __launch_bounds__(512, (KSEL == 0) ? 1 : 2) dp_cta_kernel(DpPara
         // memory, which is fine here -- the out-of-line bodies take it as a parameter anyway
         for (int64_t r = blockIdx.x; r < P.cls_count; r += gridDim.x) {
             const int64_t w = P.windows[P.cls_first + r].order;
+            if (MODE == DP_PLAN && P.generic) {
+                const int K = P.windows[w].num_exits;
+                if (K <= 4)
+                    dp_window_gen<2, OSM, FUSE>(P, w, K, rowA, rowB, opt_s, red, warp, nwarps, lane);
+                else
+                    dp_window_gen<4, OSM, FUSE>(P, w, K, rowA, rowB, opt_s, red, warp, nwarps, lane);
+                __syncthreads();
+                continue;
+            }
             switch (P.windows[w].num_exits) {
 #define TURBO_K_CASE(KK) \
     case KK: dp_window_call<KK, MODE, OSM, FUSE>(P, w, rowA, rowB, sch, cst, opt_s, red, hist, warp, nwarps, lane); \
@@ -829,6 +1033,12 @@ __global__ void __launch_bounds__(512, (KSEL == 0) ? 1 : 2) dp_cta_kernel(DpPara
         if (KSEL != 0) {
             dp_window<(KSEL > 0 ? KSEL : 2), MODE, OSM, FUSE>(P, w, rowA, rowB, sch, cst, opt_s, red, hist, warp, nwarps,
                                                              lane);
+        } else if (MODE == DP_PLAN && P.generic) {
+            const int K = P.windows[w].num_exits;
+            if (K <= 4)
+                dp_window_gen<2, OSM, FUSE>(P, w, K, rowA, rowB, opt_s, red, warp, nwarps, lane);
+            else
+                dp_window_gen<4, OSM, FUSE>(P, w, K, rowA, rowB, opt_s, red, warp, nwarps, lane);
         } else {
             switch (P.windows[w].num_exits) {
 #define TURBO_K_CASE(KK) \

@@ -157,3 +157,16 @@ def test_lockstep_kernel_bad_class_and_range():
     assert int(a["status"][0]) == 99 and int(c["status"][0]) == 99
     for k in ("exits", "best_gain", "best_cost", "feasible", "stats", "budget"):
         np.testing.assert_array_equal(a[k], c[k])
+
+
+# The runtime-K body (dp_window_gen) serves the mixed-K plan-mode launches of the short-row classes by
+# default; variant 16 extends it to the longest-row class, variant 32 turns it off (fifteen
+# K-specific bodies). Every combination must give the same bits as the oracle.
+@pytest.mark.parametrize("variant", [0, 16, 32])
+@pytest.mark.parametrize("fused", ["all", True, False], ids=["schedule", "solve", "plan+backtrack"])
+def test_runtime_k_body(variant, fused):
+    tie = synth.make_tie_heavy(seed=909, W=600, max_frames=60, max_exits=16, max_budget=6000, max_cost=40,
+                               base_cost=84)
+    wl = synth.with_budget_edges(synth.concat_workloads([synth.make_config(5, num_windows=700), tie]), seed=4)
+    want = oracle_run(wl)
+    compare(wl, gpu_run(wl, fused, variant), want, check_options=fused != "all")
