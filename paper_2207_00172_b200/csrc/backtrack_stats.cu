@@ -7,9 +7,9 @@ namespace turbo {
 // K6 (a5). Forward walk from (frame 0, b = C*): k_i = choice_i[b]; b -= c_{i,k_i}
 // (the realisation of the lexicographic tie-break, reading R7; "we
 // execute each frame according to the plan"). The chain of N dependent loads is latency-bound,
-// so one warp serves one window and SPECULATES: while frame i's word is in flight the lanes
-// already fetch frame i+1's words for all K possible shifts b - c_ik (costs of frame i do not
-// depend on b), so each round trip resolves two frames.
+// so one warp serves one window and SPECULATES (backtrack_warp_rt): while frame i's word is in
+// flight the lanes already fetch frame i+1's (and, for K <= 5, frame i+2's) words for every
+// possible shift (costs of frame i do not depend on b), so each round trip resolves 2-3 frames.
 __global__ void __launch_bounds__(256) backtrack_kernel(const turbo_window_t *__restrict__ windows,
                                                         int32_t num_windows,
                                                         const int32_t *__restrict__ opt_cost,
@@ -35,43 +35,11 @@ __global__ void __launch_bounds__(256) backtrack_kernel(const turbo_window_t *__
             for (int32_t i = lane; i < N; i += 32) exit_out[ff + i] = 0;
             continue;
         }
-        const int CB = K <= 4 ? 2 : 4;
-        const int RPT = 32 / CB;
-        const int lg_tile = K <= 4 ? 9 : 8;                   // log2(32 * RPT)
-        const uint32_t cmask = (1u << CB) - 1u;
+        const int RPT = K <= 4 ? 16 : 8;
         const int32_t gtiles = (((Bb + 32) >> 5) + RPT - 1) / RPT;
         const int32_t *__restrict__ oc = opt_cost + fo;
-        auto fetch = [&](int32_t i, int32_t b) -> int32_t {  // choice of frame i at cell b
-            const uint32_t word = __ldg(gch + ((int64_t)i * gtiles + (b >> lg_tile)) * 32 + (b & 31));
-            return (int32_t)((word >> choice_shift((b >> 5) & (RPT - 1), CB)) & cmask);
-        };
-        int32_t b = best_cost[w];
-        int32_t i = 0;
-        while (i < N) {
-            // lane 0 fetches frame i at b; lanes 1..K fetch frame i+1 at b - c_{i,lane-1}
-            // costs do not depend on b: lanes 1..K hold c_{i,lane-1} and c_{i+1,lane-1}
-            const bool opt_lane = lane >= 1 && lane <= K;
-            const int32_t ci = opt_lane ? __ldg(oc + (int64_t)i * K + (lane - 1)) : 0;
-            const int32_t cn = (opt_lane && i + 1 < N) ? __ldg(oc + (int64_t)(i + 1) * K + (lane - 1)) : 0;
-            int32_t kk = 0;
-            if (lane == 0) {
-                kk = fetch(i, b);
-            } else if (lane <= K && i + 1 < N) {
-                const int32_t b1 = b - ci;
-                kk = b1 >= 0 ? fetch(i + 1, b1) : 0;
-            }
-            const int32_t k0 = __shfl_sync(0xffffffffu, kk, 0);
-            const int32_t c0 = __shfl_sync(0xffffffffu, ci, k0 + 1);
-            if (lane == 0) exit_out[ff + i] = (uint8_t)k0;
-            b -= c0;
-            if (i + 1 < N) {
-                const int32_t k1 = __shfl_sync(0xffffffffu, kk, k0 + 1);
-                const int32_t c1 = __shfl_sync(0xffffffffu, cn, k1 + 1);
-                if (lane == 0) exit_out[ff + i + 1] = (uint8_t)k1;
-                b -= c1;
-            }
-            i += 2;
-        }
+        auto cost = [&](int32_t i, int32_t k) -> int32_t { return __ldg(oc + (int64_t)i * K + k); };
+        backtrack_warp_rt(K, N, best_cost[w], gch, gtiles, cost, exit_out + ff, lane);
     }
 }
 
@@ -98,18 +66,6 @@ cudaError_t launch_backtrack(const turbo_window_t *windows, int32_t num_windows,
 // one atomic per non-zero counter at the end. Running the walks here (thousands in flight) frees
 // the DP kernel's CTA slots, which an in-kernel walk of HBM planes would hold for its whole
 // latency-bound chain.
-template <int K>
-__device__ __noinline__ void walk_sched_window(const uint32_t *__restrict__ gch, int32_t gtiles,
-                                               const uint8_t *__restrict__ cls_ids, const int32_t *__restrict__ prof_c,
-                                               int32_t C, int32_t N, int32_t b, uint8_t *__restrict__ exit_g, int lane)
-{
-    auto cost = [&](int32_t i, int32_t k) -> int32_t {
-        const int32_t c = cls_ids[i];
-        return c < C ? __ldg(prof_c + c * K + k) : 0;
-    };
-    backtrack_warp<K, DP_SOLVE_GLOBAL>(N, b, nullptr, gch, 0, gtiles, cost, exit_g, nullptr, lane);
-}
-
 __global__ void __launch_bounds__(128) walk_sched_kernel(const turbo_window_t *__restrict__ windows,
                                                          int32_t num_windows,
                                                          const turbo_profile_t *__restrict__ profiles,
@@ -146,15 +102,16 @@ __global__ void __launch_bounds__(128) walk_sched_kernel(const turbo_window_t *_
             const int32_t gtiles = (((win.budget_bound + 32) >> 5) + RPT - 1) / RPT;
             const uint32_t *__restrict__ gch = reinterpret_cast<const uint32_t *>(workspace + win.choice_offset);
             const int32_t b = best_cost[w];
-            switch (K) {
-#define TURBO_K_CASE(KK) \
-    case KK: walk_sched_window<KK>(gch, gtiles, class_id + ff, pr.cost, pr.num_classes, N, b, exit_out + ff, lane); break;
-                TURBO_K_CASE(2) TURBO_K_CASE(3) TURBO_K_CASE(4) TURBO_K_CASE(5) TURBO_K_CASE(6)
-                TURBO_K_CASE(7) TURBO_K_CASE(8) TURBO_K_CASE(9) TURBO_K_CASE(10) TURBO_K_CASE(11)
-                TURBO_K_CASE(12) TURBO_K_CASE(13) TURBO_K_CASE(14) TURBO_K_CASE(15) TURBO_K_CASE(16)
-#undef TURBO_K_CASE
-                default: break;
-            }
+            // one runtime-K walk for every window (a per-K switch of unrolled walks thrashed the
+            // instruction cache when neighbouring warps walk windows of different K)
+            const uint8_t *__restrict__ cls_ids = class_id + ff;
+            const int32_t *__restrict__ prof_c = pr.cost;
+            const int32_t C = pr.num_classes;
+            auto cost = [&](int32_t i, int32_t k) -> int32_t {
+                const int32_t c = cls_ids[i];
+                return c < C ? __ldg(prof_c + c * K + k) : 0;
+            };
+            backtrack_warp_rt(K, N, b, gch, gtiles, cost, exit_out + ff, lane);
         }
         __syncwarp();                                   // lane 0's exit stores -> the warp
         for (int32_t i = lane; i < N; i += 32) {

@@ -406,6 +406,70 @@ __device__ __forceinline__ void backtrack_warp(int32_t N, int32_t b, const uint3
     }
 }
 
+// a5 for any K (runtime value): the warp walk of backtrack_warp with the same speculation -- lane 0
+// reads frame i at b, lanes 1..K frame i+1 at b - c_{i,a}, and (when 1 + K + K^2 <= 32, i.e.
+// K <= 5) lanes 1+K+aK+a' frame i+2 at b - c_{i,a} - c_{i+1,a'} -- compiled once for all K, so a
+// kernel walking windows of many K values keeps one small body in the instruction cache.
+template <class CostF>
+__device__ __forceinline__ void backtrack_warp_rt(const int K, int32_t N, int32_t b, const uint32_t *__restrict__ gch,
+                                                  int32_t gtiles, CostF cost, uint8_t *__restrict__ exit_g, int lane)
+{
+    const int CB = K <= 4 ? 2 : 4;
+    const int lg_tile = K <= 4 ? 9 : 8;                  // log2(32 * RPT)
+    const int rmask = K <= 4 ? 15 : 7;                   // RPT - 1
+    const uint32_t cmask = (1u << CB) - 1u;
+    const int D = (1 + K + K * K <= 32) ? 3 : 2;
+    int depth = -1, a = 0, a2 = 0;
+    if (lane == 0) {
+        depth = 0;
+    } else if (lane <= K) {
+        depth = 1;
+        a = lane - 1;
+    } else if (D == 3 && lane <= K + K * K) {
+        depth = 2;
+        a = (lane - 1 - K) / K;
+        a2 = (lane - 1 - K) % K;
+    }
+    auto choice = [&](int32_t i, int32_t cell) -> int32_t {
+        const uint32_t word = gch[((int64_t)i * gtiles + (cell >> lg_tile)) * 32 + (cell & 31)];
+        return (int32_t)((word >> choice_shift((cell >> 5) & rmask, CB)) & cmask);
+    };
+    int32_t i = 0;
+    for (; i + D <= N; i += D) {
+        const int32_t ca = depth >= 1 ? cost(i, a) : 0;
+        const int32_t cb = depth == 2 ? cost(i + 1, a2) : 0;
+        int32_t kk = 0;
+        if (depth >= 0) {
+            const int32_t bt = b - ca - cb;
+            kk = bt >= 0 ? choice(i + depth, bt) : 0;
+        }
+        const int32_t k0 = __shfl_sync(0xffffffffu, kk, 0);
+        const int32_t k1 = __shfl_sync(0xffffffffu, kk, D == 3 && depth == 2 ? 1 + a : lane);
+        const bool on_path = (depth == D - 1) && (a == k0) && (D == 2 || a2 == k1);
+        int32_t packed = 0, step = 0;
+        if (on_path) {
+            step = ca + cb + cost(i + depth, kk);
+            packed = D == 3 ? (k0 | (k1 << 4) | (kk << 8)) : (k0 | (kk << 4));
+        }
+        const int src = __ffs(__ballot_sync(0xffffffffu, on_path)) - 1;
+        packed = __shfl_sync(0xffffffffu, packed, src);
+        step = __shfl_sync(0xffffffffu, step, src);
+        if (lane == 0) {
+            exit_g[i] = (uint8_t)(packed & 15);
+            exit_g[i + 1] = (uint8_t)((packed >> 4) & 15);
+            if (D == 3) exit_g[i + 2] = (uint8_t)((packed >> 8) & 15);
+        }
+        b -= step;
+    }
+    if (lane == 0) {
+        for (; i < N; ++i) {
+            const int32_t k = choice(i, b);
+            exit_g[i] = (uint8_t)k;
+            b -= cost(i, k);
+        }
+    }
+}
+
 // a6 fused: accumulate one window's plan statistics (turbo.h layout) into the per-GPU vector.
 // The CTA-private histogram `hist` (176 u32) was filled by thread 0; every counter goes to
 // global memory with one fire-and-forget reduction (RED) per non-zero entry.
@@ -780,7 +844,7 @@ __device__ __noinline__ void dp_window_call(const DpParams &P, int64_t w, int32_
 // instruction in the short-row launch) -- these windows are latency-bound, so the option loop
 // that is not unrolled costs nothing there. Same recurrence, packed keys and outputs as dp_window.
 template <int CB, bool OSM, bool FUSE>
-__device__ __noinline__ void dp_window_gen(const DpParams &P, int64_t w, const int K, int32_t *__restrict__ rowA,
+__device__ __forceinline__ void dp_window_gen(const DpParams &P, int64_t w, const int K, int32_t *__restrict__ rowA,
                                            int32_t *__restrict__ rowB, int2 *__restrict__ opt_s,
                                            int64_t *__restrict__ red, int warp, int nwarps, int lane)
 {
@@ -1001,15 +1065,6 @@ __global__ void __launch_bounds__(512, (KSEL == 0) ? 1 : 2) dp_cta_kernel(DpPara
         // memory, which is fine here -- the out-of-line bodies take it as a parameter anyway
         for (int64_t r = blockIdx.x; r < P.cls_count; r += gridDim.x) {
             const int64_t w = P.windows[P.cls_first + r].order;
-            if (MODE == DP_PLAN && P.generic) {
-                const int K = P.windows[w].num_exits;
-                if (K <= 4)
-                    dp_window_gen<2, OSM, FUSE>(P, w, K, rowA, rowB, opt_s, red, warp, nwarps, lane);
-                else
-                    dp_window_gen<4, OSM, FUSE>(P, w, K, rowA, rowB, opt_s, red, warp, nwarps, lane);
-                __syncthreads();
-                continue;
-            }
             switch (P.windows[w].num_exits) {
 #define TURBO_K_CASE(KK) \
     case KK: dp_window_call<KK, MODE, OSM, FUSE>(P, w, rowA, rowB, sch, cst, opt_s, red, hist, warp, nwarps, lane); \
@@ -1033,12 +1088,6 @@ __global__ void __launch_bounds__(512, (KSEL == 0) ? 1 : 2) dp_cta_kernel(DpPara
         if (KSEL != 0) {
             dp_window<(KSEL > 0 ? KSEL : 2), MODE, OSM, FUSE>(P, w, rowA, rowB, sch, cst, opt_s, red, hist, warp, nwarps,
                                                              lane);
-        } else if (MODE == DP_PLAN && P.generic) {
-            const int K = P.windows[w].num_exits;
-            if (K <= 4)
-                dp_window_gen<2, OSM, FUSE>(P, w, K, rowA, rowB, opt_s, red, warp, nwarps, lane);
-            else
-                dp_window_gen<4, OSM, FUSE>(P, w, K, rowA, rowB, opt_s, red, warp, nwarps, lane);
         } else {
             switch (P.windows[w].num_exits) {
 #define TURBO_K_CASE(KK) \
@@ -1075,6 +1124,7 @@ dp_kernel_t pick_dp_kernel(int kmin, int kmax)
 }
 
 dp_kernel_t dp_kernel_plan(int kmin, int kmax, bool osm);
+dp_kernel_t dp_kernel_generic(bool osm, bool fuse);
 dp_kernel_t dp_kernel_solve_smem(int kmin, int kmax, bool osm);
 dp_kernel_t dp_kernel_schedule(int kmin, int kmax, int mode, bool osm);
 

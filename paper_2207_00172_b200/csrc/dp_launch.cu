@@ -83,7 +83,9 @@ static cudaError_t resolve_dp(const turbo_shape_t *shape, int mode, const DpPara
     const bool osm = P.osm != 0;
     // (HBM choice planes are always walked by a separate kernel: DP_SOLVE_GLOBAL never gets here)
     if (mode == DP_SOLVE_GLOBAL) return cudaErrorInvalidValue;
-    dp_kernel_t kern = P.fuse                  ? dp_kernel_schedule(shape->min_exits, shape->max_exits, mode, osm)
+    if (P.generic && mode != DP_PLAN) return cudaErrorInvalidValue;
+    dp_kernel_t kern = P.generic               ? dp_kernel_generic(osm, P.fuse != 0)
+                       : P.fuse                ? dp_kernel_schedule(shape->min_exits, shape->max_exits, mode, osm)
                        : mode == DP_PLAN         ? dp_kernel_plan(shape->min_exits, shape->max_exits, osm)
                                                  : dp_kernel_solve_smem(shape->min_exits, shape->max_exits, osm);
     static std::mutex amu;
@@ -188,6 +190,7 @@ cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P0, 
 }  // namespace turbo
 
 namespace turbo {
+dp_kernel_t dp_kernel_generic(bool osm, bool fuse);
 dp_kernel_t dp_kernel_sched_smem_osm(int kmin, int kmax);
 dp_kernel_t dp_kernel_sched_smem_reg(int kmin, int kmax);
 dp_kernel_t dp_kernel_sched_global_osm(int kmin, int kmax);

@@ -102,7 +102,7 @@ struct DpParams {
     int32_t pack_v;
     int32_t pack_tiles;
     int32_t pack_stride;
-    int32_t generic;               // mixed-K plan-mode launch: one runtime-K body (dp_window_gen)
+    int32_t generic;               // mixed-K plan-mode launch: the runtime-K kernel (dp_gen.cu)
 };
 
 // turbo_debug_trace: %globaltimer at phase p of window w (thread 0 of the window's CTA). Compiled
