@@ -309,7 +309,7 @@ turbo_status_t turbo_batched_plan(const turbo_shape_t *shape /* host */, const t
  * variant & 4: do not stage option tables in shared memory (shuffle broadcast instead);
  * variant & 8: use the lockstep multi-window kernel (dp_pack.cu; V windows per CTA) for
  * single-class short-row batches instead of one CTA per window;
- * variant & 16: the runtime-K kernel also for the longer-row classes of mixed-K plan launches;
+ * variant & 16: the runtime-K kernel also for row class 3 of mixed-K plan launches;
  * variant & 32: never the runtime-K body (the fifteen K-specific bodies everywhere).
  * Returns INVALID_ARG for other values. Process-wide; not needed in production. */
 turbo_status_t turbo_debug_set_variant(int32_t variant);

@@ -366,13 +366,13 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int kind, const DpParam
         }
         P.cls = c;
         P.max_frames = shapes[c].max_frames;
-        // mixed-K plan-mode launches of the two short-row classes run the runtime-K kernel (many
-        // small CTAs of different K per SM would thrash the instruction cache with fifteen unrolled
-        // bodies, and 128 registers per thread would cap their residency); the longer rows are
-        // pipe-bound and keep the K-specific bodies (measured: class 2 4.06 ms K-specific vs
-        // 4.82 ms runtime-K, class 3 8.4 vs 11.2 ms)
+        // mixed-K plan-mode launches of row classes 0-2 run the runtime-K kernel: several CTAs of
+        // different K per SM would thrash the instruction cache with fifteen unrolled bodies, and
+        // 128 registers per thread would cap their residency (c5, ncu: class 0 2.42 -> 0.61 ms,
+        // class 1 2.56 -> 1.06, class 2 4.02 -> 3.28). The longest rows (one CTA per SM, so one K
+        // per SM) keep the K-specific bodies (runtime-K measured 11.2 vs 8.4 ms there).
         P.generic = (modes[c] == DP_PLAN && !dp_kernel_fixed_k(shapes[c].min_exits, shapes[c].max_exits) &&
-                     (c < 2 || (g_variant & 16)) && !(g_variant & 32)) ? 1 : 0;
+                     (c < 3 || (g_variant & 16)) && !(g_variant & 32)) ? 1 : 0;
         P.cls_count = shape->cls_count[c];
         // the serving order is followed by the mixed-K kernels; fixed-K kernels go in index order
         P.ordered = (shape->ordered && !dp_kernel_fixed_k(shapes[c].min_exits, shapes[c].max_exits)) ? 1 : 0;

@@ -159,7 +159,7 @@ def test_lockstep_kernel_bad_class_and_range():
         np.testing.assert_array_equal(a[k], c[k])
 
 
-# The runtime-K body (dp_window_gen) serves the mixed-K plan-mode launches of the short-row classes by
+# The runtime-K kernel (dp_gen.cu) serves the mixed-K plan-mode launches of row classes 0-2 by
 # default; variant 16 extends it to the longest-row class, variant 32 turns it off (fifteen
 # K-specific bodies). Every combination must give the same bits as the oracle.
 @pytest.mark.parametrize("variant", [0, 16, 32])
