@@ -249,7 +249,7 @@ turbo_status_t turbo_mckp_workspace(const turbo_profile_t *profiles_host, int32_
     s.total_cells = cells;
     if (s.num_big > 0) {                 // long-window kernel scratch: flags + halo ring
         s.grid_scratch_offset = (ws + 255) & ~(int64_t)255;
-        ws = s.grid_scratch_offset + grid_scratch_bytes();
+        ws = s.grid_scratch_offset + grid_scratch_bytes(s.max_budget);
     }
     s.workspace_bytes = ws;
     *shape = s;

@@ -172,8 +172,10 @@ struct GridCtx {
     int *pub;               // [GRID_MAX_CTAS] steps published (monotone across windows)
     int *con;               // [GRID_MAX_CTAS] steps whose halo was consumed
     long long *misc;        // [8] per-window reductions (zeroed between windows)
-    unsigned long long *ring;   // [D][GRID_MAX_CTAS][TURBO_BIG_MAX_COST] of {value, step tag}
+    unsigned long long *ring;   // [D][GRID_MAX_CTAS][GRID_H] of {value, step tag}
     long long *trace;           // [GRID_MAX_CTAS][8] cycle counters (debug bit 2)
+    int32_t *l2rows;            // L2-row path: two global rows of l2stride cells
+    int64_t l2stride;
 };
 
 // a5 of the long window by the WHOLE CTA (512 threads, the rest of the GPU is idle): thread q is
@@ -289,31 +291,16 @@ __device__ __forceinline__ void backtrack_cta_spec(int32_t N, int32_t b, const u
     __syncthreads();
 }
 
-// a6 of a rejected long window (turbo_schedule): all frames at level 0, G* = C* = 0, infeasible
-// (the same counts the CTA kernels give a rejected window)
-__device__ __forceinline__ void reject_stats(const DpParams &P, uint32_t *hist, int64_t ff, int32_t N, int tid,
-                                             int nthr)
-{
-    for (int x = tid; x < 176; x += nthr) hist[x] = 0;
-    __syncthreads();
-    for (int32_t i = tid; i < N; i += nthr) {
-        const uint32_t cls = P.class_id[ff + i];
-        atomicAdd(&hist[0], 1u);
-        if (cls < 10) atomicAdd(&hist[16 + cls * 16], 1u);
-    }
-    __syncthreads();
-    flush_window_stats(P, hist, 0, 0, false, N, tid, nthr);
-    __syncthreads();
-}
-
-template <int K, int MODE>
+// a3 + a4 of ONE long window over the whole (cooperative) grid; the walk (a5) and, for
+// turbo_schedule, the statistics (a6) follow in long_walk_kernel.
+template <int K>
 __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &grid, int64_t w, int32_t *bufA, int32_t *bufB,
                            long long *red, GridCtx X, int &step_base, unsigned long long *stage_in,
-                           unsigned long long *stage_out, uint64_t *mbar, uint32_t *mbar_uses, uint32_t *hist)
+                           unsigned long long *stage_out, uint64_t *mbar, uint32_t *mbar_uses)
 {
     constexpr int CB = (K <= 4) ? 2 : 4;
     constexpr int RPT = 32 / CB;
-    constexpr int H = TURBO_BIG_MAX_COST;          // halo capacity (cells)
+    constexpr int H = GRID_H;                      // halo capacity (cells)
     constexpr int D = GRID_RING_DEPTH;
     const int tid = threadIdx.x, nthr = blockDim.x, lane = tid & 31, warp = tid >> 5, nwarps = nthr >> 5;
     const int j = blockIdx.x, NP = gridDim.x;
@@ -405,7 +392,7 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
     const long long c0_sum = *((volatile long long *)&X.misc[3]);
     const int32_t cmax = (int32_t)*((volatile long long *)&X.misc[1]);
     const bool bad = *((volatile long long *)&X.misc[0]) != 0 || *((volatile long long *)&X.misc[4]) >= GAIN_RANGE_LIMIT ||
-                     c0_sum >= 0x7fffffffll || B < 0 || B > Bb || cmax > H;
+                     c0_sum >= 0x7fffffffll || B < 0 || B > Bb;
     if (bad) {
         if (j == 0 && tid == 0) {
             P.best_gain[w] = 0;
@@ -413,9 +400,72 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
             P.feasible[w] = 0;
             atomic_min_i64(&P.status[1], w);
         }
-        if (MODE != DP_PLAN)
-            for (int32_t i = j * nthr + tid; i < N; i += NP * nthr) P.exit_out[ff + i] = 0;
-        if (fuse && j == 0) reject_stats(P, hist, ff, N, tid, nthr);
+        return;
+    }
+    uint32_t *__restrict__ gch_w = gch;
+    if (cmax > H) {
+        // ---- L2-row path (an option cost beyond the halo capacity; reading R17): S_{i+1} and S_i live
+        // in global memory (8 MB for B = 2^20, L2-resident), every warp of the grid computes whole
+        // tiles of the row, one grid barrier per frame. Reads bypass L1 (ld.global.cg): the cells
+        // were written by other SMs one frame earlier.
+        const int32_t ntile = (nrows + RPT - 1) / RPT;
+        int32_t *r0 = X.l2rows, *r1 = X.l2rows + X.l2stride;
+        for (int64_t x = (int64_t)j * nthr + tid; x < (int64_t)ntile * RPT * 32; x += (int64_t)NP * nthr) r0[x] = 0;
+        int32_t lg = 0, lc = 0;                       // lane k < K: option k of the next frame
+        if (N > 0 && lane < K) {
+            lg = opt_g(N - 1, lane);
+            lc = opt_c(N - 1, lane);
+        }
+        grid.sync();
+        const int gw = j * nwarps + warp, GW = NP * nwarps;
+        for (int32_t f = 0; f < N; ++f) {
+            const int32_t i = N - 1 - f;
+            int32_t gp[K], cc[K];
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                gp[k] = (__shfl_sync(0xffffffffu, lg, k) << 4) | (15 - k);
+                cc[k] = __shfl_sync(0xffffffffu, lc, k);
+            }
+            if (i > 0 && lane < K) {
+                lg = opt_g(i - 1, lane);
+                lc = opt_c(i - 1, lane);
+            }
+            const int32_t *cur = (f & 1) ? r1 : r0;
+            int32_t *nxt = (f & 1) ? r0 : r1;
+            for (int32_t t = gw; t < ntile; t += GW) {
+                const int32_t b_lo = t * RPT * 32;
+                int32_t key[RPT];
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) key[r] = NEG_R;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+#pragma unroll
+                    for (int r = 0; r < RPT; ++r) {
+                        const int32_t idx = b_lo + r * 32 + lane - cc[k];
+                        const int32_t v = idx >= 0 ? __ldcg(cur + idx) : NEG_R;
+                        key[r] = max_plus(v, gp[k], key[r]);
+                    }
+                }
+#pragma unroll
+                for (int r = 0; r < RPT; ++r) __stcg(nxt + b_lo + r * 32 + lane, key[r] & ~15);
+                gch_w[((int64_t)i * gtiles + t) * 32 + lane] = pack_choices<RPT, CB>(key);
+            }
+            grid.sync();                                  // S_i complete before frame i - 1 reads it
+        }
+        // ---- a4: G* = S_0[B], C* = #{b <= B : S_0[b] < G*}
+        const int32_t *S0 = (N & 1) ? r1 : r0;
+        const int32_t RB = __ldcg(S0 + B);
+        long long cnt = 0;
+        for (int64_t b = (int64_t)j * nthr + tid; b <= B; b += (int64_t)NP * nthr) cnt += __ldcg(S0 + b) < RB ? 1 : 0;
+        cnt = block_sum_ll(cnt, red, tid, nthr);
+        if (tid == 0 && cnt) atomicAdd(reinterpret_cast<unsigned long long *>(&X.misc[6]), (unsigned long long)cnt);
+        grid.sync();
+        const bool feas = RB > VALID_MIN_R;
+        if (j == 0 && tid == 0) {
+            P.best_gain[w] = feas ? (RB >> 4) : (int32_t)g0_sum;
+            P.best_cost[w] = feas ? (int32_t)*((volatile long long *)&X.misc[6]) : (int32_t)c0_sum;
+            P.feasible[w] = feas ? 1 : 0;
+        }
         return;
     }
     const int32_t hl = cmax;                        // halo length actually needed (<= H)
@@ -663,9 +713,6 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
             P.best_cost[w] = 0;
             P.feasible[w] = 0;
         }
-        if (MODE != DP_PLAN)
-            for (int32_t i = j * nthr + tid; i < N; i += NP * nthr) P.exit_out[ff + i] = 0;
-        if (fuse && j == 0) reject_stats(P, hist, ff, N, tid, nthr);
         return;
     }
     const bool feas = RB > VALID_MIN_R;
@@ -676,54 +723,33 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
         P.best_cost[w] = Cst;
         P.feasible[w] = feas ? 1 : 0;
     }
-    if (MODE == DP_PLAN) return;
-    // ---- a5 (solve): CTA 0's warp 0 walks the HBM choice planes
-    if (!feas) {
-        for (int32_t i = j * nthr + tid; i < N; i += NP * nthr) P.exit_out[ff + i] = 0;
-    } else if (j == 0) {                               // CTA 0, all threads (the grid is idle)
-        auto cost = [&](int32_t i, int32_t k) -> int32_t { return opt_c(i, k); };
-        backtrack_cta_spec<K>(N, Cst, gch, gtiles, cost, P.exit_out + ff, red + 8);
-    }
-    if (fuse && j == 0) {
-        // a6 of the long window (turbo_schedule): CTA 0 bins the plan it just wrote (an infeasible
-        // plan is all zero) and adds the window's totals to the per-GPU vector
-        for (int x = tid; x < 176; x += nthr) hist[x] = 0;
-        __syncthreads();
-        for (int32_t i = tid; i < N; i += nthr) {
-            const uint32_t k = feas ? (P.exit_out[ff + i] & 15u) : 0u;
-            const uint32_t cls = P.class_id[ff + i];
-            atomicAdd(&hist[k], 1u);
-            if (cls < 10) atomicAdd(&hist[16 + cls * 16 + k], 1u);
-        }
-        __syncthreads();
-        flush_window_stats(P, hist, G, Cst, feas, N, tid, nthr);
-        __syncthreads();
-    }
 }
 
 // Out-of-line instance per K for the mixed-K kernel (compile time); fixed-K kernels inline it.
-template <int K, int MODE>
+template <int K>
 __device__ __noinline__ void grid_window_call(const DpParams &P, cg::grid_group &grid, int64_t w, int32_t *bufA,
                                               int32_t *bufB, long long *red, GridCtx X, int &step_base,
                                               unsigned long long *stage_in, unsigned long long *stage_out,
-                                              uint64_t *mbar, uint32_t *mbar_uses, uint32_t *hist)
+                                              uint64_t *mbar, uint32_t *mbar_uses)
 {
-    grid_window<K, MODE>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar, mbar_uses, hist);
+    grid_window<K>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar, mbar_uses);
 }
 
-template <int KSEL, int MODE>
-__global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg_max, int32_t span)
+// The long-window DP (a1..a4 of every long window of the batch, one after the other): a cooperative
+// grid of GRID_THREADS-thread CTAs, two per SM when the segments fit (the barriers of one CTA
+// overlap the other's tiles), else one.
+template <int KSEL>
+__global__ void __launch_bounds__(GRID_THREADS, 2) dp_grid_kernel(DpParams P, int32_t seg_max, int32_t span)
 {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ int4 smem_raw[];
     long long *red = reinterpret_cast<long long *>(smem_raw);              // 8 x int64 (+ 8 spare)
     int32_t *bufA = reinterpret_cast<int32_t *>(smem_raw) + 32;
-    int32_t *bufB = bufA + TURBO_BIG_MAX_COST + seg_max;
-    unsigned long long *stage_in = reinterpret_cast<unsigned long long *>(bufB + TURBO_BIG_MAX_COST + seg_max);
-    unsigned long long *stage_out = stage_in + TURBO_BIG_MAX_COST;          // two stages (parity)
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(stage_out + 2 * TURBO_BIG_MAX_COST);
+    int32_t *bufB = bufA + GRID_H + seg_max;
+    unsigned long long *stage_in = reinterpret_cast<unsigned long long *>(bufB + GRID_H + seg_max);
+    unsigned long long *stage_out = stage_in + GRID_H;                      // two stages (parity)
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(stage_out + 2 * GRID_H);
     uint32_t *mbar_uses = reinterpret_cast<uint32_t *>(mbar + 1);           // completed halo loads
-    __shared__ uint32_t ghist[176];                                         // a6 of turbo_schedule
     if (threadIdx.x == 0) {
         mbar_init(mbar, 1);
         *mbar_uses = 0;
@@ -737,6 +763,8 @@ __global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg
     unsigned long long *hdr = reinterpret_cast<unsigned long long *>(flags + grid_flags_words());
     X.ring = reinterpret_cast<unsigned long long *>(flags + grid_flags_words() + GRID_HEADER_WORDS);
     X.trace = reinterpret_cast<long long *>(flags + 2 * GRID_MAX_CTAS + 64);
+    X.l2rows = reinterpret_cast<int32_t *>(X.ring + grid_ring_words());
+    X.l2stride = grid_l2_stride(P.grid_max_budget);
     // Ring tags continue from the epoch stored in this workspace (every CTA reads it before the
     // first grid barrier; CTA 0 advances it after the last one), so a ring word left by an earlier
     // launch -- or an earlier replay of a captured graph -- never carries a tag this launch expects.
@@ -747,8 +775,7 @@ __global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg
         const int epoch = ld_relaxed_gpu(reinterpret_cast<const int *>(hdr + 1));
         const bool clear = magic != GRID_MAGIC || epoch < 1 || (int64_t)epoch + span >= (1ll << 30);
         if (clear) {
-            const int64_t words = (int64_t)GRID_RING_DEPTH * GRID_MAX_CTAS * TURBO_BIG_MAX_COST;
-            for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < words;
+            for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < grid_ring_words();
                  x += (int64_t)gridDim.x * blockDim.x)
                 X.ring[x] = 0ull;
         }
@@ -758,13 +785,12 @@ __global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg
     for (int64_t w = 0; w < P.num_windows; ++w) {
         if ((int64_t)P.windows[w].budget_bound + 1 <= TURBO_BIG_CELLS) continue;
         if (KSEL != 0) {
-            grid_window<(KSEL > 0 ? KSEL : 2), MODE>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar,
-                                                     mbar_uses, ghist);
+            grid_window<(KSEL > 0 ? KSEL : 2)>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar,
+                                               mbar_uses);
         } else {
             switch (P.windows[w].num_exits) {
 #define TURBO_K_CASE(KK) \
-    case KK: grid_window_call<KK, MODE>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar, mbar_uses, \
-                                        ghist);                                                                  \
+    case KK: grid_window_call<KK>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar, mbar_uses); \
         break;
                 TURBO_K_CASE(2) TURBO_K_CASE(3) TURBO_K_CASE(4) TURBO_K_CASE(5) TURBO_K_CASE(6)
                 TURBO_K_CASE(7) TURBO_K_CASE(8) TURBO_K_CASE(9) TURBO_K_CASE(10) TURBO_K_CASE(11)
@@ -783,59 +809,148 @@ __global__ void __launch_bounds__(512, 1) dp_grid_kernel(DpParams P, int32_t seg
     }
 }
 
-typedef void (*dp_grid_kernel_t)(DpParams, int32_t, int32_t);
-static const int GRID_THREADS = 512;
-
-template <int MODE>
-static dp_grid_kernel_t pick_grid(int kmin, int kmax)
+// a5 (+ a6 for turbo_schedule) of the long windows: CTA b walks the b-th long window (the serving
+// order lists them last) with all its 512 threads (backtrack_cta_spec: D frames per HBM round
+// trip), then bins the plan it wrote. Infeasible and rejected windows get all-zero exits.
+template <int K>
+__device__ __forceinline__ void long_walk_window(const DpParams &P, int64_t w, long long *slot, uint32_t *hist)
 {
-    if (kmin != kmax) return dp_grid_kernel<0, MODE>;
-    switch (kmin) {
-        case 4: return dp_grid_kernel<4, MODE>;
-        case 5: return dp_grid_kernel<5, MODE>;
-        case 6: return dp_grid_kernel<6, MODE>;
-        case 8: return dp_grid_kernel<8, MODE>;
-        default: return dp_grid_kernel<0, MODE>;
+    constexpr int RPT = (K <= 4) ? 16 : 8;
+    const int tid = threadIdx.x, nthr = blockDim.x;
+    const turbo_window_t *win = P.windows + w;
+    const int64_t ff = win->first_frame;
+    const int32_t N = win->num_frames;
+    const bool feas = P.feasible[w] != 0;
+    const int32_t gtiles = (int32_t)(((win->budget_bound + 32) >> 5) + RPT - 1) / RPT;
+    const uint32_t *gch = reinterpret_cast<const uint32_t *>(P.workspace + win->choice_offset);
+    const bool fuse = P.fuse != 0;
+    int32_t prof_C = 0;
+    const int32_t *prof_c = nullptr;
+    if (fuse) {
+        prof_C = P.profiles[win->profile].num_classes;
+        prof_c = P.profiles[win->profile].cost;
+    }
+    const int32_t *oc = P.opt_cost + win->first_option;
+    auto cost = [&](int32_t i, int32_t k) -> int32_t {
+        if (!fuse) return __ldg(oc + (int64_t)i * K + k);
+        const int32_t cls = P.class_id[ff + i];
+        return cls < prof_C ? __ldg(prof_c + cls * K + k) : 0;
+    };
+    if (feas)
+        backtrack_cta_spec<K>(N, P.best_cost[w], gch, gtiles, cost, P.exit_out + ff, slot);
+    else
+        for (int32_t i = tid; i < N; i += nthr) P.exit_out[ff + i] = 0;
+    if (fuse) {                                        // a6: the window's plan into the per-GPU vector
+        for (int x = tid; x < 176; x += nthr) hist[x] = 0;
+        __syncthreads();
+        for (int32_t i = tid; i < N; i += nthr) {
+            const uint32_t k = feas ? (P.exit_out[ff + i] & 15u) : 0u;
+            const uint32_t cls = P.class_id[ff + i];
+            atomicAdd(&hist[k], 1u);
+            if (cls < 10) atomicAdd(&hist[16 + cls * 16 + k], 1u);
+        }
+        __syncthreads();
+        flush_window_stats(P, hist, P.best_gain[w], P.best_cost[w], feas, N, tid, nthr);
+    }
+    __syncthreads();
+}
+
+template <int K>
+__device__ __noinline__ void long_walk_call(const DpParams &P, int64_t w, long long *slot, uint32_t *hist)
+{
+    long_walk_window<K>(P, w, slot, hist);
+}
+
+template <int KSEL>
+__global__ void __launch_bounds__(512, 1) long_walk_kernel(DpParams P, int32_t num_big)
+{
+    __shared__ long long slot[8];
+    __shared__ uint32_t hist[176];
+    for (int64_t b = blockIdx.x; b < num_big; b += gridDim.x) {
+        const int64_t w = P.windows[(int64_t)P.num_windows - num_big + b].order;
+        if (KSEL != 0) {
+            long_walk_window<(KSEL > 0 ? KSEL : 2)>(P, w, slot, hist);
+        } else {
+            switch (P.windows[w].num_exits) {
+#define TURBO_K_CASE(KK) \
+    case KK: long_walk_call<KK>(P, w, slot, hist); break;
+                TURBO_K_CASE(2) TURBO_K_CASE(3) TURBO_K_CASE(4) TURBO_K_CASE(5) TURBO_K_CASE(6)
+                TURBO_K_CASE(7) TURBO_K_CASE(8) TURBO_K_CASE(9) TURBO_K_CASE(10) TURBO_K_CASE(11)
+                TURBO_K_CASE(12) TURBO_K_CASE(13) TURBO_K_CASE(14) TURBO_K_CASE(15) TURBO_K_CASE(16)
+#undef TURBO_K_CASE
+                default: break;
+            }
+        }
     }
 }
 
-// Launch geometry of the long-window kernel: CTAs, segment cells, dynamic shared memory; and the
-// host-only checks (shared memory incl. the kernel's static part, cooperative residency) that
-// run_dp performs before launching anything.
-static cudaError_t grid_geometry(const turbo_shape_t *shape, int mode, int num_sms, int smem_per_cta_max,
+typedef void (*dp_grid_kernel_t)(DpParams, int32_t, int32_t);
+typedef void (*long_walk_kernel_t)(DpParams, int32_t);
+
+static dp_grid_kernel_t pick_grid(int kmin, int kmax)
+{
+    if (kmin != kmax) return dp_grid_kernel<0>;
+    switch (kmin) {
+        case 4: return dp_grid_kernel<4>;
+        case 5: return dp_grid_kernel<5>;
+        case 6: return dp_grid_kernel<6>;
+        case 8: return dp_grid_kernel<8>;
+        default: return dp_grid_kernel<0>;
+    }
+}
+
+static long_walk_kernel_t pick_walk(int kmin, int kmax)
+{
+    if (kmin != kmax) return long_walk_kernel<0>;
+    switch (kmin) {
+        case 4: return long_walk_kernel<4>;
+        case 5: return long_walk_kernel<5>;
+        case 6: return long_walk_kernel<6>;
+        case 8: return long_walk_kernel<8>;
+        default: return long_walk_kernel<0>;
+    }
+}
+
+// Launch geometry of the long-window kernel: CTAs (two per SM when the segment fits, else one),
+// segment cells, dynamic shared memory; and the host-only checks (shared memory incl. the kernel's
+// static part, cooperative residency) that run_dp performs before launching anything.
+static cudaError_t grid_geometry(const turbo_shape_t *shape, int num_sms, int smem_per_cta_max,
                                  dp_grid_kernel_t *kern_out, int *np_out, int32_t *seg_out, size_t *smem_out)
 {
-    const int NP = num_sms < GRID_MAX_CTAS ? num_sms : GRID_MAX_CTAS;
-    int32_t seg = (int32_t)(((int64_t)shape->max_budget + 1 + NP - 1) / NP);
-    seg = (seg + 511) & ~511;
-    if (seg < TURBO_BIG_MAX_COST) seg = TURBO_BIG_MAX_COST;
-    const size_t smem = 128 + (size_t)8 * (TURBO_BIG_MAX_COST + seg) + (size_t)24 * TURBO_BIG_MAX_COST + 16;
-    dp_grid_kernel_t kern = mode == DP_PLAN ? pick_grid<DP_PLAN>(shape->min_exits, shape->max_exits)
-                                            : pick_grid<DP_SOLVE_GLOBAL>(shape->min_exits, shape->max_exits);
+    dp_grid_kernel_t kern = pick_grid(shape->min_exits, shape->max_exits);
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, kern);
     if (e != cudaSuccess) return e;
-    if (smem + fa.sharedSizeBytes > (size_t)smem_per_cta_max) return cudaErrorInvalidConfiguration;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int occ = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, GRID_THREADS, smem);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) return cudaErrorCooperativeLaunchTooLarge;
-    *kern_out = kern;
-    *np_out = NP;
-    *seg_out = seg;
-    *smem_out = smem;
-    return cudaSuccess;
+    for (int per_sm = 2; per_sm >= 1; --per_sm) {
+        const int NP = std::min(num_sms * per_sm, GRID_MAX_CTAS);
+        int32_t seg = (int32_t)(((int64_t)shape->max_budget + 1 + NP - 1) / NP);
+        seg = (seg + 511) & ~511;
+        if (seg < GRID_H) seg = GRID_H;
+        const size_t smem = 128 + (size_t)8 * (GRID_H + seg) + (size_t)24 * GRID_H + 16;
+        if (smem + fa.sharedSizeBytes > (size_t)smem_per_cta_max) continue;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        int occ = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, GRID_THREADS, smem);
+        if (e != cudaSuccess) return e;
+        if (occ < per_sm) continue;
+        *kern_out = kern;
+        *np_out = NP;
+        *seg_out = seg;
+        *smem_out = smem;
+        return cudaSuccess;
+    }
+    return cudaErrorCooperativeLaunchTooLarge;
 }
 
 cudaError_t check_dp_grid(const turbo_shape_t *shape, int mode, int num_sms, int smem_per_cta_max)
 {
+    (void)mode;
     dp_grid_kernel_t kern;
     int NP;
     int32_t seg;
     size_t smem;
-    return grid_geometry(shape, mode, num_sms, smem_per_cta_max, &kern, &NP, &seg, &smem);
+    return grid_geometry(shape, num_sms, smem_per_cta_max, &kern, &NP, &seg, &smem);
 }
 
 cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams &P0, int num_sms,
@@ -846,7 +961,7 @@ cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams 
     int NP;
     int32_t seg;
     size_t smem;
-    cudaError_t e = grid_geometry(shape, mode, num_sms, smem_per_cta_max, &kern, &NP, &seg, &smem);
+    cudaError_t e = grid_geometry(shape, num_sms, smem_per_cta_max, &kern, &NP, &seg, &smem);
     if (e != cudaSuccess) return e;
     e = cudaMemsetAsync(P.workspace + P.grid_scratch_offset, 0, (size_t)grid_flags_words() * 4, stream);
     if (e != cudaSuccess) return e;
@@ -856,9 +971,16 @@ cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams 
         const char *dbg = getenv("TURBO_GRID_DEBUG");      // 1: no halo exchange (timing only)
         P.debug = dbg ? atoi(dbg) : 0;
     }
+    P.grid_max_budget = shape->max_budget;
     void *args[] = {(void *)&P, (void *)&seg, (void *)&span};
     note_launch();
-    return cudaLaunchCooperativeKernel((const void *)kern, dim3(NP), dim3(GRID_THREADS), args, smem, stream);
+    e = cudaLaunchCooperativeKernel((const void *)kern, dim3(NP), dim3(GRID_THREADS), args, smem, stream);
+    if (e != cudaSuccess || mode == DP_PLAN) return e;
+    // a5 (+ a6): one 512-thread CTA per long window
+    note_launch();
+    long_walk_kernel_t wk = pick_walk(shape->min_exits, shape->max_exits);
+    wk<<<(unsigned)std::min<int64_t>(shape->num_big, 65535), 512, 0, stream>>>(P, shape->num_big);
+    return cudaGetLastError();
 }
 
 }  // namespace turbo

@@ -103,6 +103,7 @@ struct DpParams {
     int32_t pack_tiles;
     int32_t pack_stride;
     int32_t generic;               // mixed-K plan-mode launch: the runtime-K kernel (dp_gen.cu)
+    int32_t grid_max_budget;       // long-window kernel: largest budget bound (L2-row path row size)
 };
 
 // turbo_debug_trace: %globaltimer at phase p of window w (thread 0 of the window's CTA). Compiled
@@ -152,7 +153,9 @@ cudaError_t check_dp(const turbo_shape_t *shape, int mode, const DpParams &P, in
 cudaError_t check_dp_grid(const turbo_shape_t *shape, int mode, int num_sms, int smem_per_cta_max);
 
 // long-window (grid) kernel: scratch = flags (pub/con per CTA + misc) + halo ring
-constexpr int GRID_MAX_CTAS = 256;
+constexpr int GRID_MAX_CTAS = 512;                 // two CTAs per SM on 148 SMs
+constexpr int GRID_H = TURBO_BIG_MAX_COST;         // halo capacity of the segment path (cells)
+constexpr int GRID_THREADS = 256;                  // threads per CTA of the long-window DP kernel
 constexpr int GRID_RING_DEPTH = 8;
 // scratch = [flags: cleared by every launch][header: persists across launches][halo ring]
 __host__ __device__ constexpr int64_t grid_flags_words() { return 2 * GRID_MAX_CTAS + 64 + 16 * GRID_MAX_CTAS; }
@@ -161,10 +164,13 @@ __host__ __device__ constexpr int64_t grid_flags_words() { return 2 * GRID_MAX_C
 // kernel arguments are frozen at capture (the kernel advances the epoch on the device).
 constexpr int64_t GRID_HEADER_WORDS = 16;
 constexpr unsigned long long GRID_MAGIC = 0x7475726230677264ull;   // "turb0grd"
-__host__ __device__ constexpr int64_t grid_scratch_bytes()
+__host__ __device__ constexpr int64_t grid_ring_words() { return (int64_t)GRID_RING_DEPTH * GRID_MAX_CTAS * GRID_H; }
+// cells of one global row of the L2-row path: whole 512-cell tiles above the largest budget
+__host__ __device__ constexpr int64_t grid_l2_stride(int64_t max_budget) { return (max_budget + 1 + 511) & ~(int64_t)511; }
+// scratch = [flags][header][halo ring: 8-B words][two global rows (L2-row path): int32]
+__host__ __device__ constexpr int64_t grid_scratch_bytes(int64_t max_budget)
 {
-    return 4 * (grid_flags_words() + GRID_HEADER_WORDS) +
-           8 * (int64_t)GRID_RING_DEPTH * GRID_MAX_CTAS * TURBO_BIG_MAX_COST;
+    return 4 * (grid_flags_words() + GRID_HEADER_WORDS) + 8 * grid_ring_words() + 8 * grid_l2_stride(max_budget);
 }
 cudaError_t launch_heuristic(const turbo_shape_t *shape, const turbo_window_t *windows, const int32_t *opt_gain,
                              const int32_t *opt_cost, int32_t *gain_out, int32_t *cost_out, uint8_t *feasible,
