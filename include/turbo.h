@@ -117,13 +117,13 @@ typedef struct {
 #define TURBO_CLASS_CELLS_3 24576
 
 /* Rows longer than this many cells (budget_bound + 1) are planned by the long-window kernel:
- * one cooperative grid of CTAs per window (two per SM), each CTA owning a contiguous budget
+ * one cooperative grid of CTAs per window (one per SM), each CTA owning a contiguous budget
  * segment in shared memory, with neighbour halos exchanged through an L2 ring (SURVEY.md §8(a)
  * c4). A window whose largest option cost exceeds TURBO_BIG_MAX_COST cells (the halo capacity)
  * is planned instead with its two rows in global memory (L2-resident) and one grid barrier per
  * frame -- same results, slower; no cost is rejected for its size (reading R17). */
 #define TURBO_BIG_CELLS 24576
-#define TURBO_BIG_MAX_COST 2048
+#define TURBO_BIG_MAX_COST 4096
 
 /* Number of int64 words of the status vector written by lookup / plan. */
 #define TURBO_STATUS_WORDS 2

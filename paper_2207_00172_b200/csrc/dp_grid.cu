@@ -736,10 +736,9 @@ __device__ __noinline__ void grid_window_call(const DpParams &P, cg::grid_group 
 }
 
 // The long-window DP (a1..a4 of every long window of the batch, one after the other): a cooperative
-// grid of GRID_THREADS-thread CTAs, two per SM when the segments fit (the barriers of one CTA
-// overlap the other's tiles), else one.
+// grid of GRID_THREADS-thread CTAs, GRID_CTAS_PER_SM per SM when the segments fit, else one.
 template <int KSEL>
-__global__ void __launch_bounds__(GRID_THREADS, 2) dp_grid_kernel(DpParams P, int32_t seg_max, int32_t span)
+__global__ void __launch_bounds__(GRID_THREADS, GRID_CTAS_PER_SM) dp_grid_kernel(DpParams P, int32_t seg_max, int32_t span)
 {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ int4 smem_raw[];
@@ -921,7 +920,7 @@ static cudaError_t grid_geometry(const turbo_shape_t *shape, int num_sms, int sm
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, kern);
     if (e != cudaSuccess) return e;
-    for (int per_sm = 2; per_sm >= 1; --per_sm) {
+    for (int per_sm = GRID_CTAS_PER_SM; per_sm >= 1; --per_sm) {
         const int NP = std::min(num_sms * per_sm, GRID_MAX_CTAS);
         int32_t seg = (int32_t)(((int64_t)shape->max_budget + 1 + NP - 1) / NP);
         seg = (seg + 511) & ~511;

@@ -90,11 +90,11 @@ def test_graph_replay_with_changed_inputs(fused):
 
 @pytest.mark.parametrize("fused", [True, False, "all"], ids=["solve", "plan+backtrack", "schedule"])
 def test_long_window_costs_beyond_the_halo(fused):
-    """Option costs above the halo capacity (TURBO_BIG_MAX_COST = 2048 cells) take the L2-row path
+    """Option costs above the halo capacity (TURBO_BIG_MAX_COST cells) take the L2-row path
     (rows in global memory, a grid barrier per frame) -- planned exactly, no longer rejected
     (reading R17). The batch mixes such windows with halo-path windows, K fixed and mixed."""
     parts = [synth.make_long_window(7, N=30, K=4, B=30000, c_max=5000),
-             synth.make_long_window(8, N=41, K=6, B=60000, c_max=2049, random_rows=True),
+             synth.make_long_window(8, N=41, K=6, B=60000, c_max=4097, random_rows=True),
              synth.make_long_window(9, N=25, K=5, B=40000, c_max=900, random_rows=True),
              synth.make_long_window(10, N=17, K=3, B=27000, c_max=26000, random_rows=True)]
     wl = synth.concat_workloads(parts)
