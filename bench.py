@@ -458,6 +458,9 @@ def run_turbo(args):
         dist = dist_mod
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if rank == 0:
+            print(f"[bench] NCCL communicator: {dist.get_world_size()} ranks (backend {dist.get_backend()})",
+                  file=sys.stderr, flush=True)
     else:
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -678,6 +681,7 @@ def run_turbo(args):
                             "plan": "lookup + plan + backtrack + stats"}[path],
                    "l2": "flushed between timed steps (256 MiB write outside the step events)",
                    "parallelism": f"{args.scaling} dp{N} (windows sharded, NCCL allreduce of stats)",
+                   "nccl_ranks": (dist.get_world_size() if dist is not None else 1),
                    "windows_total": W_total},
         "windows_per_s": W_total / t_step,
         "dp_ms": t_dp * 1e3,

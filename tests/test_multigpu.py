@@ -82,3 +82,40 @@ def test_rank_shards_regenerate_identically():
     whole = synth.make_config(3, num_windows=40)
     part = synth.make_config(3, window_offset=16, num_windows=8)
     np.testing.assert_array_equal(part.class_id, whole.subset(16, 24).class_id)
+
+
+def _strong_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import bench
+    # strong scaling as in bench.py --scaling strong: the config's whole window set, work-balanced
+    wl = bench.make_workload("c2", rank, world, "strong")
+    out = oracle.run(wl, threads=1)
+    stats = torch.from_numpy(out["stats"].copy())
+    dist.all_reduce(stats)
+    n = torch.tensor([wl.num_windows, wl.total_cells], dtype=torch.int64)
+    dist.all_reduce(n)
+    if rank == 0:
+        q.put((stats.numpy().copy(), n.tolist()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_strong_scaling_split_covers_config():
+    """bench.py --scaling strong on 2 ranks: the shards partition config c2's 1024 windows, and the
+    allreduced statistics equal a single run over the whole config."""
+    world = 2
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_strong_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    stats, n = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    whole = synth.make_config(2)
+    assert n == [whole.num_windows, whole.total_cells]
+    np.testing.assert_array_equal(stats, oracle.run(whole, threads=4)["stats"])
