@@ -238,6 +238,22 @@ turbo_status_t turbo_schedule(const turbo_shape_t *shape /* host */, const turbo
                               uint8_t *exit_out, int64_t *stats, int64_t *status, turbo_stream_t stream);
 
 /* ---------------------------------------------------------------------------
+ * NEXT-3 fused: turbo_schedule taking the discriminator's difficulty scores theta'_x (PAPER.md:525
+ * "theta'_x from D_f") instead of class ids. Every kernel that reads a frame's class derives it
+ * from its score exactly as turbo_bucketize does (PAPER.md:511 buckets of width bucket_width on
+ * d = 1 - theta, reading R6; IEEE float32 decision, NaN -> 0), clamped to the window's profile's
+ * C classes, and the DP launch writes the classes to class_out (u8 [total_frames], caller-owned;
+ * the walk / statistics kernels read them there). theta: float32 [total_frames]. Outputs are
+ * bit-identical to turbo_bucketize -> turbo_schedule with num_classes = C. Other arguments,
+ * launches and errors as turbo_schedule. */
+turbo_status_t turbo_schedule_theta(const turbo_shape_t *shape /* host */, const turbo_profile_t *profiles,
+                                    turbo_window_t *windows, const float *theta, float bucket_width,
+                                    uint8_t *class_out, const int32_t *capacity /* nullable */, int32_t base_cost,
+                                    void *workspace, size_t workspace_bytes, int32_t *best_gain,
+                                    int32_t *best_cost, uint8_t *feasible, uint8_t *exit_out, int64_t *stats,
+                                    int64_t *status, turbo_stream_t stream);
+
+/* ---------------------------------------------------------------------------
  * NEXT-1 (comparison arm): the paper's own scheduler, prune-and-search (PAPER.md:539-545,
  * §5.2), on the option tables of turbo_profile_lookup: all frames start at level K-1; while the
  * cost sum_i c_{i,k_i} exceeds the budget, the frame with the minimal marginal gain
@@ -266,9 +282,17 @@ turbo_status_t turbo_bucketize(const float *theta, int64_t num_frames, int32_t n
  * count_out[16 w + k] = n_k, the number of frames planned at level k; order_out[first_frame_w
  * + j] = window-local frame indices grouped by level ascending, arrival order inside a level
  * (a stable partition; the batch of level k starts at sum_{k' < k} n_k'). exit_out: the plan
- * (u8 [total_frames]); count_out: int32 [16 W]; order_out: int32 [total_frames]. */
+ * (u8 [total_frames]); count_out: int32 [16 W]; order_out: int32 [total_frames].
+ * Executed latency (optional, latency_out != NULL): latency_out[w] = f = sum_{k < K_w} I_k(n_k),
+ * the GPU time of running the window's batches (PAPER.md:525 f(.) of the constraint), with I_k(n)
+ * from batch_cost in the layout of turbo_batched_plan (profile p at p * 16 * (batch_cap + 1),
+ * row k = I_k(0 .. batch_cap)); int64 [W]. A window with some n_k > batch_cap gets latency -1 and
+ * sets status[1] (min window index; int64[2], required with latency_out). With linear tables
+ * (I_k(n) = n c_k) f is the plan's summed per-frame cost (reading R1). */
 turbo_status_t turbo_batches(const turbo_shape_t *shape /* host */, const turbo_window_t *windows,
                              const uint8_t *exit_out, int32_t *count_out, int32_t *order_out,
+                             const int32_t *batch_cost /* nullable */, int32_t batch_cap,
+                             int64_t *latency_out /* nullable */, int64_t *status /* nullable */,
                              turbo_stream_t stream);
 
 /* ---------------------------------------------------------------------------

@@ -167,6 +167,22 @@ def batches(num_frames, exits):
     return count[:W * 16].reshape(W, 16), order[:F]
 
 
+def batch_latency(count16, num_exits, profile, profiles_batch, ncap: int) -> np.ndarray:
+    """NEXT-2 executed latency per window: sum_k I_k(n_k) over the window's levels (PAPER.md:525);
+    profiles_batch[p] = int32 [K_p * (ncap + 1)] (row k = I_k(0..ncap)); -1 when some n_k > ncap."""
+    lib = _load()
+    cnt = np.ascontiguousarray(count16, dtype=np.int32).reshape(-1)
+    W = len(cnt) // 16
+    tabs = np.concatenate([_i32(t) for t in profiles_batch])
+    sz = np.array([len(t) for t in profiles_batch], dtype=np.int64)
+    off = np.zeros(len(sz), dtype=np.int64)
+    off[1:] = np.cumsum(sz[:-1])
+    out = np.zeros(max(W, 1), dtype=np.int64)
+    lib.oracle_batch_latency(ctypes.c_int32(W), _p(cnt), _p(_i32(num_exits)), _p(tabs), _p(off), _p(_i32(profile)),
+                             ctypes.c_int32(int(ncap)), _p(out))
+    return out[:W]
+
+
 def stats(num_frames, class_id, exits, best_gain, best_cost, feasible) -> np.ndarray:
     lib = _load()
     out = np.zeros(181, dtype=np.int64)

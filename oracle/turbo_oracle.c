@@ -415,6 +415,28 @@ void oracle_batches(int32_t num_windows, const int32_t *num_frames, const uint8_
     }
 }
 
+/* NEXT-2, executed latency (f "organize[s] the frames assigned by the same enhancement
+ * level to execute in a batch"): f = sum over the levels k < K of I_k(n_k), the batch latency of the
+ * n_k frames planned at level k (table I[k * (ncap + 1) + n]). A count above ncap: -1. */
+void oracle_batch_latency(int32_t num_windows, const int32_t *count16, const int32_t *num_exits,
+                          const int32_t *tables, const int64_t *table_off, const int32_t *profile, int32_t ncap,
+                          int64_t *latency)
+{
+    for (int32_t w = 0; w < num_windows; ++w) {
+        const int32_t *I = tables + table_off[profile[w]];
+        int64_t f = 0;
+        for (int32_t k = 0; k < num_exits[w]; ++k) {
+            const int32_t n = count16[(int64_t)w * 16 + k];
+            if (n > ncap) {
+                f = -1;
+                break;
+            }
+            f += I[(int64_t)k * (ncap + 1) + n];
+        }
+        latency[w] = f;
+    }
+}
+
 /* ------------------------------------------------------------------ NEXT-4: batched-cost GAP
  * PAPER.md:523-525 (§5.2): maximise sum_x P_{kappa_x}^{theta'_x} subject to f(sum I_kappa) <= T,
  * where f batches the frames that run at the same level; PAPER.md:533 calls it a non-linear GAP.

@@ -567,10 +567,12 @@ turbo_status_t turbo_mckp_solve(const turbo_shape_t *shape, const turbo_window_t
                   stream);
 }
 
-turbo_status_t turbo_schedule(const turbo_shape_t *shape, const turbo_profile_t *profiles, turbo_window_t *windows,
-                              const uint8_t *class_id, const int32_t *capacity, int32_t base_cost, void *workspace,
-                              size_t workspace_bytes, int32_t *best_gain, int32_t *best_cost, uint8_t *feasible,
-                              uint8_t *exit_out, int64_t *stats, int64_t *status, turbo_stream_t stream)
+static turbo_status_t schedule_impl(const turbo_shape_t *shape, const turbo_profile_t *profiles,
+                                    turbo_window_t *windows, const uint8_t *class_id, const float *theta,
+                                    float inv_width, uint8_t *class_out, const int32_t *capacity, int32_t base_cost,
+                                    void *workspace, size_t workspace_bytes, int32_t *best_gain, int32_t *best_cost,
+                                    uint8_t *feasible, uint8_t *exit_out, int64_t *stats, int64_t *status,
+                                    turbo_stream_t stream)
 {
     if (!shape) return TURBO_ERR_INVALID_ARG;
     if (shape->num_windows == 0) return TURBO_OK;
@@ -585,11 +587,37 @@ turbo_status_t turbo_schedule(const turbo_shape_t *shape, const turbo_profile_t 
     P.windows_rw = windows;
     P.profiles = profiles;
     P.class_id = class_id;
+    P.theta = theta;
+    P.inv_width = inv_width;
+    P.class_out = class_out;
     P.capacity = capacity;
     P.base_cost = base_cost;
     P.fuse = 1;
     P.stats = stats;
     return run_dp(shape, RUN_SCHEDULE, P, stream);
+}
+
+turbo_status_t turbo_schedule(const turbo_shape_t *shape, const turbo_profile_t *profiles, turbo_window_t *windows,
+                              const uint8_t *class_id, const int32_t *capacity, int32_t base_cost, void *workspace,
+                              size_t workspace_bytes, int32_t *best_gain, int32_t *best_cost, uint8_t *feasible,
+                              uint8_t *exit_out, int64_t *stats, int64_t *status, turbo_stream_t stream)
+{
+    return schedule_impl(shape, profiles, windows, class_id, nullptr, 0.0f, nullptr, capacity, base_cost, workspace,
+                         workspace_bytes, best_gain, best_cost, feasible, exit_out, stats, status, stream);
+}
+
+turbo_status_t turbo_schedule_theta(const turbo_shape_t *shape, const turbo_profile_t *profiles,
+                                    turbo_window_t *windows, const float *theta, float bucket_width,
+                                    uint8_t *class_out, const int32_t *capacity, int32_t base_cost, void *workspace,
+                                    size_t workspace_bytes, int32_t *best_gain, int32_t *best_cost,
+                                    uint8_t *feasible, uint8_t *exit_out, int64_t *stats, int64_t *status,
+                                    turbo_stream_t stream)
+{
+    if (!(bucket_width > 0.0f)) return TURBO_ERR_INVALID_ARG;
+    if (shape && shape->total_frames > 0 && (!theta || !class_out)) return TURBO_ERR_INVALID_ARG;
+    const float inv = 1.0f / bucket_width;             // rounded to float32 once, as turbo_bucketize
+    return schedule_impl(shape, profiles, windows, class_out, theta, inv, class_out, capacity, base_cost, workspace,
+                         workspace_bytes, best_gain, best_cost, feasible, exit_out, stats, status, stream);
 }
 
 turbo_status_t turbo_heuristic_plan(const turbo_shape_t *shape, const turbo_window_t *windows,
@@ -655,15 +683,18 @@ turbo_status_t turbo_bucketize(const float *theta, int64_t num_frames, int32_t n
 }
 
 turbo_status_t turbo_batches(const turbo_shape_t *shape, const turbo_window_t *windows, const uint8_t *exit_out,
-                             int32_t *count_out, int32_t *order_out, turbo_stream_t stream)
+                             int32_t *count_out, int32_t *order_out, const int32_t *batch_cost, int32_t batch_cap,
+                             int64_t *latency_out, int64_t *status, turbo_stream_t stream)
 {
     if (!shape) return TURBO_ERR_INVALID_ARG;
     if (shape->num_windows == 0) return TURBO_OK;
     if (!windows || !count_out) return TURBO_ERR_INVALID_ARG;
     if (shape->total_frames > 0 && (!exit_out || !order_out)) return TURBO_ERR_INVALID_ARG;
+    if (latency_out && (!batch_cost || !status || batch_cap < 0 || batch_cap > 65535)) return TURBO_ERR_INVALID_ARG;
     DeviceInfo d;
     if (device_info(&d) != cudaSuccess) return TURBO_ERR_CUDA;
-    cudaError_t e = launch_batches(windows, shape->num_windows, exit_out, count_out, order_out, d.num_sms,
+    cudaError_t e = launch_batches(windows, shape->num_windows, exit_out, count_out, order_out,
+                                   latency_out ? batch_cost : nullptr, batch_cap, latency_out, status, d.num_sms,
                                    (cudaStream_t)stream);
     return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
 }

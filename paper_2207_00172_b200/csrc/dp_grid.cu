@@ -330,12 +330,12 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
     }
     auto opt_g = [&](int32_t i, int32_t k) -> int32_t {
         if (!fuse) return __ldg(og + (int64_t)i * K + k);
-        const int32_t cls = P.class_id[ff + i];
+        const int32_t cls = frame_class(P, ff + i, prof_C);
         return cls < prof_C ? __ldg(prof_g + cls * K + k) : 0;
     };
     auto opt_c = [&](int32_t i, int32_t k) -> int32_t {
         if (!fuse) return __ldg(oc + (int64_t)i * K + k);
-        const int32_t cls = P.class_id[ff + i];
+        const int32_t cls = frame_class(P, ff + i, prof_C);
         return cls < prof_C ? __ldg(prof_c + cls * K + k) : 0;
     };
     uint32_t *__restrict__ gch = reinterpret_cast<uint32_t *>(P.workspace + win->choice_offset);
@@ -355,7 +355,11 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
         long long bad = 0, cmax = 0, g0 = 0, c0 = 0, asum = 0;
         for (int32_t i = j * nthr + tid; i < N; i += NP * nthr) {
             int32_t m = 0;
-            if (fuse && (int32_t)P.class_id[ff + i] >= prof_C) atomic_min_i64(&P.status[0], ff + i);
+            if (fuse) {
+                const int32_t cls = frame_class(P, ff + i, prof_C);
+                if (cls >= prof_C) atomic_min_i64(&P.status[0], ff + i);
+                if (P.theta != nullptr) P.class_out[ff + i] = (uint8_t)cls;    // NEXT-3 fused, for the walk
+            }
             for (int k = 0; k < K; ++k) {
                 const int32_t g = opt_g(i, k);
                 const int32_t c = opt_c(i, k);

@@ -531,7 +531,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     }
     auto load_opt = [&](int32_t i, int32_t k, int32_t &g, int32_t &c) {
         if (FUSE) {
-            const int32_t cls = P.class_id[ff + i];
+            const int32_t cls = frame_class(P, ff + i, prof_C);
             if (cls < prof_C) {
                 g = __ldg(prof_g + cls * K + k);
                 c = __ldg(prof_c + cls * K + k);
@@ -546,7 +546,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     };
     auto class_of = [&](int32_t i) -> uint32_t {               // fused statistics only
         return OSM ? reinterpret_cast<const uint8_t *>(opt_s + P.max_options + P.prof_entries)[i]
-                   : (uint32_t)P.class_id[ff + i];
+                   : (uint32_t)frame_class(P, ff + i, prof_C);
     };
 
     if (FUSE) {
@@ -557,6 +557,8 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
             if (tid == 0) P.windows_rw[w].budget = B;
         }
         for (int x = tid; x < 176; x += nthr) hist[x] = 0;
+        if (P.theta != nullptr)                           // NEXT-3 fused: the classes, for the walk / stats
+            for (int32_t x = tid; x < N; x += nthr) P.class_out[ff + x] = (uint8_t)frame_class(P, ff + x, prof_C);
     }
 
     // ---- prologue: stage options (OSM), validate, sums for the infeasible report (reading R8)
@@ -573,7 +575,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
             const int32_t *__restrict__ pc = pr.cost;
             int2 *__restrict__ prof_s = opt_s + P.max_options;
             uint8_t *__restrict__ cls_s = reinterpret_cast<uint8_t *>(prof_s + P.prof_entries);
-            for (int32_t x = tid; x < N; x += nthr) cls_s[x] = P.class_id[ff + x];
+            for (int32_t x = tid; x < N; x += nthr) cls_s[x] = (uint8_t)frame_class(P, ff + x, C);
             for (int32_t x = tid; x < C * K; x += nthr) prof_s[x] = make_int2(__ldg(pg + x), __ldg(pc + x));
             if (nwarps > 1) __syncthreads(); else __syncwarp();
             for (int32_t o = tid; o < n_opt; o += nthr) {
@@ -619,7 +621,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
                 } else {
                     load_opt(i, k, g, c);
                     bad |= (c < 0) || (c >= (1 << 30)) || (g > (1 << 24)) || (g < -(1 << 24));
-                    if (FUSE && k == 0 && (int32_t)P.class_id[ff + i] >= prof_C)
+                    if (FUSE && k == 0 && frame_class(P, ff + i, prof_C) >= prof_C)
                         atomic_min_i64(&P.status[0], ff + i);
                 }
                 const int32_t a = g < 0 ? -g : g;
@@ -690,7 +692,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     const int lq = lane / K, lk = lane - (lane / K) * K;
     auto load_cls = [&](int32_t hi) -> int32_t {               // frames hi, hi-1, ... of a chunk
         const int32_t i = hi - lq;
-        return (FUSE && lq < CH && i >= 0) ? (int32_t)P.class_id[ff + i] : 0;
+        return (FUSE && lq < CH && i >= 0) ? frame_class(P, ff + i, prof_C) : 0;
     };
     auto load_raw = [&](int32_t hi, int32_t cls, int32_t &g, int32_t &c, bool &ok) {
         const int32_t i = hi - lq;
@@ -872,10 +874,12 @@ __device__ __forceinline__ void dp_window_gen(const DpParams &P, int64_t w, cons
             B = (int32_t)(b < 0 ? 0 : (b > 0x7fffffffll ? 0x7fffffff : b));
             if (tid == 0) P.windows_rw[w].budget = B;
         }
+        if (P.theta != nullptr)          // NEXT-3 fused: the classes, for the walk / stats kernels
+            for (int32_t x = tid; x < N; x += nthr) P.class_out[ff + x] = (uint8_t)frame_class(P, ff + x, prof_C);
     }
     auto load_opt = [&](int32_t i, int32_t k, int32_t &g, int32_t &c) {
         if (FUSE) {                      // a2: the profile row of the frame's class (zero row for >= C)
-            const int32_t cls = P.class_id[ff + i];
+            const int32_t cls = frame_class(P, ff + i, prof_C);
             g = cls < prof_C ? __ldg(prof_g + cls * K + k) : 0;
             c = cls < prof_C ? __ldg(prof_c + cls * K + k) : 0;
         } else {
@@ -899,7 +903,7 @@ __device__ __forceinline__ void dp_window_gen(const DpParams &P, int64_t w, cons
         int64_t abs_sum = 0, g0_sum = 0, c0_sum = 0;
         for (int32_t i = lane; i < N; i += 32) {
             int32_t m = 0;
-            if (FUSE && (int32_t)P.class_id[ff + i] >= prof_C) atomic_min_i64(&P.status[0], ff + i);
+            if (FUSE && frame_class(P, ff + i, prof_C) >= prof_C) atomic_min_i64(&P.status[0], ff + i);
             for (int k = 0; k < K; ++k) {
                 int32_t g, c;
                 if (OSM) {

@@ -96,7 +96,11 @@ __global__ void __launch_bounds__(1024, 1) dp_pack_kernel(DpParams P)
         for (int v = 0; v < nv; ++v) {
             const turbo_profile_t &pr = P.profiles[ws[v].prof];
             const int32_t C = pr.num_classes;
-            for (int32_t x = tid; x < ws[v].N; x += nthr) clss(v)[x] = P.class_id[ws[v].ff + x];
+            for (int32_t x = tid; x < ws[v].N; x += nthr) {
+                const uint8_t c = (uint8_t)frame_class(P, ws[v].ff + x, C);
+                clss(v)[x] = c;
+                if (P.theta != nullptr) P.class_out[ws[v].ff + x] = c;      // NEXT-3 fused
+            }
             for (int32_t x = tid; x < C * K; x += nthr) profs(v)[x] = make_int2(__ldg(pr.gain + x), __ldg(pr.cost + x));
         }
         __syncthreads();

@@ -7,24 +7,13 @@
 // round-to-nearest intrinsics (no contraction), exactly as the oracle does.
 //
 // NEXT-2 (after): the plan -> per-exit batches ("organize the frames assigned by the
-// same enhancement level to execute in a batch", :545): per window the batch sizes n_k and a
-// stable partition of the window's frames by exit level. One warp per window; per 32-frame chunk
-// and level, a ballot ranks the frames (arrival order preserved).
+// same enhancement level to execute in a batch", :545): per window the batch sizes n_k, a stable
+// partition of the window's frames by exit level, and (optionally) the executed latency
+// f = sum_k I_k(n_k) of those batches. One warp per window; per 32-frame chunk and level, a ballot
+// ranks the frames (arrival order preserved).
 #include "turbo_internal.cuh"
 
 namespace turbo {
-
-__device__ __forceinline__ uint32_t bucket_of(float theta, float inv_width, int C)
-{
-    const float d = __fsub_rn(1.0f, theta);
-    const float q = __fmul_rn(d, inv_width);
-    int c = 0;
-    if (q >= (float)C)
-        c = C - 1;
-    else if (q >= 0.0f)
-        c = (int)floorf(q);                          // NaN fails both tests -> class 0
-    return (uint32_t)min(c, C - 1);
-}
 
 __global__ void __launch_bounds__(256) bucketize_kernel(const float *__restrict__ theta, int64_t n, float inv_width,
                                                         int C, uint8_t *__restrict__ cls)
@@ -57,7 +46,9 @@ cudaError_t launch_bucketize(const float *theta, int64_t n, int32_t C, float inv
 
 __global__ void __launch_bounds__(256) batches_kernel(const turbo_window_t *__restrict__ windows, int32_t num_windows,
                                                       const uint8_t *__restrict__ exit_out, int32_t *__restrict__ count,
-                                                      int32_t *__restrict__ order)
+                                                      int32_t *__restrict__ order, const int32_t *__restrict__ batch,
+                                                      int32_t cap, int64_t *__restrict__ latency,
+                                                      int64_t *__restrict__ status)
 {
     const int lane = threadIdx.x & 31;
     const int wpc = blockDim.x >> 5;
@@ -77,6 +68,20 @@ __global__ void __launch_bounds__(256) batches_kernel(const turbo_window_t *__re
             }
         }
         if (lane < 16) count[w * 16 + lane] = mine;
+        if (latency != nullptr) {
+            // executed latency f = sum_k I_k(n_k): lane k < K reads its level's table
+            const int32_t K = windows[w].num_exits;
+            const int64_t tab = (int64_t)windows[w].profile * 16 * (cap + 1);
+            const bool over = lane < K && mine > cap;
+            int64_t v = (lane < K && !over) ? (int64_t)batch[tab + (int64_t)lane * (cap + 1) + mine] : 0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            const bool bad = __any_sync(0xffffffffu, over);
+            if (lane == 0) {
+                latency[w] = bad ? -1 : v;
+                if (bad) atomic_min_i64(&status[1], w);
+            }
+        }
         // exclusive prefix over levels -> base offset of each batch
         int32_t base = mine;
 #pragma unroll
@@ -102,13 +107,15 @@ __global__ void __launch_bounds__(256) batches_kernel(const turbo_window_t *__re
 }
 
 cudaError_t launch_batches(const turbo_window_t *windows, int32_t num_windows, const uint8_t *exit_out,
-                           int32_t *count, int32_t *order, int num_sms, cudaStream_t stream)
+                           int32_t *count, int32_t *order, const int32_t *batch_cost, int32_t batch_cap,
+                           int64_t *latency, int64_t *status, int num_sms, cudaStream_t stream)
 {
     if (num_windows <= 0) return cudaSuccess;
     int64_t blocks = ((int64_t)num_windows + 7) / 8;
     if (blocks > (int64_t)num_sms * 16) blocks = (int64_t)num_sms * 16;
     note_launch();
-    batches_kernel<<<(unsigned)blocks, 256, 0, stream>>>(windows, num_windows, exit_out, count, order);
+    batches_kernel<<<(unsigned)blocks, 256, 0, stream>>>(windows, num_windows, exit_out, count, order, batch_cost,
+                                                         batch_cap, latency, status);
     return cudaGetLastError();
 }
 

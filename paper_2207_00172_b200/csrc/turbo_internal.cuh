@@ -104,7 +104,34 @@ struct DpParams {
     int32_t pack_stride;
     int32_t generic;               // mixed-K plan-mode launch: the runtime-K kernel (dp_gen.cu)
     int32_t grid_max_budget;       // long-window kernel: largest budget bound (L2-row path row size)
+    // turbo_schedule_theta (NEXT-3 fused): classes from the difficulty scores, written to class_out
+    const float *theta;
+    float inv_width;
+    uint8_t *class_out;
 };
+
+// NEXT-3 (PAPER.md:511 buckets of width 0.1; :525 theta'_x from D_f; reading R6): the class of a
+// difficulty score = the bucket of d = 1 - theta, clamped to [0, C-1], decided in IEEE float32 with
+// explicit round-to-nearest operations (no contraction); NaN -> class 0.
+__device__ __forceinline__ uint32_t bucket_of(float theta, float inv_width, int C)
+{
+    const float d = __fsub_rn(1.0f, theta);
+    const float q = __fmul_rn(d, inv_width);
+    int c = 0;
+    if (q >= (float)C)
+        c = C - 1;
+    else if (q >= 0.0f)
+        c = (int)floorf(q);                          // NaN fails both tests -> class 0
+    return (uint32_t)min(c, C - 1);
+}
+
+// The class of frame idx of a fused launch (turbo_schedule: the class-id input; turbo_schedule_theta:
+// the bucket of its score under the window's profile's C classes)
+__device__ __forceinline__ int32_t frame_class(const DpParams &P, int64_t idx, int32_t C)
+{
+    if (P.theta != nullptr) return (int32_t)bucket_of(__ldg(P.theta + idx), P.inv_width, C);
+    return (int32_t)P.class_id[idx];
+}
 
 // turbo_debug_trace: %globaltimer at phase p of window w (thread 0 of the window's CTA). Compiled
 // in only with -DTURBO_TRACE (TURBO_TRACE=1 python -m paper_2207_00172_b200.build): the marks
@@ -180,7 +207,8 @@ cudaError_t launch_heuristic(const turbo_shape_t *shape, const turbo_window_t *w
 cudaError_t launch_bucketize(const float *theta, int64_t n, int32_t C, float inv_width, uint8_t *cls, int num_sms,
                              cudaStream_t stream);
 cudaError_t launch_batches(const turbo_window_t *windows, int32_t num_windows, const uint8_t *exit_out,
-                           int32_t *count, int32_t *order, int num_sms, cudaStream_t stream);
+                           int32_t *count, int32_t *order, const int32_t *batch_cost, int32_t batch_cap,
+                           int64_t *latency, int64_t *status, int num_sms, cudaStream_t stream);
 // lockstep multi-window kernel for short-row single-class batches (dp_pack.cu)
 bool pack_geometry(const turbo_shape_t *s, const DpParams &P, int num_sms, int smem_per_cta_max, int *V_out,
                    int *T_out, int *warps_out, size_t *smem_out);

@@ -63,7 +63,8 @@ WINDOW_DTYPE = np.dtype([("first_frame", "<i8"), ("first_option", "<i8"), ("choi
 assert WINDOW_DTYPE.itemsize == 48
 
 EXPORTS = ["turbo_mckp_workspace", "turbo_profile_lookup", "turbo_mckp_plan", "turbo_backtrack",
-           "turbo_mckp_solve", "turbo_mckp_solve_workspace", "turbo_mckp_plane_bytes", "turbo_schedule", "turbo_heuristic_plan", "turbo_stats",
+           "turbo_mckp_solve", "turbo_mckp_solve_workspace", "turbo_mckp_plane_bytes", "turbo_schedule",
+           "turbo_schedule_theta", "turbo_heuristic_plan", "turbo_stats",
            "turbo_bucketize", "turbo_batches", "turbo_batched_plan",
            "turbo_debug_set_variant", "turbo_debug_trace", "turbo_debug_smem_stream", "turbo_launch_count",
            "turbo_status_string", "turbo_abi_version"]
@@ -90,9 +91,11 @@ def load(path: Optional[str] = None):
     lib.turbo_mckp_plane_bytes.argtypes = [vp, vp, i32, vp]
     lib.turbo_stats.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.turbo_schedule.argtypes = [vp, vp, vp, vp, vp, i32, vp, sz, vp, vp, vp, vp, vp, vp, vp]
+    lib.turbo_schedule_theta.argtypes = [vp, vp, vp, vp, ctypes.c_float, vp, vp, i32, vp, sz, vp, vp, vp, vp, vp, vp,
+                                         vp]
     lib.turbo_heuristic_plan.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.turbo_bucketize.argtypes = [vp, i64, i32, ctypes.c_float, vp, vp]
-    lib.turbo_batches.argtypes = [vp, vp, vp, vp, vp, vp]
+    lib.turbo_batches.argtypes = [vp, vp, vp, vp, vp, vp, i32, vp, vp, vp]
     lib.turbo_batched_plan.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp]
     lib.turbo_debug_set_variant.argtypes = [i32]
     lib.turbo_debug_trace.argtypes = [vp, i64]
@@ -196,6 +199,17 @@ def schedule(shape, profiles_dev, windows_dev, class_id, capacity, base_cost, wo
                                  _stream(stream)))
 
 
+def schedule_theta(shape, profiles_dev, windows_dev, theta, bucket_width, class_out, capacity, base_cost, workspace,
+                   best_gain, best_cost, feasible, exit_out, stats_out, status, stream=None):
+    """NEXT-3 fused: turbo_schedule on difficulty scores (float32, device); classes written to class_out."""
+    nbytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
+    _check("turbo_schedule_theta",
+           load().turbo_schedule_theta(ctypes.addressof(shape), _ptr(profiles_dev), _ptr(windows_dev), _ptr(theta),
+                                       float(bucket_width), _ptr(class_out), _ptr(capacity), int(base_cost),
+                                       _ptr(workspace), nbytes, _ptr(best_gain), _ptr(best_cost), _ptr(feasible),
+                                       _ptr(exit_out), _ptr(stats_out), _ptr(status), _stream(stream)))
+
+
 def heuristic_plan(shape, windows_dev, opt_gain, opt_cost, gain_out, cost_out, feasible, exit_out, steps=None,
                    stream=None):
     """NEXT-1: the paper's prune-and-search heuristic on the option tables (comparison arm)."""
@@ -231,11 +245,14 @@ def bucketize(theta, class_out, num_classes: int = 10, bucket_width: float = 0.1
                                   _ptr(class_out), _stream(stream)))
 
 
-def batches(shape, windows_dev, exit_out, count_out, order_out, stream=None):
-    """NEXT-2: plan -> per-exit batch sizes [W, 16] and stable per-exit frame order."""
+def batches(shape, windows_dev, exit_out, count_out, order_out, batch_cost=None, batch_cap=0, latency_out=None,
+            status=None, stream=None):
+    """NEXT-2: plan -> per-exit batch sizes [W, 16], stable per-exit frame order and (with batch_cost
+    and latency_out) the executed latency sum_k I_k(n_k) per window."""
     _check("turbo_batches",
            load().turbo_batches(ctypes.addressof(shape), _ptr(windows_dev), _ptr(exit_out), _ptr(count_out),
-                                _ptr(order_out), _stream(stream)))
+                                _ptr(order_out), _ptr(batch_cost), int(batch_cap), _ptr(latency_out), _ptr(status),
+                                _stream(stream)))
 
 
 def stats(shape, windows_dev, class_id, exit_out, best_gain, best_cost, feasible, stats_out, stream=None):
