@@ -562,8 +562,8 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
             const uint32_t pub_tag = (uint32_t)(sb + f + 1);
             const int32_t pub_lo = seg_lo + seg - hl8;                 // first published cell
             unsigned long long *stg = stage_out + (f & 1) * H;         // two publication stages
-            const unsigned long long *halo_src =
-                X.ring + ((int64_t)((sb + f - 1) % D) * GRID_MAX_CTAS + (j - 1)) * H;
+            const unsigned long long *halo_src =                       // (sb >= 1: no signed modulo)
+                X.ring + ((int64_t)((sb + f - 1) & (D - 1)) * GRID_MAX_CTAS + (j - 1)) * H;
             if (need_halo && tid == 0) tma_load_1d(stage_in, halo_src, hl8 * 8, mbar);
             auto do_tile = [&](int32_t t) {
                 const int32_t b_lo = t * RPT * 32;
@@ -600,7 +600,7 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
                         atomic_min_i64(&status[1], w);
                         atomicOr(reinterpret_cast<unsigned long long *>(&X.misc[7]), 1ull);   // window failed
                     }
-                    unsigned long long *dst = X.ring + ((int64_t)(slot_step % D) * GRID_MAX_CTAS + j) * H;
+                    unsigned long long *dst = X.ring + ((int64_t)(slot_step & (D - 1)) * GRID_MAX_CTAS + j) * H;
                     tma_store_1d(dst, stg, hl8 * 8);
                     if (trace) X.trace[j * 8 + 2] += clock64() - c0;
                 }
