@@ -222,10 +222,40 @@ def batched_brute(cls, gain, C, K, batch, ncap, B):
     return int(bg.value), int(bc.value), cnt[:K].copy(), int(fe.value)
 
 
+def _batched_one(fn, cls, gain, C, K, batch, ncap, B):
+    lib = _load()
+    cl = np.ascontiguousarray(cls, dtype=np.uint8)
+    ex = np.zeros(max(len(cl), 1), dtype=np.uint8)
+    bg, bc = ctypes.c_int64(0), ctypes.c_int64(0)
+    fe = ctypes.c_uint8(0)
+    e = getattr(lib, fn)(ctypes.c_int32(len(cl)), ctypes.c_int32(C), ctypes.c_int32(K), _p(cl), _p(_i32(gain)),
+                         _p(_i32(batch)), ctypes.c_int32(ncap), ctypes.c_int32(int(B)), _p(ex), ctypes.byref(bg),
+                         ctypes.byref(bc), ctypes.byref(fe))
+    if e:
+        raise RuntimeError(f"{fn} failed: {e}")
+    return ex[:len(cl)].copy(), int(bg.value), int(bc.value), int(fe.value)
+
+
+def batched_dp(cls, gain, C, K, batch, ncap, B):
+    """NEXT-4 for any gain table (reading R20), one window: the DP over the canonical prefix and its
+    count vector (turbo_oracle.c oracle_batched_dp). Returns (exits, G*, C*, feasible)."""
+    return _batched_one("oracle_batched_dp", cls, gain, C, K, batch, ncap, B)
+
+
+def batched_brute_plan(cls, gain, C, K, batch, ncap, B):
+    """The R20 plan by its definition over all K^N plans (N <= 12). Returns (exits, G*, C*, feasible)."""
+    return _batched_one("oracle_batched_brute_plan", cls, gain, C, K, batch, ncap, B)
+
+
+def batched_enum(cls, gain, C, K, batch, ncap, B):
+    """NEXT-4 under R19 (count vectors + canonical assignment), one window; raises on an R19 violation."""
+    return _batched_one("oracle_batched_enum", cls, gain, C, K, batch, ncap, B)
+
+
 def batched(wl):
     """NEXT-4 on a batched workload (synth profiles_batch): exact optimum per window by
-    count-vector enumeration (turbo_oracle.c oracle_batched_enum). Returns (exits, G*, C*,
-    feasible)."""
+    count-vector enumeration (turbo_oracle.c oracle_batched_enum) when the gains satisfy R19, else
+    by the general program (oracle_batched_dp, reading R20). Returns (exits, G*, C*, feasible)."""
     lib = _load()
     gain = np.concatenate([_i32(g) for g in wl.profiles_gain])
     gsz = np.array([len(g) for g in wl.profiles_gain], dtype=np.int64)

@@ -620,6 +620,193 @@ int oracle_batched_enum(int32_t N, int32_t C, int32_t K, const uint8_t *cls, con
 }
 
 /* windows of a batch (one table pair per window via profile index) */
+/* ------------------------------------------------------------------ NEXT-4 for ANY gain table
+ * Reading R20: without R19 the canonical assignment need not be optimal for its counts,
+ * so the gain of a count vector n is the transportation optimum
+ *     gain(n) = max { sum_x g[c_x][kappa_x] : #{x : kappa_x = k} = n_k for every k }.
+ * The count vector is chosen as in R18 (larger gain, then smaller cost, then (n_{K-1}, .., n_0)
+ * lexicographically smaller). The assignment: frames in canonical order (class, then arrival)
+ * x_0 .. x_{N-1}; going BACKWARDS from x_{N-1}, each frame takes the highest level k that still
+ * admits an optimal completion. (Under R19 this is R18's canonical assignment: the canonical plan is
+ * optimal, and its last frame sits on the highest used level.)
+ *
+ * Plain algorithm: dynamic program over the canonical prefix x_0 .. x_{j-1} and the count vector m
+ * of that prefix (total j):  F_0(0) = 0,
+ *     F_{j+1}(m) = max over k with m_k > 0 of F_j(m - e_k) + g[c_{x_j}][k],
+ * so F_N(n) = gain(n). Count vectors are stored in a dense mixed-radix table (index
+ * sum_{k>=1} m_k (N+1)^(k-1); m_0 is implied by the total) -- small windows only (tests).
+ * Return: 0 ok; -1 bad arguments or table too large. */
+static int64_t bdp_index(int32_t K, int32_t N, const int32_t *m)
+{
+    int64_t idx = 0, mul = 1;
+    for (int32_t k = 1; k < K; ++k) {
+        idx += (int64_t)m[k] * mul;
+        mul *= (N + 1);
+    }
+    return idx;
+}
+
+int oracle_batched_dp(int32_t N, int32_t C, int32_t K, const uint8_t *cls, const int32_t *g, const int32_t *I,
+                      int32_t ncap, int32_t B, uint8_t *exits, int64_t *best_gain, int64_t *best_cost,
+                      uint8_t *feasible)
+{
+    if (N < 0 || K < 2 || K > 16 || C < 1 || N > ncap) return -1;
+    int64_t S = 1;                               /* (N+1)^(K-1) table entries per prefix length */
+    for (int32_t k = 1; k < K; ++k) {
+        S *= (N + 1);
+        if (S > (1ll << 24)) return -1;
+    }
+    for (int32_t i = 0; i < N; ++i)
+        if ((int32_t)cls[i] >= C) return -1;
+    int32_t *order = (int32_t *)malloc(sizeof(int32_t) * (size_t)(N > 0 ? N : 1));
+    int32_t t = 0;
+    for (int32_t c = 0; c < C; ++c)
+        for (int32_t i = 0; i < N; ++i)
+            if ((int32_t)cls[i] == c) order[t++] = i;
+    const int64_t NEG = INT64_MIN / 4;
+    int64_t *F = (int64_t *)malloc(sizeof(int64_t) * (size_t)(N + 1) * (size_t)S);   /* F[j][index] */
+    for (int64_t e = 0; e < (int64_t)(N + 1) * S; ++e) F[e] = NEG;
+    F[0] = 0;
+    int32_t m[16];
+    for (int32_t j = 0; j < N; ++j) {
+        const int32_t c = cls[order[j]];
+        /* every count vector of total j + 1: iterate the table, keep entries whose total fits */
+        for (int64_t idx = 0; idx < S; ++idx) {
+            int64_t r = idx;
+            int32_t tot = 0;
+            for (int32_t k = 1; k < K; ++k) {
+                m[k] = (int32_t)(r % (N + 1));
+                r /= (N + 1);
+                tot += m[k];
+            }
+            if (tot > j + 1) continue;
+            m[0] = j + 1 - tot;
+            int64_t best = NEG;
+            for (int32_t k = 0; k < K; ++k) {
+                if (m[k] == 0) continue;
+                m[k] -= 1;
+                const int64_t prev = F[(int64_t)j * S + bdp_index(K, N, m)];
+                m[k] += 1;
+                if (prev == NEG) continue;
+                const int64_t v = prev + g[c * K + k];
+                if (v > best) best = v;
+            }
+            F[(int64_t)(j + 1) * S + idx] = best;
+        }
+    }
+    /* choose the count vector (R18 order over the final layer) */
+    int have = 0;
+    int64_t bg = 0, bc = 0;
+    int32_t bn[16];
+    for (int64_t idx = 0; idx < S; ++idx) {
+        int64_t r = idx;
+        int32_t tot = 0;
+        for (int32_t k = 1; k < K; ++k) {
+            m[k] = (int32_t)(r % (N + 1));
+            r /= (N + 1);
+            tot += m[k];
+        }
+        if (tot > N) continue;
+        m[0] = N - tot;
+        const int64_t gain = F[(int64_t)N * S + idx];
+        if (gain == NEG) continue;
+        int64_t cost = 0;
+        for (int32_t k = 0; k < K; ++k) cost += I[k * (ncap + 1) + m[k]];
+        if (cost > B) continue;
+        int better = !have || gain > bg || (gain == bg && cost < bc) ||
+                     (gain == bg && cost == bc && batched_lex_less(K, m, bn));
+        if (better) {
+            have = 1;
+            bg = gain;
+            bc = cost;
+            for (int32_t k = 0; k < K; ++k) bn[k] = m[k];
+        }
+    }
+    if (!have) {
+        int64_t g0 = 0;
+        for (int32_t i = 0; i < N; ++i) g0 += g[(int32_t)cls[i] * K];
+        for (int32_t i = 0; i < N; ++i) exits[i] = 0;
+        *best_gain = g0;
+        *best_cost = I[N];
+        *feasible = 0;
+    } else {
+        /* backwards: frame x_{j-1} takes the highest level that keeps F optimal */
+        for (int32_t k = 0; k < K; ++k) m[k] = bn[k];
+        for (int32_t j = N; j >= 1; --j) {
+            const int32_t c = cls[order[j - 1]];
+            const int64_t target = F[(int64_t)j * S + bdp_index(K, N, m)];
+            int32_t pick = -1;
+            for (int32_t k = K - 1; k >= 0 && pick < 0; --k) {
+                if (m[k] == 0) continue;
+                m[k] -= 1;
+                const int64_t prev = F[(int64_t)(j - 1) * S + bdp_index(K, N, m)];
+                m[k] += 1;
+                if (prev != NEG && prev + g[c * K + k] == target) pick = k;
+            }
+            exits[order[j - 1]] = (uint8_t)pick;
+            m[pick] -= 1;
+        }
+        *best_gain = bg;
+        *best_cost = bc;
+        *feasible = 1;
+    }
+    free(F);
+    free(order);
+    return 0;
+}
+
+/* The R20 assignment by its definition, for tiny windows: among all K^N plans with the optimal
+ * gain, cost and count vector (brute force), the one whose exits read in REVERSE canonical order
+ * (x_{N-1} first) are lexicographically largest. */
+int oracle_batched_brute_plan(int32_t N, int32_t C, int32_t K, const uint8_t *cls, const int32_t *g,
+                              const int32_t *I, int32_t ncap, int32_t B, uint8_t *exits, int64_t *best_gain,
+                              int64_t *best_cost, uint8_t *feasible)
+{
+    int32_t bn[16];
+    int e = oracle_batched_brute(N, C, K, cls, g, I, ncap, B, best_gain, best_cost, bn, feasible);
+    if (e) return e;
+    if (!*feasible) {
+        for (int32_t i = 0; i < N; ++i) exits[i] = 0;
+        return 0;
+    }
+    int32_t order[16], t = 0;
+    for (int32_t c = 0; c < C; ++c)
+        for (int32_t i = 0; i < N; ++i)
+            if ((int32_t)cls[i] == c) order[t++] = i;
+    int64_t total = 1;
+    for (int32_t i = 0; i < N; ++i) total *= K;
+    int32_t plan[16], cnt[16], best[16];
+    int have = 0;
+    for (int64_t code = 0; code < total; ++code) {
+        int64_t r = code;
+        for (int32_t k = 0; k < K; ++k) cnt[k] = 0;
+        int64_t gain = 0;
+        for (int32_t i = 0; i < N; ++i) {
+            plan[i] = (int32_t)(r % K);
+            r /= K;
+            cnt[plan[i]] += 1;
+            gain += g[(int32_t)cls[i] * K + plan[i]];
+        }
+        int same = gain == *best_gain;
+        for (int32_t k = 0; k < K && same; ++k) same = cnt[k] == bn[k];
+        if (!same) continue;
+        int larger = !have;
+        for (int32_t j = N - 1; j >= 0 && !larger; --j) {
+            const int32_t a = plan[order[j]], b = best[order[j]];
+            if (a != b) {
+                larger = a > b;
+                break;
+            }
+        }
+        if (larger) {
+            have = 1;
+            for (int32_t i = 0; i < N; ++i) best[i] = plan[i];
+        }
+    }
+    for (int32_t i = 0; i < N; ++i) exits[i] = (uint8_t)best[i];
+    return 0;
+}
+
 int oracle_batched_batch(int32_t num_windows, const int32_t *num_frames, const int32_t *budget,
                          const int32_t *profile, const int64_t *first_frame, const uint8_t *class_id,
                          const int32_t *gains, const int64_t *gain_off, const int32_t *C, const int32_t *K,
@@ -631,6 +818,10 @@ int oracle_batched_batch(int32_t num_windows, const int32_t *num_frames, const i
         int e = oracle_batched_enum(num_frames[w], C[p], K[p], class_id + first_frame[w], gains + gain_off[p],
                                     batch + batch_off[p], ncap, budget[w], exits + first_frame[w], &best_gain[w],
                                     &best_cost[w], &feasible[w]);
+        if (e == -2)                /* gains without R19: the general program (reading R20) */
+            e = oracle_batched_dp(num_frames[w], C[p], K[p], class_id + first_frame[w], gains + gain_off[p],
+                                  batch + batch_off[p], ncap, budget[w], exits + first_frame[w], &best_gain[w],
+                                  &best_cost[w], &feasible[w]);
         if (e) return e;
     }
     return 0;

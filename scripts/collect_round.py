@@ -3,7 +3,8 @@
 round prefix: bench lines, the launch list, ncu summaries (+ details CSV) and the per-workload DRAM
 traffic files bench.py reports as roofline.traffic.
 
-usage: scripts/collect_round.py r02"""
+usage: scripts/collect_round.py r02 [DEST_DIR]   (default profiles/; on a GPU box use a directory
+under gpurun_out/ -- only gpurun_out/ travels back)"""
 import json
 import os
 import shutil
@@ -18,7 +19,11 @@ TRAFFIC = {"full_schedule_c2": "c2", "full_schedule_c3": "c3", "full_grid_c4": "
 
 
 def main():
+    global DST
     tag = sys.argv[1]
+    if len(sys.argv) > 2:
+        DST = sys.argv[2]
+        os.makedirs(DST, exist_ok=True)
     for f in sorted(os.listdir(SRC)):
         p = os.path.join(SRC, f)
         if f.startswith("bench_") and f.endswith(".json"):
@@ -31,7 +36,7 @@ def main():
         elif f.endswith(".ncu-rep"):
             name = f[:-8]
             args = [sys.executable, os.path.join(ROOT, "scripts", "ncu_summary.py"), p, f"{tag}_ncu_{name}",
-                    TRAFFIC.get(name, name)]
+                    TRAFFIC.get(name, name), "", DST]
             r = subprocess.run(args, capture_output=True, text=True)
             if r.returncode != 0:
                 print("summary failed", f, r.stderr[-500:])

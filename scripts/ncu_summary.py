@@ -3,7 +3,7 @@
 the details page (CSV), and the DRAM traffic per launch that bench.py reports as
 roofline.traffic (profiles/traffic_<workload>.json).
 
-usage: scripts/ncu_summary.py REPORT.ncu-rep NAME WORKLOAD [KERNEL_LABEL]"""
+usage: scripts/ncu_summary.py REPORT.ncu-rep NAME WORKLOAD [KERNEL_LABEL] [DEST_DIR]"""
 import csv
 import io
 import json
@@ -51,7 +51,7 @@ def main():
     rep, name, workload = sys.argv[1], sys.argv[2], sys.argv[3]
     label = sys.argv[4] if len(sys.argv) > 4 else ""
     d = raw(rep)
-    prof = os.path.join(ROOT, "profiles")
+    prof = sys.argv[5] if len(sys.argv) > 5 else os.path.join(ROOT, "profiles")
     with open(os.path.join(prof, f"{name}_summary.json"), "w") as f:
         json.dump(d, f, indent=1)
     det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True,

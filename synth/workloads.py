@@ -364,10 +364,11 @@ def make_batched_config(k: int, num_windows: Optional[int] = None, window_offset
 
 
 def make_batched_random(seed: int, W: int, max_frames: int = 8, K: int = 3, C: int = 4, max_budget: int = 40,
-                        linear: bool = False) -> Workload:
+                        linear: bool = False, general: bool = False) -> Workload:
     """Parity set for NEXT-4: random supermodular gains (negative entries allowed), random
     non-decreasing batch tables (or linear ones, I_k(n) = n c_k, when `linear`), random budgets
-    including infeasible windows (I_0(n) > 0 in some profiles)."""
+    including infeasible windows (I_0(n) > 0 in some profiles). general: gains U{-4..12} with no
+    structure at all (most profiles then violate R19; small ranges give many ties)."""
     wid = np.arange(W, dtype=np.int64)
     nf = rand_int(seed, S_TN, wid, 0, max_frames).astype(np.int32)
     bud = rand_int(seed, S_TBUD, wid, 0, max_budget).astype(np.int32)
@@ -380,6 +381,8 @@ def make_batched_random(seed: int, W: int, max_frames: int = 8, K: int = 3, C: i
         H = np.cumsum(rand_int(seed, S_TGAIN * 89 + q, np.arange(K), 0, 3))
         r = rand_int(seed, S_TGAIN * 83 + q, np.arange(K), -3, 3)
         g = (A[:, None] * H[None, :] + r[None, :]).astype(np.int32).reshape(-1)
+        if general:
+            g = rand_int(seed, S_TGAIN * 79 + q, np.arange(C * K), -4, 12).astype(np.int32)
         ck = rand_int(seed, S_TCOST * 97 + q, np.arange(K), 0, 6)
         fixed = rand_int(seed, S_TBASE * 97 + q, np.arange(K), 0, 4)
         t = np.zeros((K, cap + 1), dtype=np.int64)

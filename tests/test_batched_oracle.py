@@ -108,10 +108,86 @@ def test_budget_monotone():
         prev = G
 
 
-def test_r19_violation_is_rejected():
+def test_r19_violation_goes_to_the_general_program():
+    """The count-vector enumeration refuses gains without R19; the batch entry then plans the window
+    with the general program (reading R20) instead of rejecting it."""
     wl = synth.make_batched_random(6, 4, max_frames=4, K=3, C=3)
-    g = wl.profiles_gain[int(wl.profile[0])].copy().reshape(3, 3)
+    p = int(wl.profile[0])
+    g = wl.profiles_gain[p].copy().reshape(3, 3)
     g[0, 2] += 50                                          # easiest class gains most: breaks R19
-    wl.profiles_gain[int(wl.profile[0])] = g.reshape(-1)
+    wl.profiles_gain[p] = g.reshape(-1)
+    cls, gg, C, K, I, cap, B, ff, n = _window(wl, 0)
     with pytest.raises(RuntimeError):
-        oracle.batched(wl)
+        oracle.batched_enum(cls, gg, C, K, I, cap, B)
+    ex, G, Cs, fe = oracle.batched(wl)
+    want = oracle.batched_brute_plan(cls, gg, C, K, I, cap, B)
+    assert (G[0], Cs[0], fe[0]) == want[1:]
+    np.testing.assert_array_equal(ex[ff:ff + n], want[0])
+
+
+# ---- NEXT-4 for any gain table (reading R20): the program over the canonical prefix and its counts
+def _r19(g, C, K):
+    g = np.asarray(g, dtype=np.int64).reshape(C, K)
+    return bool((np.diff(np.diff(g, axis=1), axis=0) >= 0).all())
+
+
+@pytest.mark.parametrize("seed", [21, 22, 23, 24])
+def test_general_program_equals_brute_force_plan(seed):
+    """G*, C*, the count vector AND the assignment against the plain R20 definition (all K^N plans)."""
+    wl = synth.make_batched_random(seed, 300, max_frames=7, K=3 + seed % 2, C=4, max_budget=40, general=True)
+    n_non_r19 = 0
+    for w in range(wl.num_windows):
+        cls, g, C, K, I, cap, B, ff, n = _window(wl, w)
+        n_non_r19 += not _r19(g, C, K)
+        got = oracle.batched_dp(cls, g, C, K, I, cap, B)
+        want = oracle.batched_brute_plan(cls, g, C, K, I, cap, B)
+        assert got[1:] == want[1:], w
+        np.testing.assert_array_equal(got[0], want[0], err_msg=f"window {w}")
+    assert n_non_r19 > wl.num_windows // 2                 # the set really exercises non-R19 gains
+
+
+@pytest.mark.parametrize("seed", [31, 32])
+def test_general_program_equals_canonical_under_r19(seed):
+    """Under R19 the R20 plan is R18's canonical plan: identical to the count-vector enumeration."""
+    wl = synth.make_batched_random(seed, 300, max_frames=16, K=4, C=5, max_budget=60)
+    for w in range(wl.num_windows):
+        cls, g, C, K, I, cap, B, ff, n = _window(wl, w)
+        assert _r19(g, C, K)
+        got = oracle.batched_dp(cls, g, C, K, I, cap, B)
+        want = oracle.batched_enum(cls, g, C, K, I, cap, B)
+        assert got[1:] == want[1:], w
+        np.testing.assert_array_equal(got[0], want[0], err_msg=f"window {w}")
+
+
+def test_general_program_gain_is_the_transportation_optimum():
+    """For the chosen count vector, G* equals the C x K transportation LP optimum (scipy HiGHS,
+    an independent solver; the LP is integral), and the plan realises it."""
+    from scipy.optimize import linprog
+    wl = synth.make_batched_random(41, 80, max_frames=14, K=4, C=4, max_budget=70, general=True)
+    checked = 0
+    for w in range(wl.num_windows):
+        cls, g, C, K, I, cap, B, ff, n = _window(wl, w)
+        ex, G, Cst, fe = oracle.batched_dp(cls, g, C, K, I, cap, B)
+        if not fe or n == 0:
+            continue
+        gain, cost, cnt = _gain_cost(cls, ex, g, K, I, cap)
+        assert (gain, cost) == (G, Cst)
+        h = np.bincount(np.asarray(cls, dtype=np.int64), minlength=C)
+        # variables y[c][k] >= 0: sum_k y = h_c, sum_c y = n_k; maximise sum g y
+        A_eq, b_eq = [], []
+        for c in range(C):
+            row = np.zeros(C * K)
+            row[c * K:(c + 1) * K] = 1
+            A_eq.append(row)
+            b_eq.append(h[c])
+        for k in range(K):
+            row = np.zeros(C * K)
+            row[k::K] = 1
+            A_eq.append(row)
+            b_eq.append(cnt[k])
+        res = linprog(-np.asarray(g[:C * K], dtype=np.float64), A_eq=np.array(A_eq), b_eq=np.array(b_eq),
+                      bounds=(0, None), method="highs")
+        assert res.status == 0
+        assert round(-res.fun) == G, w
+        checked += 1
+    assert checked > 40
