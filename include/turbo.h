@@ -311,23 +311,32 @@ turbo_status_t turbo_stats(const turbo_shape_t *shape /* host */, const turbo_wi
  * cost(plan) = sum_k I_k(n_k), n_k = frames planned at level k, I_k(n) = the latency of a batch of
  * n frames at level k (latency independent of content :103). Result per window:
  * larger gain, then smaller cost, then the count vector (n_{K-1}, ..., n_0) lexicographically
- * smaller, then the canonical assignment -- frames sorted by (class, arrival index) fill level 0,
- * then 1, ... (readings R18, R19). Preconditions: the profile's gains have increasing
- * differences in the class, g[c+1][k+1] - g[c+1][k] >= g[c][k+1] - g[c][k] (R19)
- * and |g| <= 2^24, sum over the window's frames of |g| per level <= 2^30, batch latencies in [0, 2^26];
- * a window violating them (or with budget < 0) is planned all-zero, feasible = 0,
- * gain = cost = 0, and status[1] = min such window; a class id >= C sets status[0] like the lookup.
- * batch_cost (device int32): per profile p a table at p * 16 * (batch_cap + 1), row k (k < K_p) =
- * I_k(0 .. batch_cap). Host checks (TURBO_ERR_UNSUPPORTED): max_frames <= batch_cap <= 255,
- * C(max_frames + max_exits - 1, max_exits - 1) <= 2^26 count vectors per window and
- * (max_frames + 1)^(max_exits - 1) < 2^62. Infeasible windows: all frames at level 0,
+ * smaller, then the assignment: frames in canonical order (class, then arrival index) x_0 ..
+ * x_{N-1}; backwards from x_{N-1}, each takes the highest level that keeps the plan optimal
+ * (reading R20). When the gains have increasing differences in the class,
+ * g[c+1][k+1] - g[c+1][k] >= g[c][k+1] - g[c][k] (R19), this is the canonical
+ * assignment (sorted frames fill level 0, then 1, ...; R18) and the count vectors are enumerated
+ * directly; windows WITHOUT R19 are solved by the program over the canonical prefix and its count
+ * vector (every transportation optimum at once), which needs `workspace` (device, >=
+ * turbo_batched_workspace() bytes; K <= 8, C <= 16). Without a workspace such windows are rejected.
+ * Preconditions: |g| <= 2^24, sum over the window's frames of |g| per level <= 2^30, batch
+ * latencies in [0, 2^26]; a window violating them (or with budget < 0) is planned all-zero,
+ * feasible = 0, gain = cost = 0, and status[1] = min such window; a class id >= C sets status[0]
+ * like the lookup. batch_cost (device int32): per profile p a table at p * 16 * (batch_cap + 1),
+ * row k (k < K_p) = I_k(0 .. batch_cap). Host checks (TURBO_ERR_UNSUPPORTED): max_frames <=
+ * batch_cap <= 255, C(max_frames + max_exits - 1, max_exits - 1) <= 2^26 count vectors per window
+ * and (max_frames + 1)^(max_exits - 1) < 2^62. Infeasible windows: all frames at level 0,
  * feasible = 0, best_gain = sum g[c_x][0], best_cost = I_0(N). Budgets are read from
  * windows[w].budget (set them on the device, or a1 via turbo_profile_lookup). Stream-ordered. */
 turbo_status_t turbo_batched_plan(const turbo_shape_t *shape /* host */, const turbo_window_t *windows,
                                   const turbo_profile_t *profiles /* device */, const int32_t *batch_cost,
-                                  int32_t batch_cap, const uint8_t *class_id, int32_t *best_gain,
-                                  int32_t *best_cost, uint8_t *feasible, uint8_t *exit_out, int64_t *status,
-                                  turbo_stream_t stream);
+                                  int32_t batch_cap, const uint8_t *class_id, void *workspace /* nullable */,
+                                  size_t workspace_bytes, int32_t *best_gain, int32_t *best_cost,
+                                  uint8_t *feasible, uint8_t *exit_out, int64_t *status, turbo_stream_t stream);
+
+/* Bytes of device workspace turbo_batched_plan needs to plan windows without R19 for this shape
+ * (0: the shape is too large for that program -- such windows are then rejected). Host only. */
+turbo_status_t turbo_batched_workspace(const turbo_shape_t *shape, size_t *bytes /* host, out */);
 
 /* Debug / test hook: force a DP kernel variant. variant & 3: 0 = automatic, 1 = fused solve
  * keeps choice planes in shared memory (when they fit the per-CTA maximum), 2 = in HBM;
@@ -335,7 +344,8 @@ turbo_status_t turbo_batched_plan(const turbo_shape_t *shape /* host */, const t
  * variant & 8: use the lockstep multi-window kernel (dp_pack.cu; V windows per CTA) for
  * single-class short-row batches instead of one CTA per window;
  * variant & 16: the runtime-K kernel also for row class 3 of mixed-K plan launches;
- * variant & 32: never the runtime-K body (the fifteen K-specific bodies everywhere).
+ * variant & 32: never the runtime-K body (the fifteen K-specific bodies everywhere);
+ * variant & 64: turbo_batched_plan plans every valid window with the general program (R20).
  * Returns INVALID_ARG for other values. Process-wide; not needed in production. */
 turbo_status_t turbo_debug_set_variant(int32_t variant);
 

@@ -146,7 +146,7 @@ turbo_status_t turbo_debug_trace(int64_t *trace, int64_t words)
 
 turbo_status_t turbo_debug_set_variant(int32_t variant)
 {
-    if (variant < 0 || variant > 63 || (variant & 3) == 3) return TURBO_ERR_INVALID_ARG;
+    if (variant < 0 || variant > 127 || (variant & 3) == 3) return TURBO_ERR_INVALID_ARG;
     g_variant = variant;
     return TURBO_OK;
 }
@@ -641,10 +641,32 @@ turbo_status_t turbo_heuristic_plan(const turbo_shape_t *shape, const turbo_wind
     return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
 }
 
+// bytes of the general (R20) program's scratch for this batch: one slice per SM; 0 when the batch
+// has too many frames per window for it
+static int64_t batched_ws_bytes(const turbo_shape_t *s, int num_sms)
+{
+    // the program's last layer holds C(N + K, K) choice bytes: bounded to 2^24 (16 MB per slice)
+    const int64_t N = s->max_frames, K = std::min<int32_t>(s->max_exits, 8);
+    double T = 1.0;
+    for (int64_t r = 0; r < K; ++r) T = T * (double)(N + K - r) / (double)(r + 1);
+    if (T > (double)(1 << 24)) return 0;
+    return batched_dp_bytes(s->max_frames, s->max_exits, num_sms);
+}
+
+turbo_status_t turbo_batched_workspace(const turbo_shape_t *shape, size_t *bytes)
+{
+    if (!shape || !bytes) return TURBO_ERR_INVALID_ARG;
+    DeviceInfo d;
+    if (device_info(&d) != cudaSuccess) return TURBO_ERR_CUDA;
+    *bytes = (size_t)batched_ws_bytes(shape, d.num_sms);
+    return TURBO_OK;
+}
+
 turbo_status_t turbo_batched_plan(const turbo_shape_t *shape, const turbo_window_t *windows,
                                   const turbo_profile_t *profiles, const int32_t *batch_cost, int32_t batch_cap,
-                                  const uint8_t *class_id, int32_t *best_gain, int32_t *best_cost, uint8_t *feasible,
-                                  uint8_t *exit_out, int64_t *status, turbo_stream_t stream)
+                                  const uint8_t *class_id, void *workspace, size_t workspace_bytes,
+                                  int32_t *best_gain, int32_t *best_cost, uint8_t *feasible, uint8_t *exit_out,
+                                  int64_t *status, turbo_stream_t stream)
 {
     if (!shape) return TURBO_ERR_INVALID_ARG;
     if (shape->num_windows == 0) return TURBO_OK;
@@ -662,8 +684,14 @@ turbo_status_t turbo_batched_plan(const turbo_shape_t *shape, const turbo_window
     if (vectors > (double)(1 << 26) || code >= 4.6e18) return TURBO_ERR_UNSUPPORTED;
     DeviceInfo d;
     if (device_info(&d) != cudaSuccess) return TURBO_ERR_CUDA;
+    // the general program (windows without R19) runs only with a workspace of the documented size
+    const int64_t need = batched_ws_bytes(shape, d.num_sms);
+    if (workspace != nullptr && need > 0 && (int64_t)workspace_bytes < need) return TURBO_ERR_WORKSPACE;
+    void *ws = (workspace != nullptr && need > 0) ? workspace : nullptr;
+    const int32_t general = (g_variant & 64) ? 2 : 1;
     cudaError_t e = launch_batched(windows, shape->num_windows, profiles, batch_cost, batch_cap, class_id, best_gain,
-                                   best_cost, feasible, exit_out, status, (int32_t)K, d.num_sms, (cudaStream_t)stream);
+                                   best_cost, feasible, exit_out, status, (int32_t)K, (int32_t)N, ws, general,
+                                   d.num_sms, (cudaStream_t)stream);
     return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
 }
 

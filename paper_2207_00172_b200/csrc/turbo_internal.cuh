@@ -157,7 +157,8 @@ __host__ __device__ inline bool dp_kernel_fixed_k(int kmin, int kmax)
 cudaError_t launch_batched(const turbo_window_t *windows, int32_t num_windows, const turbo_profile_t *profiles,
                            const int32_t *batch, int32_t cap, const uint8_t *class_id, int32_t *best_gain,
                            int32_t *best_cost, uint8_t *feasible, uint8_t *exit_out, int64_t *status, int32_t kmax,
-                           int num_sms, cudaStream_t stream);
+                           int32_t max_frames, void *workspace, int32_t general, int num_sms, cudaStream_t stream);
+int64_t batched_dp_bytes(int32_t max_frames, int32_t max_exits, int num_sms);
 // every kernel launch of the library is counted (turbo_launch_count)
 void note_launch();
 

@@ -65,7 +65,7 @@ assert WINDOW_DTYPE.itemsize == 48
 EXPORTS = ["turbo_mckp_workspace", "turbo_profile_lookup", "turbo_mckp_plan", "turbo_backtrack",
            "turbo_mckp_solve", "turbo_mckp_solve_workspace", "turbo_mckp_plane_bytes", "turbo_schedule",
            "turbo_schedule_theta", "turbo_heuristic_plan", "turbo_stats",
-           "turbo_bucketize", "turbo_batches", "turbo_batched_plan",
+           "turbo_bucketize", "turbo_batches", "turbo_batched_plan", "turbo_batched_workspace",
            "turbo_debug_set_variant", "turbo_debug_trace", "turbo_debug_smem_stream", "turbo_launch_count",
            "turbo_status_string", "turbo_abi_version"]
 
@@ -96,7 +96,8 @@ def load(path: Optional[str] = None):
     lib.turbo_heuristic_plan.argtypes = [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     lib.turbo_bucketize.argtypes = [vp, i64, i32, ctypes.c_float, vp, vp]
     lib.turbo_batches.argtypes = [vp, vp, vp, vp, vp, vp, i32, vp, vp, vp]
-    lib.turbo_batched_plan.argtypes = [vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp]
+    lib.turbo_batched_plan.argtypes = [vp, vp, vp, vp, i32, vp, vp, sz, vp, vp, vp, vp, vp, vp]
+    lib.turbo_batched_workspace.argtypes = [vp, vp]
     lib.turbo_debug_set_variant.argtypes = [i32]
     lib.turbo_debug_trace.argtypes = [vp, i64]
     lib.turbo_debug_smem_stream.argtypes = [i32, i32, i32, vp, vp, vp]
@@ -219,13 +220,22 @@ def heuristic_plan(shape, windows_dev, opt_gain, opt_cost, gain_out, cost_out, f
                                        _stream(stream)))
 
 
+def batched_workspace(shape) -> int:
+    """Device bytes turbo_batched_plan needs for windows without R19 (turbo.h turbo_batched_workspace)."""
+    out = ctypes.c_size_t(0)
+    _check("turbo_batched_workspace", load().turbo_batched_workspace(ctypes.addressof(shape), ctypes.addressof(out)))
+    return int(out.value)
+
+
 def batched_plan(shape, windows_dev, profiles_dev, batch_cost, batch_cap, class_id, best_gain, best_cost, feasible,
-                 exit_out, status, stream=None):
-    """NEXT-4: exact plans under the batched latency tables (turbo.h turbo_batched_plan)."""
+                 exit_out, status, stream=None, workspace=None):
+    """NEXT-4: exact plans under the batched latency tables (turbo.h turbo_batched_plan); with a
+    workspace (batched_workspace bytes) also for gains without R19."""
+    nbytes = 0 if workspace is None else workspace.numel() * workspace.element_size()
     _check("turbo_batched_plan",
            load().turbo_batched_plan(ctypes.addressof(shape), _ptr(windows_dev), _ptr(profiles_dev), _ptr(batch_cost),
-                                     int(batch_cap), _ptr(class_id), _ptr(best_gain), _ptr(best_cost), _ptr(feasible),
-                                     _ptr(exit_out), _ptr(status), _stream(stream)))
+                                     int(batch_cap), _ptr(class_id), _ptr(workspace), nbytes, _ptr(best_gain),
+                                     _ptr(best_cost), _ptr(feasible), _ptr(exit_out), _ptr(status), _stream(stream)))
 
 
 def batch_cost_table(profiles_batch, profiles_shape, cap: int, device="cuda"):
