@@ -46,6 +46,8 @@ WORKLOADS = {
 METRIC_B = "NEXT-4 exact batched-cost plans: count vectors evaluated/s (and windows/s)"
 UNIT_B = "count-vectors/s"
 ISSUE_PEAK = 148 * 4 * 1.965e9          # warp-instructions/s: 4 SMSPs x 1 issue/clk x sm_max_mhz
+ALU_PEAK = 148 * 128 * 1.965e9          # 32-bit integer lane-operations/s: 4 SMSPs x 32 lanes per clock
+ALG_OPS_PER_VECTOR = 11                 # NEXT-4 enumeration: per count vector (see the roofline note)
 
 
 def dist_env():
@@ -147,9 +149,14 @@ def run_batched(args):
     W, F = wl.num_windows, wl.total_frames
     vec = _vectors(wl)
 
+    nws = turbo.batched_workspace(b.shape)                 # the general program's scratch (R20)
+    ws_t = torch.empty(max(nws, 16), dtype=torch.uint8, device=dev) if nws else None
+    if args.variant:
+        turbo.debug_set_variant(args.variant)             # 64: the general program on every window
+
     def call(stream=None):
         turbo.batched_plan(b.shape, b.windows_dev, b.profiles_dev, bt, wl.batch_cap, b.class_id, b.best_gain,
-                           b.best_cost, b.feasible, b.exit_out, b.status, stream)
+                           b.best_cost, b.feasible, b.exit_out, b.status, stream, workspace=ws_t)
 
     for _ in range(max(args.warmup, 3)):
         call()
@@ -234,12 +241,16 @@ def run_batched(args):
                        "l2": "flushed between timed steps (256 MiB write outside the step events)",
                        "parallelism": f"weak dp{N} (windows sharded, no collective)"},
             "windows_per_s": W * N / t_step,
-            "roofline": {"bound": "alu", "achieved": (ops / t_step) if ops else None, "peak": ISSUE_PEAK,
-                         "unit": "warp-instructions/s", "frac": (ops / t_step / ISSUE_PEAK) if ops else None,
+            "roofline": {"bound": "alu", "achieved": vec * ALG_OPS_PER_VECTOR / t_step, "peak": ALU_PEAK,
+                         "unit": "int-ops/s", "frac": vec * ALG_OPS_PER_VECTOR / t_step / ALU_PEAK,
                          "traffic": None, "kernel": "turbo::batched_kernel",
-                         "note": "integer compare/select + smem reads; achieved = warp instructions per launch "
-                                 "(profiles/issue_<workload>.json, ncu smsp__inst_executed) / live launch time; "
-                                 "peak = 148 SMs x 4 issue/clk x sm_max_mhz"},
+                         "note": f"achieved = count vectors x {ALG_OPS_PER_VECTOR} algorithmic integer operations "
+                                 "per vector (2 batch-table reads + 2 prefix-gain reads, 2 adds for the cost, 2 subs "
+                                 "+ 1 add for the gain, 1 compare against the budget, 1 against the best) / live "
+                                 "launch time; peak = 148 SMs x 128 int lanes/clk x sm_max_mhz (DESIGN.md §6)",
+                         "issue": {"achieved": (ops / t_step) if ops else None, "peak": ISSUE_PEAK,
+                                   "unit": "warp-instructions/s", "frac": (ops / t_step / ISSUE_PEAK) if ops else None,
+                                   "source": "profiles/issue_<workload>.json (ncu smsp__inst_executed per launch)"}},
             "e2e": {"value": vec * N / t_e2e, "unit": UNIT_B, "h2d_bytes_per_step": F,
                     "d2h_bytes_per_step": int(b.out_arena.numel()), "ms_per_step": t_e2e * 1e3},
             "gpu_launches": launches * args.steps,
