@@ -271,7 +271,7 @@ turbo_status_t turbo_profile_lookup(const turbo_shape_t *shape, const turbo_prof
     DeviceInfo d;
     if (device_info(&d) != cudaSuccess) return TURBO_ERR_CUDA;
     cudaError_t e = launch_lookup(profiles, windows, shape->num_windows, class_id, capacity, base_cost, opt_gain,
-                                  opt_cost, status, d.num_sms, (cudaStream_t)stream);
+                                  opt_cost, status, shape->max_options, d.num_sms, (cudaStream_t)stream);
     return e == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
 }
 

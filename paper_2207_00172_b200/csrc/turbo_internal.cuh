@@ -171,7 +171,7 @@ struct DpLaunch {
 
 cudaError_t launch_lookup(const turbo_profile_t *profiles, turbo_window_t *windows, int32_t num_windows,
                           const uint8_t *class_id, const int32_t *capacity, int32_t base_cost, int32_t *opt_gain,
-                          int32_t *opt_cost, int64_t *status, int num_sms, cudaStream_t stream);
+                          int32_t *opt_cost, int64_t *status, int32_t max_options, int num_sms, cudaStream_t stream);
 cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P, int num_sms, int smem_per_sm,
                       int smem_per_cta_max, cudaStream_t stream, DpLaunch *info);
 int dp_warps_per_window(const turbo_shape_t *shape);
