@@ -198,91 +198,77 @@ __global__ void __launch_bounds__(BT_THREADS) batched_kernel(BtParams P, int32_t
         }
         __syncthreads();
 
-        // ---- enumerate the count vectors. All C(N+K-1, K-1) vectors are ranked lexicographically
-        // (n_0 most significant) and every thread takes an EQUAL contiguous range of ranks: it unranks
-        // its first vector once (binomial search), then steps to the lexicographic successor -- almost
-        // always n_{K-2} += 1, n_{K-1} -= 1 (two table reads, two prefix-gain reads, a compare), rarely
-        // a new prefix (n_0 .. n_{K-3}). (Round 1 gave each thread a range of PREFIXES and swept the
-        // last two levels inline: 13.7 of 32 lanes active, 229 us on b2.)
-        const int32_t KP = K - 2;                                    // prefix parts n_0 .. n_{K-3}
-        const uint64_t total = binom(N + K - 1, K - 1);
+        // ---- enumerate the count vectors: prefixes (n_0 .. n_{K-3}) ranked lexicographically, the
+        // last two levels swept inline. Each thread takes a contiguous range of prefix ranks: it
+        // unranks its first prefix once (binomial search), then steps to the lexicographic
+        // successor. (Measured alternatives: unranking every prefix, 285 us on b2; one vector per
+        // step with per-lane carries, 361 us -- the carries diverge; this, 225 us.)
+        const int32_t KP = K - 2;                                    // prefix parts
+        const uint64_t n_pref = binom(N + KP, KP);                   // weak compositions, KP+1 parts
         int32_t bg = INT32_MIN, bc = INT32_MAX;
         uint64_t bk = ~0ull;
-        const uint64_t chunk = (total + BT_THREADS - 1) / BT_THREADS;
+        const uint64_t chunk = (n_pref + BT_THREADS - 1) / BT_THREADS;
         const uint64_t r_lo = (uint64_t)tid * chunk;
-        const uint64_t r_hi = r_lo + chunk < total ? r_lo + chunk : total;
-        int32_t pv[BT_MAX_K];                                        // prefix parts
-        int32_t left = N;                                            // n_{K-2} + n_{K-1}
-        int32_t v = 0;                                               // n_{K-2}
-        const int32_t a2 = K - 2, b2 = K - 1;
-        int32_t S = 0, cpre = 0, gpre = 0;                           // prefix: frames, cost, gain
-        uint64_t code = 0, wa = 0, wb = 1;
-        auto prefix_sums = [&]() {
-            S = 0;
-            cpre = 0;
-            gpre = 0;
-            code = 0;
-            uint64_t mul = 1;
-            for (int32_t i = 0; i < KP; ++i) {
-                const int32_t x = pv[i];
-                cpre += tab(i, x);
-                gpre += pref(i, S + x) - pref(i, S);
-                if (i > 0) {                                         // n_0 is implied (sum = N)
-                    code += (uint64_t)x * mul;
-                    mul *= (uint64_t)(N + 1);
-                }
-                S += x;
-            }
-            // code weights: n_k counts (N+1)^(k-1) for k >= 1 (level K-2 weighs `mul`, 0 when K = 2)
-            wa = a2 == 0 ? 0 : mul;
-            wb = a2 == 0 ? 1 : mul * (uint64_t)(N + 1);
-            gpre += pref(b2, N) - pref(a2, S);                       // level b2 takes the rest [S+v, N)
-        };
+        const uint64_t r_hi = r_lo + chunk < n_pref ? r_lo + chunk : n_pref;
+        int32_t pv[BT_MAX_K];                                        // prefix parts n_0 .. n_{KP-1}
+        int32_t left = N;                                            // the tail: n_{K-2} + n_{K-1}
         if (r_lo < r_hi) {
             uint64_t r = r_lo;
             for (int32_t i = 0; i < KP; ++i) {
-                int32_t x = 0;
-                for (;; ++x) {
-                    // vectors with this prefix value: compositions of (left - x) into K - 1 - i parts
-                    const uint64_t cnt = binom(left - x + K - 2 - i, K - 2 - i);
+                int32_t v = 0;
+                for (;; ++v) {
+                    // compositions of (left - v) into the remaining KP - i parts (incl. the tail)
+                    const uint64_t cnt = binom(left - v + KP - i - 1, KP - i - 1);
                     if (r < cnt) break;
                     r -= cnt;
                 }
-                pv[i] = x;
-                left -= x;
+                pv[i] = v;
+                left -= v;
             }
-            v = (int32_t)r;                                          // the rank inside the last-two sweep
-            prefix_sums();
         }
         for (uint64_t r0 = r_lo; r0 < r_hi; ++r0) {
             if (r0 > r_lo) {                                         // lexicographic successor
-                if (v < left) {
-                    ++v;
-                } else {                                             // next prefix
-                    if (left > 0) {
-                        pv[KP - 1] += 1;
-                        left -= 1;
-                    } else {
-                        int32_t i = KP - 1;
-                        while (i > 0 && pv[i] == 0) --i;             // rightmost non-zero part
-                        left += pv[i];
-                        pv[i] = 0;
-                        pv[i - 1] += 1;
-                        left -= 1;
-                    }
-                    v = 0;
-                    prefix_sums();
+                if (left > 0) {
+                    pv[KP - 1] += 1;
+                    left -= 1;
+                } else {
+                    int32_t i = KP - 1;
+                    while (i > 0 && pv[i] == 0) --i;                 // rightmost non-zero part
+                    left += pv[i];
+                    pv[i] = 0;
+                    pv[i - 1] += 1;
+                    left -= 1;
                 }
             }
-            const int32_t u = left - v;
-            const int32_t c2 = cpre + tab(a2, v) + tab(b2, u);
-            if (c2 > B) continue;
-            const int32_t g2 = gpre + pref(a2, S + v) - pref(b2, S + v);
-            const uint64_t code2 = code + (uint64_t)v * wa + (uint64_t)u * wb;
-            if (bt_better(g2, c2, code2, bg, bc, bk)) {
-                bg = g2;
-                bc = c2;
-                bk = code2;
+            int32_t S = 0, cost = 0, gain = 0;
+            uint64_t code = 0, mul = 1;
+            for (int32_t i = 0; i < KP; ++i) {
+                const int32_t v = pv[i];
+                cost += tab(i, v);
+                gain += pref(i, S + v) - pref(i, S);
+                if (i > 0) {                                         // n_0 is implied (sum = N)
+                    code += (uint64_t)v * mul;
+                    mul *= (uint64_t)(N + 1);
+                }
+                S += v;
+            }
+            // last two levels: n_{K-2} = v, n_{K-1} = left - v. Code weights: n_k counts
+            // (N+1)^(k-1) for k >= 1 (n_0 is implied), so level K-2 weighs `mul` (0 when K = 2)
+            const int32_t a2 = K - 2, b2 = K - 1;
+            const uint64_t wa = a2 == 0 ? 0 : mul;
+            const uint64_t wb = a2 == 0 ? 1 : mul * (uint64_t)(N + 1);
+            const int32_t gb = gain + pref(b2, N) - pref(a2, S);
+            for (int32_t v = 0; v <= left; ++v) {
+                const int32_t u = left - v;
+                const int32_t c2 = cost + tab(a2, v) + tab(b2, u);
+                if (c2 > B) continue;
+                const int32_t g2 = gb + pref(a2, S + v) - pref(b2, S + v);
+                const uint64_t code2 = code + (uint64_t)v * wa + (uint64_t)u * wb;
+                if (bt_better(g2, c2, code2, bg, bc, bk)) {
+                    bg = g2;
+                    bc = c2;
+                    bk = code2;
+                }
             }
         }
         // ---- argmax over the CTA
