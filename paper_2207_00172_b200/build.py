@@ -10,7 +10,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
-LIB = os.path.join(PKG, "libturbo.so")
+CHECKED = bool(os.environ.get("TURBO_CHECKS"))        # bounds-checked build (device TCHECK reports)
+LIB = os.path.join(PKG, "checked", "libturbo.so") if CHECKED else os.path.join(PKG, "libturbo.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 NVCC_FLAGS = [
@@ -36,6 +37,8 @@ def _stale() -> bool:
 
 def _compile(src: str, obj: str):
     extra = ["-DTURBO_TRACE"] if os.environ.get("TURBO_TRACE") else []   # profiling build (trace marks)
+    if CHECKED:
+        extra.append("-DTURBO_CHECKS")
     cmd = [NVCC, *NVCC_FLAGS, *extra, "-I", INCLUDE, "-I", CSRC, "-c", "-o", obj, src]
     return subprocess.run(cmd, capture_output=True, text=True)
 
@@ -45,7 +48,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
-    objdir = os.path.join(PKG, "build")
+    objdir = os.path.join(PKG, "build_checked" if CHECKED else "build")
+    os.makedirs(os.path.dirname(LIB), exist_ok=True)
     os.makedirs(objdir, exist_ok=True)
     srcs = sources()
     objs = [os.path.join(objdir, os.path.basename(s)[:-3] + ".o") for s in srcs]
@@ -53,7 +57,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h")) + [__file__]
     t_hdr = max(os.path.getmtime(h) for h in headers)
     stamp = os.path.join(objdir, ".flags")
-    flags = " ".join(NVCC_FLAGS) + (" -DTURBO_TRACE" if os.environ.get("TURBO_TRACE") else "")
+    flags = " ".join(NVCC_FLAGS) + (" -DTURBO_TRACE" if os.environ.get("TURBO_TRACE") else "") + \
+        (" -DTURBO_CHECKS" if CHECKED else "")
     same_flags = os.path.exists(stamp) and open(stamp).read() == flags
     todo = [i for i, (s, o) in enumerate(zip(srcs, objs))
             if force or not same_flags or not os.path.exists(o)
@@ -77,7 +82,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if link.returncode != 0:
         sys.stderr.write(link.stdout + link.stderr)
         raise RuntimeError("nvcc link of libturbo.so failed")
-    with open(os.path.join(PKG, "ptxas.log"), "a" if len(todo) < len(srcs) else "w") as f:
+    with open(os.path.join(objdir if CHECKED else PKG, "ptxas.log"), "a" if len(todo) < len(srcs) else "w") as f:
         f.write("\n".join(log))
     if verbose:
         sys.stderr.write("\n".join(log))

@@ -438,6 +438,7 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
             int32_t *nxt = (f & 1) ? r0 : r1;
             for (int32_t t = gw; t < ntile; t += GW) {
                 const int32_t b_lo = t * RPT * 32;
+                TCHECK(b_lo + RPT * 32 <= X.l2stride && t < gtiles);
                 int32_t key[RPT];
 #pragma unroll
                 for (int r = 0; r < RPT; ++r) key[r] = NEG_R;
@@ -569,6 +570,11 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
                 const int32_t b_lo = t * RPT * 32;
                 const int32_t nr = min(RPT, nrows - t * RPT);
                 const bool pack = publish && b_lo + RPT * 32 > pub_lo;
+                // the segment buffer is [seg_lo - H, seg_lo + seg): reads reach down to b_lo - c_max
+                TCHECK(b_lo >= seg_lo && b_lo + RPT * 32 <= seg_lo + seg);
+                TCHECK(b_lo - hl >= seg_lo - H || b_lo - hl < 0);
+                TCHECK(!pack || (b_lo + RPT * 32 - pub_lo <= H && hl8 <= H));
+                TCHECK(t < gtiles);
                 int32_t *dst = nxt_base + b_lo + lane;
                 if (nr == RPT && !pack) {                              // interior tile: no checks
                     tile_keys_fast<K, RPT>(cur_base + lane, b_lo, gp, cc, key);
@@ -626,6 +632,7 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
                     bool stale = false;
                     const ulonglong2 *in2 = reinterpret_cast<const ulonglong2 *>(stage_in);
                     int2 *out2 = reinterpret_cast<int2 *>(cur + H - hl8);
+                    TCHECK(hl8 <= H);
                     for (int32_t x = gtid; x < hl8 / 2; x += gn) {
                         const ulonglong2 u = in2[x];
                         stale |= ((uint32_t)(u.x >> 32) != (uint32_t)(sb + f)) |

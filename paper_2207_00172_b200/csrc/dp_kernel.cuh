@@ -126,6 +126,11 @@ __device__ __forceinline__ void dp_tile(const DpParams &P, int32_t t, int32_t i,
     const int32_t nr = min(RPT, nrows - t * RPT);
     int32_t key[RPT];
     const bool fast = (nr == RPT) && (cmax <= b_lo + P.pad_words);
+    // rows are [-pad_words, row_words) around `cur` / `nxt`; planes hold ntiles tiles per frame
+    TCHECK(b_lo + RPT * 32 <= P.row_words);
+    TCHECK(!fast || b_lo - cmax >= -P.pad_words);
+    TCHECK(MODE != DP_SOLVE_SMEM || (int64_t)(i * ntiles + t) * 32 + 32 <= (int64_t)P.chs_words);
+    TCHECK(MODE == DP_SOLVE_SMEM || t < gtiles);
     if (fast) {
         const int32_t *__restrict__ src = cur + lane + b_lo;
         if (OWN && cc[0] == 0) {
@@ -359,6 +364,7 @@ __device__ __forceinline__ void backtrack_warp(int32_t N, int32_t b, const uint3
     auto choice = [&](int32_t i, int32_t cell) -> int32_t {
         const int32_t t = cell / (32 * RPT);
         const int32_t j = (cell >> 5) & (RPT - 1);
+        TCHECK(cell >= 0 && i >= 0 && i < N && t < (MODE == DP_SOLVE_SMEM ? ntiles : gtiles));
         const uint32_t word = (MODE == DP_SOLVE_SMEM) ? sch[(i * ntiles + t) * 32 + (cell & 31)]
                                                       : gch[((int64_t)i * gtiles + t) * 32 + (cell & 31)];
         return (int32_t)((word >> choice_shift(j, CB)) & CMASK);
@@ -431,6 +437,7 @@ __device__ __forceinline__ void backtrack_warp_rt(const int K, int32_t N, int32_
         a2 = (lane - 1 - K) % K;
     }
     auto choice = [&](int32_t i, int32_t cell) -> int32_t {
+        TCHECK(cell >= 0 && i >= 0 && i < N && (cell >> lg_tile) < gtiles);
         const uint32_t word = gch[((int64_t)i * gtiles + (cell >> lg_tile)) * 32 + (cell & 31)];
         return (int32_t)((word >> choice_shift((cell >> 5) & rmask, CB)) & cmask);
     };
@@ -734,6 +741,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
 
     for (int32_t i = N - 1; i >= 0; --i) {
         int32_t gp[K], cc[K];
+        TCHECK(!OSM || (i + 1) * K <= P.max_options);
         if (OSM) {
 #pragma unroll
             for (int k = 0; k < K; ++k) {
@@ -981,6 +989,7 @@ __device__ __forceinline__ void dp_window_gen(const DpParams &P, int64_t w, cons
         }
         for (int32_t t = t0; t >= 0 && t < ntiles; t += dt) {
             const int32_t b_lo = t * RPT * 32;
+            TCHECK(b_lo + RPT * 32 <= P.row_words && t < gtiles);
             int32_t key[RPT];
 #pragma unroll
             for (int r = 0; r < RPT; ++r) key[r] = NEG_R;
@@ -995,6 +1004,7 @@ __device__ __forceinline__ void dp_window_gen(const DpParams &P, int64_t w, cons
                     c = __shfl_sync(0xffffffffu, a_c, q * K + k);
                 }
                 if (c <= b_lo + pad) {
+                    TCHECK(b_lo - c >= -pad);
                     const int32_t *__restrict__ s = cur + (b_lo + lane - c);
 #pragma unroll
                     for (int r = 0; r < RPT; ++r) key[r] = max_plus(s[r * 32], g, key[r]);

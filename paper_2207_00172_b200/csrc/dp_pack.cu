@@ -207,6 +207,8 @@ __global__ void __launch_bounds__(1024, 1) dp_pack_kernel(DpParams P)
                 for (int k = 1; k < K; ++k) cmax = max(cmax, cc[k]);
                 const int32_t *cur = (f & 1) ? rb : ra;
                 int32_t *nxt = (f & 1) ? ra : rb;
+                TCHECK(b_lo + RPT * 32 <= row && (int64_t)(N - 1 - f) * nt * 32 + 32 <= P.chs_words);
+                TCHECK(cmax > b_lo + pad || b_lo - cmax >= -pad);
                 int32_t key[RPT];
                 if (cmax <= b_lo + pad) {                    // every shift inside the -inf pad
                     const int32_t *src = cur + b_lo + lane;

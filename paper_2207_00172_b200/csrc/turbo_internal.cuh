@@ -7,6 +7,24 @@
 
 #include "turbo.h"
 
+// Checked build (TURBO_CHECKS=1 python -m paper_2207_00172_b200.build -> checked/libturbo.so): every
+// TCHECK prints its location on a violated index bound instead of compiling to nothing.
+// compute-sanitizer is closed on the GPU pool; tests/test_gpu_checked.py runs every kernel path of
+// the checked library and fails on any report.
+#ifdef TURBO_CHECKS
+#include <cstdio>
+#define TCHECK(cond)                                                                        \
+    do {                                                                                    \
+        if (!(cond))                                                                        \
+            printf("TCHECK %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x, \
+                   (int)threadIdx.x, #cond);                                                \
+    } while (0)
+#else
+#define TCHECK(cond) \
+    do {             \
+    } while (0)
+#endif
+
 namespace turbo {
 
 // ---------------------------------------------------------------------------------------------

@@ -14,7 +14,8 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libturbo.so")
+# TURBO_LIB selects another build of the same library (the bounds-checked checked/libturbo.so)
+LIB_PATH = os.environ.get("TURBO_LIB") or os.path.join(_PKG, "libturbo.so")
 
 TURBO_OK = 0
 STATUS_NAMES = {0: "ok", 1: "invalid argument", 2: "value out of range", 3: "workspace too small",
