@@ -363,6 +363,9 @@ turbo_status_t turbo_debug_trace(int64_t *trace, int64_t words);
  * (CUDA events) and divides. sink: device, >= 4 KB, never meaningfully written. */
 turbo_status_t turbo_debug_smem_stream(int32_t iters, int32_t ctas_per_sm, int32_t bytes_per_lane, void *sink,
                                        double *bytes_out, turbo_stream_t stream);
+/* Test hook: launches one kernel whose bounds check is violated on purpose. In the checked build
+ * (TURBO_CHECKS) it prints one "TCHECK" report; in the production build it does nothing. */
+turbo_status_t turbo_debug_tcheck_selftest(turbo_stream_t stream);
 /* Kernels this library has launched so far in the process (all threads and devices; graph
  * capture counts the captured launches once). Lets a caller count the kernels of a call. */
 int64_t turbo_launch_count(void);

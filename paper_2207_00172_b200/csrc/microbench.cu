@@ -73,3 +73,17 @@ extern "C" turbo_status_t turbo_debug_smem_stream(int32_t iters, int32_t ctas_pe
         smem_stream_kernel<16><<<blocks, SMEM_BENCH_THREADS, 0, st>>>(iters, (uint32_t *)sink);
     return cudaGetLastError() == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
 }
+
+// Self-test of the checked build's reporting path (tests/test_gpu_checked.py): one deliberately
+// violated TCHECK -- a report in the checked library, nothing in the production one.
+__global__ void tcheck_selftest_kernel(int32_t v)
+{
+    TCHECK(v != 7);
+}
+
+extern "C" turbo_status_t turbo_debug_tcheck_selftest(turbo_stream_t stream)
+{
+    note_launch();
+    tcheck_selftest_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(7);
+    return cudaGetLastError() == cudaSuccess ? TURBO_OK : TURBO_ERR_CUDA;
+}

@@ -67,7 +67,8 @@ EXPORTS = ["turbo_mckp_workspace", "turbo_profile_lookup", "turbo_mckp_plan", "t
            "turbo_mckp_solve", "turbo_mckp_solve_workspace", "turbo_mckp_plane_bytes", "turbo_schedule",
            "turbo_schedule_theta", "turbo_heuristic_plan", "turbo_stats",
            "turbo_bucketize", "turbo_batches", "turbo_batched_plan", "turbo_batched_workspace",
-           "turbo_debug_set_variant", "turbo_debug_trace", "turbo_debug_smem_stream", "turbo_launch_count",
+           "turbo_debug_set_variant", "turbo_debug_trace", "turbo_debug_smem_stream", "turbo_debug_tcheck_selftest",
+           "turbo_launch_count",
            "turbo_status_string", "turbo_abi_version"]
 
 _lib = None
@@ -102,6 +103,7 @@ def load(path: Optional[str] = None):
     lib.turbo_debug_set_variant.argtypes = [i32]
     lib.turbo_debug_trace.argtypes = [vp, i64]
     lib.turbo_debug_smem_stream.argtypes = [i32, i32, i32, vp, vp, vp]
+    lib.turbo_debug_tcheck_selftest.argtypes = [vp]
     lib.turbo_launch_count.argtypes = []
     lib.turbo_launch_count.restype = i64
     lib.turbo_status_string.restype = ctypes.c_char_p

@@ -37,6 +37,22 @@ def _run(lib, args):
     return out
 
 
+SELFTEST = ("import torch; from paper_2207_00172_b200 import turbo; turbo.load(); "
+            "turbo._check('selftest', turbo.load().turbo_debug_tcheck_selftest(None)); torch.cuda.synchronize(); "
+            "print('selftest done')")
+
+
+def test_reporting_path_is_live(checked_lib):
+    """A deliberately violated check reports in the checked library (and not in production)."""
+    env = dict(os.environ, TURBO_LIB=checked_lib)
+    r = subprocess.run([sys.executable, "-c", SELFTEST], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "selftest done" in r.stdout, r.stdout + r.stderr
+    assert any(ln.startswith("TCHECK") and "v != 7" in ln for ln in r.stdout.splitlines()), r.stdout
+    r = subprocess.run([sys.executable, "-c", SELFTEST], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "TCHECK" not in r.stdout
+
+
 def test_every_kernel_path_checked(checked_lib):
     out = _run(checked_lib, [os.path.join("scripts", "sanitize_cases.py")])
     assert "sanitize cases ok" in out
