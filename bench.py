@@ -54,7 +54,18 @@ def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: run every rank on one device (the multi-rank code path on a 1-GPU box, with the
+    # gloo backend -- host-staged collectives, no kernel waits on another rank)
+    if os.environ.get("TURBO_BENCH_DEVICE") is not None:
+        local = int(os.environ["TURBO_BENCH_DEVICE"])
     return ws, rank, local
+
+
+def init_dist(torch, dist, local, backend):
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
 
 
 def make_workload(name: str, rank: int, world: int = 1, scaling: str = "weak"):
@@ -133,7 +144,7 @@ def run_batched(args):
         import torch.distributed as dist_mod
         dist = dist_mod
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(torch, dist, local, args.dist_backend)
     else:
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -468,7 +479,7 @@ def run_turbo(args):
         import torch.distributed as dist_mod
         dist = dist_mod
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        init_dist(torch, dist, local, args.dist_backend)
         if rank == 0:
             print(f"[bench] NCCL communicator: {dist.get_world_size()} ranks (backend {dist.get_backend()})",
                   file=sys.stderr, flush=True)
@@ -493,10 +504,11 @@ def run_turbo(args):
     cells = wl.total_cells
     W = wl.num_windows
 
-    def dominant():
+    def dominant(stats_buf=None):
+        sb = b.stats if stats_buf is None else stats_buf
         if path == "schedule":       # a1..a6 in one launch
             turbo.schedule(b.shape, b.profiles_dev, b.windows_dev, b.class_id, b.capacity, b.base_cost, b.solve_ws,
-                           b.best_gain, b.best_cost, b.feasible, b.exit_out, b.stats, b.status)
+                           b.best_gain, b.best_cost, b.feasible, b.exit_out, sb, b.status)
         elif path == "solve":
             turbo.mckp_solve(b.shape, b.windows_dev, b.opt_gain, b.opt_cost, b.solve_ws, b.best_gain,
                              b.best_cost, b.feasible, b.exit_out, b.status)
@@ -504,12 +516,19 @@ def run_turbo(args):
             turbo.mckp_plan(b.shape, b.windows_dev, b.opt_gain, b.opt_cost, b.workspace, b.best_gain,
                             b.best_cost, b.feasible, b.status)
 
-    def step(reset: bool = True):
+    def step(reset: bool = True, stats_buf=None):
+        """One pass of the path. stats_buf: accumulate a6 into this buffer instead of the arena's
+        (the second buffer of the overlapped allreduce, N > 1)."""
         stream = torch.cuda.current_stream(dev)
+        sb = b.stats if stats_buf is None else stats_buf
         if reset:                    # stats = 0, status = -1: one device-to-device copy
-            turbo.reset_outputs(b)
+            if stats_buf is None:
+                turbo.reset_outputs(b)
+            else:
+                stats_buf.zero_()
+                b.status.fill_(-1)
         if path == "schedule":
-            dominant()
+            dominant(stats_buf)
             return
         turbo.profile_lookup(b.shape, b.profiles_dev, b.windows_dev, b.class_id, b.capacity, b.base_cost,
                              b.opt_gain, b.opt_cost, b.status, stream)
@@ -522,7 +541,7 @@ def run_turbo(args):
         if not fused:
             turbo.backtrack(b.shape, b.windows_dev, b.opt_cost, b.workspace, b.best_cost, b.feasible, b.exit_out,
                             stream)
-        turbo.stats(b.shape, b.windows_dev, b.class_id, b.exit_out, b.best_gain, b.best_cost, b.feasible, b.stats,
+        turbo.stats(b.shape, b.windows_dev, b.class_id, b.exit_out, b.best_gain, b.best_cost, b.feasible, sb,
                     stream)
     # L2 flush buffer (> 126 MB L2) written between timed steps (outside the timed events)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
@@ -547,6 +566,21 @@ def run_turbo(args):
     g_step = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g_step):
         step()
+    # N > 1: the a6 allreduce of step k runs on a communication stream while step k+1 computes, so
+    # the statistics are double-buffered (step k+2 reuses step k's buffer only after its allreduce
+    # completed -- that wait is inside step k+2's timed window); the last step's allreduce is
+    # waited for inside the last window
+    stats2 = torch.zeros_like(b.stats)
+    g_step2 = None
+    comm = None
+    if dist is not None:
+        step(stats_buf=stats2)
+        dist.all_reduce(stats2)
+        torch.cuda.synchronize(dev)
+        g_step2 = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g_step2):
+            step(stats_buf=stats2)
+        comm = torch.cuda.Stream(device=dev)
     g_dp = torch.cuda.CUDAGraph()                        # the dominant kernel alone
     with torch.cuda.graph(g_dp):
         dominant()
@@ -573,12 +607,27 @@ def run_turbo(args):
         dist.barrier()
     torch.cuda.synchronize(dev)
     clk.start()
+    ev_ar = [torch.cuda.Event(), torch.cuda.Event()]
+    ar_pending = [False, False]
     for k in range(args.steps):
         flush.fill_(k & 0xff)
         evs[k][0].record(stream)
-        g_step.replay()
-        if dist is not None:
-            dist.all_reduce(b.stats)
+        if dist is None:
+            g_step.replay()
+        else:
+            j = k & 1
+            if ar_pending[j]:
+                stream.wait_event(ev_ar[j])              # this buffer's previous allreduce is done
+            (g_step if j == 0 else g_step2).replay()
+            done = torch.cuda.Event()
+            done.record(stream)
+            comm.wait_event(done)
+            with torch.cuda.stream(comm):
+                dist.all_reduce(b.stats if j == 0 else stats2)
+            ev_ar[j].record(comm)
+            ar_pending[j] = True
+            if k == args.steps - 1:
+                stream.wait_event(ev_ar[j])              # the last allreduce inside the last window
         evs[k][1].record(stream)
     torch.cuda.synchronize(dev)
     if dist is not None:
@@ -759,6 +808,8 @@ def main():
                     help="weak: per-GPU windows fixed (per_gpu of the workload); strong: the config's whole "
                          "window set split over the ranks by work (shard.py)")
     ap.add_argument("--variant", type=int, default=0, help="kernel-variant debug switch (A/B runs; 0 = automatic)")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="N > 1 collective backend (gloo only to exercise the multi-rank path on one GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
