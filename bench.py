@@ -481,7 +481,7 @@ def run_turbo(args):
         torch.cuda.set_device(local)
         init_dist(torch, dist, local, args.dist_backend)
         if rank == 0:
-            print(f"[bench] NCCL communicator: {dist.get_world_size()} ranks (backend {dist.get_backend()})",
+            print(f"[bench] communicator: {dist.get_world_size()} ranks (backend {dist.get_backend()})",
                   file=sys.stderr, flush=True)
     else:
         torch.cuda.set_device(local)
