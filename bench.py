@@ -646,6 +646,8 @@ def run_turbo(args):
     clocks = clk.stop()
     t_step = sum(a.elapsed_time(bb) for a, bb in evs) / args.steps / 1e3          # s per step (this rank)
     t_dp = sum(a.elapsed_time(bb) for a, bb in evd) / args.steps / 1e3
+    per_step = sorted(a.elapsed_time(bb) for a, bb in evs)                          # ms, this rank
+    per_dp = sorted(a.elapsed_time(bb) for a, bb in evd)
     t_lk = sum(a.elapsed_time(bb) for a, bb in evl) / args.steps / 1e3
     turbo.reset_outputs(b)                               # (the lookup graph left status untouched)
 
@@ -745,6 +747,9 @@ def run_turbo(args):
                    "windows_total": W_total},
         "windows_per_s": W_total / t_step,
         "dp_ms": t_dp * 1e3,
+        "step_ms_stats": {"median": statistics.median(per_step), "min": per_step[0], "max": per_step[-1],
+                          "dp_median": statistics.median(per_dp), "dp_min": per_dp[0],
+                          "note": "rank 0's per-step CUDA-event times; value/ms_per_step use the mean (max over ranks)"},
         "dp_cell_updates_per_s": total_cells / t_dp,
         "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
                      "frac": achieved / smem_peak, "traffic": traffic,
@@ -776,6 +781,19 @@ def run_turbo(args):
     if rank == 0 and not args.no_cpu_baseline:
         nthr = os.cpu_count() or 1
         sub = sample_for_oracle(wl, 2.5e8 * nthr * args.cpu_seconds / 10.0)
+        # the timed run's own outputs (last e2e step) against the oracle on the same sample windows
+        import oracle
+        want = oracle.run(sub, threads=nthr)
+        got = turbo.results(b)
+        n_s, f_s = sub.num_windows, sub.total_frames
+        bad_w = int(((got["best_gain"][:n_s].astype(np.int64) != want["best_gain"]) |
+                     (got["best_cost"][:n_s].astype(np.int64) != want["best_cost"]) |
+                     (got["feasible"][:n_s] != want["feasible"])).sum())
+        bad_x = int((got["exits"][:f_s] != want["exits"]).sum())
+        line["parity"] = {"windows_checked": n_s, "window_mismatches": bad_w, "frames_checked": f_s,
+                          "exit_mismatches": bad_x,
+                          "note": "outputs of the timed run (last e2e step) vs the CPU oracle on the cpu_baseline "
+                                  "sample windows; the full parity suite is pytest -m gpu"}
         rate, reps, el = oracle_rate(sub, args.cpu_seconds, nthr)
         sub1 = sample_for_oracle(wl, 2.5e8 * args.cpu_seconds / 20.0)
         rate1, reps1, el1 = oracle_rate(sub1, args.cpu_seconds / 2.0, 1)
