@@ -27,9 +27,17 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+def _flags() -> str:
+    return " ".join(NVCC_FLAGS) + (" -DTURBO_TRACE" if os.environ.get("TURBO_TRACE") else "") + \
+        (" -DTURBO_CHECKS" if CHECKED else "")
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
+    stamp = os.path.join(PKG, "build_checked" if CHECKED else "build", ".flags")
+    if not os.path.exists(stamp) or open(stamp).read() != _flags():
+        return True                       # built with other flags (e.g. the trace marks)
     t = os.path.getmtime(LIB)
     deps = sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h"))
     return any(os.path.getmtime(d) > t for d in deps)
@@ -57,8 +65,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     headers = glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(INCLUDE, "*.h")) + [__file__]
     t_hdr = max(os.path.getmtime(h) for h in headers)
     stamp = os.path.join(objdir, ".flags")
-    flags = " ".join(NVCC_FLAGS) + (" -DTURBO_TRACE" if os.environ.get("TURBO_TRACE") else "") + \
-        (" -DTURBO_CHECKS" if CHECKED else "")
+    flags = _flags()
     same_flags = os.path.exists(stamp) and open(stamp).read() == flags
     todo = [i for i, (s, o) in enumerate(zip(srcs, objs))
             if force or not same_flags or not os.path.exists(o)
