@@ -71,6 +71,11 @@ EDGE_CASES = {
     "c5": lambda: synth.make_config(5, num_windows=512),
     "tie": lambda: synth.make_tie_heavy(seed=303, W=2000, max_frames=40, max_exits=16, max_budget=900),
     "c3": lambda: synth.make_config(3, num_windows=256),
+    # long windows (grid kernel: halo path and L2-row path) next to short ones
+    "long": lambda: synth.concat_workloads([synth.make_config(2, num_windows=8),
+                                            synth.make_long_window(51, N=33, K=6, B=40000),
+                                            synth.make_long_window(52, N=21, K=4, B=30000, c_max=6000,
+                                                                   random_rows=True)]),
 }
 EDGE_PATHS = [("all", 0), (True, 0), (False, 0), (True, 1), (True, 2), ("all", 2)]
 EDGE_IDS = ["schedule", "solve", "plan+backtrack", "solve-smem", "solve-hbm", "schedule-hbm"]
