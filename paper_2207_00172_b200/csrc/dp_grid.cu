@@ -533,7 +533,11 @@ __device__ __forceinline__ void grid_window(const DpParams &P, cg::grid_group &g
 
     const int32_t sb = step_base;                     // ring tag base (register copy)
     const bool exch = !(P.debug & 1);                 // timing switch: no halo exchange
+#ifdef TURBO_TRACE
     const bool trace = (P.debug & 2) != 0;            // cycle counters in X.trace (grid_trace.py)
+#else
+    constexpr bool trace = false;                     // (compiled out of production builds)
+#endif
     int64_t *const status = P.status;
     for (int32_t f = 0; f < N; ++f) {
         const int32_t i = N - 1 - f;
