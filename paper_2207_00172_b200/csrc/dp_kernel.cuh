@@ -32,6 +32,29 @@ __device__ __forceinline__ int64_t warp_sum_i64(int64_t v)
     return v;
 }
 
+// a4's C* = min{b <= B : S_0[b] = G*} by ONE warp: S_0 is non-decreasing in b over the feasible
+// cells and every infeasible cell (a prefix of the row) lies below any feasible value (R14), so
+// "S_0[b] >= S_0[B]" is false ... false, true ... true on [0, B] and a 32-ary search finds its first
+// true cell in ceil(log_31(B + 1)) + 1 rounds of one load and one vote (B = 1000: 3 rounds) --
+// instead of counting the B + 1 cells below G* with every thread and a CTA-wide reduction.
+__device__ __forceinline__ int32_t warp_first_at_least(const int32_t *__restrict__ S, int32_t B, int32_t RB,
+                                                       int lane)
+{
+    int32_t lo = 0, hi = B;                               // invariant: answer in [lo, hi], S[hi] >= RB
+    while (hi - lo >= 32) {
+        const int32_t step = (hi - lo + 30) / 31;         // lane 31 probes >= hi
+        const int32_t p = min(lo + lane * step, hi);
+        const unsigned m = __ballot_sync(0xffffffffu, S[p] >= RB);
+        const int f = __ffs(m) - 1;                       // m != 0: lane 31 probes hi
+        const int32_t nhi = min(lo + f * step, hi);
+        lo = f == 0 ? lo : lo + (f - 1) * step + 1;
+        hi = nhi;
+    }
+    const int32_t p = lo + lane;
+    const unsigned m = __ballot_sync(0xffffffffu, p > hi || S[min(p, hi)] >= RB);
+    return lo + __ffs(m) - 1;
+}
+
 // One tile of one frame: keys of RPT rows (cells b_lo + r*32 + lane) from row `src`.
 // `src` is preceded by `pad` words of -inf, so an option whose shift stays inside the pad
 // (c <= b_lo + pad) needs no bounds check; only larger shifts in the lowest tiles take the
@@ -780,17 +803,10 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     // after the swap `cur` holds S_0 (in place: cur == nxt == rowA)
     trace_mark(P, w, 2);
 
-    // ---- a4: optimum extraction
+    // ---- a4: optimum extraction (C* by warp 0, the warp that walks; nobody else needs it)
     const int32_t RB = cur[B];
     const bool feas = RB > VALID_MIN_R;
-    int32_t cnt = 0;
-    for (int32_t b = tid; b <= B; b += nthr) cnt += cur[b] < RB ? 1 : 0;
-    cnt = __reduce_add_sync(0xffffffffu, cnt);
-    if (nwarps > 1) {
-        if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(&red[3]), (unsigned long long)cnt);
-        __syncthreads();
-        cnt = (int32_t)red[3];
-    }
+    const int32_t cnt = (warp == 0 && feas) ? warp_first_at_least(cur, B, RB, lane) : 0;
     const int32_t G = feas ? (RB >> 4) : (int32_t)red[1];
     const int32_t Cst = feas ? cnt : (int32_t)red[2];
     if (tid == 0) {
@@ -1028,17 +1044,10 @@ __device__ __forceinline__ void dp_window_gen(const DpParams &P, int64_t w, cons
         cur = nxt;
         nxt = tmp;
     }
-    // ---- a4: G* = S_0[B], C* = #{b <= B : S_0[b] < G*}
+    // ---- a4: G* = S_0[B], C* = min{b : S_0[b] = G*} (32-ary search by warp 0)
     const int32_t RB = cur[B];
     const bool feas = RB > VALID_MIN_R;
-    int32_t cnt = 0;
-    for (int32_t b = tid; b <= B; b += nthr) cnt += cur[b] < RB ? 1 : 0;
-    cnt = __reduce_add_sync(0xffffffffu, cnt);
-    if (nwarps > 1) {
-        if (lane == 0) atomicAdd(reinterpret_cast<unsigned long long *>(&red[3]), (unsigned long long)cnt);
-        __syncthreads();
-        cnt = (int32_t)red[3];
-    }
+    const int32_t cnt = (warp == 0 && feas) ? warp_first_at_least(cur, B, RB, lane) : 0;
     if (tid == 0) {
         P.best_gain[w] = feas ? (RB >> 4) : (int32_t)red[1];
         P.best_cost[w] = feas ? cnt : (int32_t)red[2];

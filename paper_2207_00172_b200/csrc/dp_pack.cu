@@ -307,9 +307,7 @@ __global__ void __launch_bounds__(1024, 1) dp_pack_kernel(DpParams P)
             const int32_t *S0 = (N & 1) ? rowB(v) : rowA(v);   // frame 0 was written at f = N - 1
             const int32_t RB = S0[B];
             const bool feas = RB > VALID_MIN_R;
-            int32_t cnt = 0;
-            for (int32_t b = lane; b <= B; b += 32) cnt += S0[b] < RB ? 1 : 0;
-            cnt = __reduce_add_sync(0xffffffffu, cnt);
+            const int32_t cnt = feas ? warp_first_at_least(S0, B, RB, lane) : 0;
             const int32_t G = feas ? (RB >> 4) : (int32_t)s.g0;
             const int32_t Cst = feas ? cnt : (int32_t)s.c0;
             if (lane == 0) {
