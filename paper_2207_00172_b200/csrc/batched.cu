@@ -55,10 +55,12 @@ __device__ __forceinline__ bool bt_better(int32_t g, int32_t c, uint64_t code, i
 //   pref  int32 [kmax][cap + 1]   P_k(j), gain of the first j canonical frames at level k
 //   tab   int32 [kmax][cap + 1]   I_k(n)
 //   binom u32   [cap + kmax + 1][kmax]  C(n, r), saturated at 2^31 (counts used stay < 2^26)
+//   dif   int32 [cap + 1]         P_{K-2}(j) - P_{K-1}(j) (the inline sweep's gain term)
 //   pos_cls u8  [cap]             class at canonical position j
 __host__ __device__ inline size_t bt_smem_bytes(int32_t kmax, int32_t cap)
 {
-    return (size_t)2 * kmax * (cap + 1) * 4 + (size_t)(cap + kmax + 1) * kmax * 4 + (size_t)((cap + 15) & ~15);
+    return (size_t)2 * kmax * (cap + 1) * 4 + (size_t)(cap + kmax + 1) * kmax * 4 +
+           (size_t)((cap + 1 + 3) & ~3) * 4 + (size_t)((cap + 15) & ~15);
 }
 
 __global__ void __launch_bounds__(BT_THREADS) batched_kernel(BtParams P, int32_t kmax)
@@ -68,7 +70,8 @@ __global__ void __launch_bounds__(BT_THREADS) batched_kernel(BtParams P, int32_t
     int32_t *pref_s = reinterpret_cast<int32_t *>(bt_dyn);
     int32_t *tab_s = pref_s + kmax * ST;
     uint32_t *binom_s = reinterpret_cast<uint32_t *>(tab_s + kmax * ST);
-    uint8_t *pos_cls = reinterpret_cast<uint8_t *>(binom_s + (P.cap + kmax + 1) * kmax);
+    int32_t *dif_s = reinterpret_cast<int32_t *>(binom_s + (P.cap + kmax + 1) * kmax);   // [cap + 1]
+    uint8_t *pos_cls = reinterpret_cast<uint8_t *>(dif_s + ((P.cap + 1 + 3) & ~3));
 #define pref(k, j) pref_s[(k) * ST + (j)]
 #define tab(k, n) tab_s[(k) * ST + (n)]
 #define binom(n, r) binom_s[(n) * kmax + (r)]
@@ -197,6 +200,8 @@ __global__ void __launch_bounds__(BT_THREADS) batched_kernel(BtParams P, int32_t
             pref(k, j) = v;
         }
         __syncthreads();
+        for (int32_t j = tid; j <= N; j += BT_THREADS) dif_s[j] = pref(K - 2, j) - pref(K - 1, j);
+        __syncthreads();
 
         // ---- enumerate the count vectors: prefixes (n_0 .. n_{K-3}) ranked lexicographically, the
         // last two levels swept inline. Each thread takes a contiguous range of prefix ranks: it
@@ -258,13 +263,18 @@ __global__ void __launch_bounds__(BT_THREADS) batched_kernel(BtParams P, int32_t
             const uint64_t wa = a2 == 0 ? 0 : mul;
             const uint64_t wb = a2 == 0 ? 1 : mul * (uint64_t)(N + 1);
             const int32_t gb = gain + pref(b2, N) - pref(a2, S);
+            // per vector: two batch-table reads, one read of the level-difference prefix gains, two
+            // compares; the 64-bit counts code only when the vector is not worse than the best
+            const int32_t *__restrict__ tA = &tab(a2, 0);
+            const int32_t *__restrict__ tB = &tab(b2, left);          // tB[-v] = I_{K-1}(left - v)
+            const int32_t *__restrict__ dd = dif_s + S;               // dd[v] = P_{K-2}(S+v) - P_{K-1}(S+v)
             for (int32_t v = 0; v <= left; ++v) {
-                const int32_t u = left - v;
-                const int32_t c2 = cost + tab(a2, v) + tab(b2, u);
+                const int32_t c2 = cost + tA[v] + tB[-v];
                 if (c2 > B) continue;
-                const int32_t g2 = gb + pref(a2, S + v) - pref(b2, S + v);
-                const uint64_t code2 = code + (uint64_t)v * wa + (uint64_t)u * wb;
-                if (bt_better(g2, c2, code2, bg, bc, bk)) {
+                const int32_t g2 = gb + dd[v];
+                if (g2 < bg || (g2 == bg && c2 > bc)) continue;
+                const uint64_t code2 = code + (uint64_t)v * wa + (uint64_t)(left - v) * wb;
+                if (g2 > bg || c2 < bc || code2 < bk) {
                     bg = g2;
                     bc = c2;
                     bk = code2;
