@@ -345,7 +345,11 @@ turbo_status_t turbo_batched_workspace(const turbo_shape_t *shape, size_t *bytes
  * single-class short-row batches instead of one CTA per window;
  * variant & 16: the runtime-K kernel also for row class 3 of mixed-K plan launches;
  * variant & 32: never the runtime-K body (the fifteen K-specific bodies everywhere);
- * variant & 64: turbo_batched_plan plans every valid window with the general program (R20).
+ * variant & 64: turbo_batched_plan plans every valid window with the general program (R20);
+ * variant & 128: u16 rows (NEXT-5) for the windows that qualify in the fixed-K CTA kernels with
+ *   staged options and the walk in the kernel -- gains >= 0, a cost-0 exit in every frame,
+ *   sum_i max_k g + max g + 1 <= 65535. Opt-in: measured slower than the int32 rows on c2 (the
+ *   two-cells-per-word unpack costs more instructions than the halved shared loads save).
  * Returns INVALID_ARG for other values. Process-wide; not needed in production. */
 turbo_status_t turbo_debug_set_variant(int32_t variant);
 
@@ -356,6 +360,11 @@ turbo_status_t turbo_debug_set_variant(int32_t variant);
  * needed in production. Returns TURBO_ERR_UNSUPPORTED unless the library was built with
  * TURBO_TRACE defined (the marks are compiled out of production builds). */
 turbo_status_t turbo_debug_trace(int64_t *trace, int64_t words);
+/* Test hook: with counter != NULL (device memory, one int64, caller-owned and zeroed) every DP
+ * kernel launch that follows adds 1 per window it planned on u16 rows (NEXT-5, opt-in with
+ * turbo_debug_set_variant bit 128), so tests can prove which row format served a batch. NULL
+ * disables (the default). Process-wide; not needed in production. */
+turbo_status_t turbo_debug_u16_counter(int64_t *counter);
 /* Measurement hook (not a step of the method): the shared-memory roofline denominator. Launches
  * ctas_per_sm (1 or 2) x SMs CTAs of 1024 threads, each thread issuing iters x 32 conflict-free
  * shared loads of bytes_per_lane (4, 8 or 16) bytes (4: one 128-B wavefront per warp instruction,

@@ -144,9 +144,17 @@ turbo_status_t turbo_debug_trace(int64_t *trace, int64_t words)
     return TURBO_OK;
 }
 
+static int64_t *g_u16_count = nullptr;
+
+turbo_status_t turbo_debug_u16_counter(int64_t *counter)
+{
+    g_u16_count = counter;
+    return TURBO_OK;
+}
+
 turbo_status_t turbo_debug_set_variant(int32_t variant)
 {
-    if (variant < 0 || variant > 127 || (variant & 3) == 3) return TURBO_ERR_INVALID_ARG;
+    if (variant < 0 || variant > 255 || (variant & 3) == 3) return TURBO_ERR_INVALID_ARG;
     g_variant = variant;
     return TURBO_OK;
 }
@@ -301,14 +309,14 @@ static int solve_mode(const turbo_shape_t *cs)
     dp_smem_words(cs, DP_SOLVE_SMEM, &P);
     P.pad_words = dp_pad_words(cs);
     const int64_t bytes = (int64_t)dp_smem_bytes(P, dp_warps_per_window(cs));
-    if ((g_variant & 3) == 1) {
-        DeviceInfo d;
-        if (device_info(&d) == cudaSuccess && bytes <= (int64_t)d.smem_per_cta_optin) return DP_SOLVE_SMEM;
-        return DP_SOLVE_GLOBAL;
-    }
+    DeviceInfo d;
+    // planes in smem only when the whole CTA still fits (2-bit planes of long rows are below
+    // twice the rows yet over the per-CTA maximum with them)
+    const bool fits = device_info(&d) == cudaSuccess && bytes + 1024 <= (int64_t)d.smem_per_cta_optin;
+    if ((g_variant & 3) == 1) return fits ? DP_SOLVE_SMEM : DP_SOLVE_GLOBAL;
     const int64_t planes = (int64_t)P.chs_words * 4;
     const int64_t rows = bytes - planes;
-    return (planes <= smem_choice_floor || planes <= 2 * rows) ? DP_SOLVE_SMEM : DP_SOLVE_GLOBAL;
+    return fits && (planes <= smem_choice_floor || planes <= 2 * rows) ? DP_SOLVE_SMEM : DP_SOLVE_GLOBAL;
 }
 
 // Does a fused solve / schedule of this batch write any choice plane to HBM?
@@ -477,6 +485,8 @@ static DpParams base_params(const turbo_shape_t *shape, const turbo_window_t *wi
         dbg = e ? atoi(e) : 0;
     }
     P.debug = dbg;
+    P.u16 = (g_variant & 128) ? 1 : 0;                 // NEXT-5 u16 rows: opt-in
+    P.u16_count = g_u16_count;
     P.trace = g_trace;
     P.trace_words = g_trace_words;
     return P;

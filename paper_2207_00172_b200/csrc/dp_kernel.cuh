@@ -37,21 +37,22 @@ __device__ __forceinline__ int64_t warp_sum_i64(int64_t v)
 // "S_0[b] >= S_0[B]" is false ... false, true ... true on [0, B] and a 32-ary search finds its first
 // true cell in ceil(log_31(B + 1)) + 1 rounds of one load and one vote (B = 1000: 3 rounds) --
 // instead of counting the B + 1 cells below G* with every thread and a CTA-wide reduction.
-__device__ __forceinline__ int32_t warp_first_at_least(const int32_t *__restrict__ S, int32_t B, int32_t RB,
-                                                       int lane)
+// (T = int32_t: packed-key rows; T = uint16_t: the u16 rows of NEXT-5, values S + V0)
+template <class T>
+__device__ __forceinline__ int32_t warp_first_at_least(const T *__restrict__ S, int32_t B, int32_t RB, int lane)
 {
     int32_t lo = 0, hi = B;                               // invariant: answer in [lo, hi], S[hi] >= RB
     while (hi - lo >= 32) {
         const int32_t step = (hi - lo + 30) / 31;         // lane 31 probes >= hi
         const int32_t p = min(lo + lane * step, hi);
-        const unsigned m = __ballot_sync(0xffffffffu, S[p] >= RB);
+        const unsigned m = __ballot_sync(0xffffffffu, (int32_t)S[p] >= RB);
         const int f = __ffs(m) - 1;                       // m != 0: lane 31 probes hi
         const int32_t nhi = min(lo + f * step, hi);
         lo = f == 0 ? lo : lo + (f - 1) * step + 1;
         hi = nhi;
     }
     const int32_t p = lo + lane;
-    const unsigned m = __ballot_sync(0xffffffffu, p > hi || S[min(p, hi)] >= RB);
+    const unsigned m = __ballot_sync(0xffffffffu, p > hi || (int32_t)S[min(p, hi)] >= RB);
     return lo + __ffs(m) - 1;
 }
 
@@ -179,6 +180,89 @@ __device__ __forceinline__ void dp_tile(const DpParams &P, int32_t t, int32_t i,
         const int32_t v = key[r] & ~15;
         if (OWN) own[r] = v;
         if (fast || r < nr) dst[r * 32] = v;
+    }
+    const uint32_t word = pack_choices<RPT, CB>(key);
+    if (MODE == DP_SOLVE_SMEM)
+        sch[(i * ntiles + t) * 32 + lane] = word;
+    else
+        gch[((int64_t)i * gtiles + t) * 32 + lane] = word;
+}
+
+// ---- NEXT-5: u16 DP rows -------------------------------------------------------
+// For a window whose values fit 16 bits the row holds v = S + V0 as u16 -- two cells per 32-bit
+// word, so one conflict-free LDS.32 per option serves TWO cells (the 4-byte shared-load
+// instruction rate, not bytes, bounds the int32 rows: DESIGN.md §6). Eligibility (decided per
+// window on the device, dp_window): every gain >= 0, every frame has a cost-0 option (so every
+// cell b >= 0 is feasible and the only -inf cells are the pad below 0, stored as 0), and
+// sum_i max_k g_ik + V0 <= 65535 with V0 = max g + 1 (a candidate built on a pad cell, at most
+// max g, then loses to every real one, at least V0). Exactly the int32 recurrence and tie-break:
+// the key becomes (v << 16) | (15 - k), compared unsigned.
+// Layout of one row buffer X (int32 words [X - PW, X + RW)): pad0 = [X - PW, X - PW/2) (zeros),
+// copy0 = X - PW/2 (word q = cells 2q, 2q+1), pad1 = [X + RW/2 - PW/2, X + RW/2) (zeros),
+// copy1 = X + RW/2 (word q = cells 2q - 1, 2q: the row shifted by one cell, so an ODD shift is an
+// aligned word read of copy1 and an even one of copy0). Lane l of pair-row r of tile t owns pair
+// p = t RPT 16 + r 32 + l (cells 2p, 2p + 1); a tile spans the same RPT 32 cells as the int32 tile.
+template <int K, int MODE>
+__device__ __forceinline__ void dp_tile_u16(const DpParams &P, int32_t t, int32_t i, int32_t ntiles, int32_t gtiles,
+                                            const uint32_t *__restrict__ c0, const uint32_t *__restrict__ c1,
+                                            uint32_t *__restrict__ n0, uint16_t *__restrict__ n1h,
+                                            uint32_t *__restrict__ sch, uint32_t *__restrict__ gch,
+                                            const uint32_t (&gp)[K], const int32_t (&cc)[K], int32_t cmax,
+                                            bool inplace, int lane)
+{
+    constexpr int CB = (K <= 4) ? 2 : 4;
+    constexpr int RPT = 32 / CB;
+    constexpr int R2 = RPT / 2;                           // pair-rows per tile
+    const int32_t cells = P.row_words;                    // u16 cells per copy
+    const int32_t hp = P.pad_words >> 1;                  // pad words per copy
+    const int32_t b_lo = t * RPT * 32;
+    const int32_t p0 = t * RPT * 16 + lane;
+    const bool fast = cmax <= b_lo + 2 * hp;              // every read inside the row or its pad
+    TCHECK(2 * (p0 + (R2 - 1) * 32) + 1 < cells);
+    TCHECK(MODE != DP_SOLVE_SMEM || (int64_t)(i * ntiles + t) * 32 + 32 <= (int64_t)P.chs_words);
+    TCHECK(MODE == DP_SOLVE_SMEM || t < gtiles);
+    uint32_t klo[R2], khi[R2];
+    // option k of pair-row r: the word holding cells (2p - c, 2p + 1 - c) -> both candidate keys
+    auto upd = [&](int k, int r, uint32_t wv) {
+        const uint32_t lo = wv << 16, hi = wv & 0xffff0000u;
+        if (k == 0) {
+            klo[r] = lo + gp[0];
+            khi[r] = hi + gp[0];
+        } else {
+            klo[r] = __viaddmax_u32(lo, gp[k], klo[r]);
+            khi[r] = __viaddmax_u32(hi, gp[k], khi[r]);
+        }
+    };
+    if (fast) {                                           // unchecked: every shift stays in the pad
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const uint32_t *__restrict__ s = ((cc[k] & 1) ? c1 : c0) + (p0 - (cc[k] >> 1));
+#pragma unroll
+            for (int r = 0; r < R2; ++r) upd(k, r, s[r * 32]);
+        }
+    } else {                                              // low tiles: words below the pad read 0
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int32_t sh = cc[k] >> 1;
+            const uint32_t *__restrict__ s = ((cc[k] & 1) ? c1 : c0) + (p0 - sh);
+#pragma unroll
+            for (int r = 0; r < R2; ++r) {
+                const int32_t q = p0 + r * 32 - sh;
+                upd(k, r, q >= -hp ? s[q < -hp ? 0 : r * 32] : 0u);
+            }
+        }
+    }
+    if (inplace) __syncwarp();                            // all reads of this tile done
+    uint32_t *__restrict__ d0 = n0 + p0;
+    uint16_t *__restrict__ d1 = n1h + 2 * p0 + 1;         // copy1 u16 index of cell 2p is 2p + 1
+    int32_t key[RPT];
+#pragma unroll
+    for (int r = 0; r < R2; ++r) {
+        d0[r * 32] = __byte_perm(klo[r], khi[r], 0x7632);
+        d1[r * 64] = (uint16_t)(klo[r] >> 16);
+        if (2 * (p0 + r * 32) + 2 < cells) d1[r * 64 + 1] = (uint16_t)(khi[r] >> 16);
+        key[2 * r] = (int32_t)klo[r];
+        key[2 * r + 1] = (int32_t)khi[r];
     }
     const uint32_t word = pack_choices<RPT, CB>(key);
     if (MODE == DP_SOLVE_SMEM)
@@ -363,7 +447,8 @@ __device__ __forceinline__ void backtrack_warp_spec(int32_t N, int32_t b, const 
 // choice at b, lane 1 + a reads frame i+1's at b - c_{i,a} and (D = 3, when 1 + K + K^2 <= 32)
 // lane 1 + K + a K + a' reads frame i+2's at b - c_{i,a} - c_{i+1,a'}; shuffles then pick the
 // realised branch. Lane 0 writes the exits (global, and shared when exit_s != nullptr).
-template <int K, int MODE, class CostF>
+// U16: planes written by dp_tile_u16 (a lane's tile word holds the choices of its cell PAIRS).
+template <int K, int MODE, class CostF, bool U16 = false>
 __device__ __forceinline__ void backtrack_warp(int32_t N, int32_t b, const uint32_t *__restrict__ sch,
                                                const uint32_t *__restrict__ gch, int32_t ntiles, int32_t gtiles,
                                                CostF cost, uint8_t *__restrict__ exit_g, uint8_t *__restrict__ exit_s,
@@ -386,10 +471,18 @@ __device__ __forceinline__ void backtrack_warp(int32_t N, int32_t b, const uint3
     }
     auto choice = [&](int32_t i, int32_t cell) -> int32_t {
         const int32_t t = cell / (32 * RPT);
-        const int32_t j = (cell >> 5) & (RPT - 1);
+        int32_t ln, j;
+        if (U16) {                                    // cell q of the tile: pair q/2 = (row, lane)
+            const int32_t q = cell - t * 32 * RPT;
+            ln = (q >> 1) & 31;
+            j = 2 * (q >> 6) + (q & 1);
+        } else {
+            ln = cell & 31;
+            j = (cell >> 5) & (RPT - 1);
+        }
         TCHECK(cell >= 0 && i >= 0 && i < N && t < (MODE == DP_SOLVE_SMEM ? ntiles : gtiles));
-        const uint32_t word = (MODE == DP_SOLVE_SMEM) ? sch[(i * ntiles + t) * 32 + (cell & 31)]
-                                                      : gch[((int64_t)i * gtiles + t) * 32 + (cell & 31)];
+        const uint32_t word = (MODE == DP_SOLVE_SMEM) ? sch[(i * ntiles + t) * 32 + ln]
+                                                      : gch[((int64_t)i * gtiles + t) * 32 + ln];
         return (int32_t)((word >> choice_shift(j, CB)) & CMASK);
     };
     auto emit = [&](int32_t i, int32_t k) {
@@ -525,7 +618,8 @@ __device__ __forceinline__ void flush_window_stats(const DpParams &P, uint32_t *
 // chunk ahead) and the warp broadcasts it with shuffles (windows whose option table does not fit).
 // FUSE (turbo_schedule): a1 (budget from capacity) and a2 (options straight from class ids and
 // the profile, never materialised in HBM) in the prologue, a6 (statistics) in the epilogue.
-template <int K, int MODE, bool OSM, bool FUSE>
+// U16: windows that qualify (decided on the device, see dp_tile_u16) run the u16-row body.
+template <int K, int MODE, bool OSM, bool FUSE, bool U16 = false>
 __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t *__restrict__ rowA,
                                           int32_t *__restrict__ rowB, uint32_t *__restrict__ sch,
                                           int32_t *__restrict__ cst, int2 *__restrict__ opt_s,
@@ -534,6 +628,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
 {
     constexpr int CB = (K <= 4) ? 2 : 4;          // choice bits
     constexpr int RPT = 32 / CB;                   // rows of 32 cells per tile (per choice word)
+    static_assert(!U16 || (OSM && MODE != DP_PLAN), "u16 rows: staged options, walk in the kernel");
     const bool inplace = (nwarps == 1);
     const int tid = warp * 32 + lane;
     const int nthr = nwarps * 32;
@@ -639,8 +734,11 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     }
     if (warp == 0) {
         int64_t abs_sum = 0, g0_sum = 0, c0_sum = 0;
+        bool u_ok = true;                                 // U16: gains >= 0, a cost-0 option per frame
+        int32_t u_gmax = 0;
         for (int32_t i = lane; i < N; i += 32) {
             int32_t m = 0;
+            bool zc = false;
 #pragma unroll
             for (int k = 0; k < K; ++k) {
                 int32_t g, c;
@@ -660,18 +758,30 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
                     g0_sum += g;
                     c0_sum += c;
                 }
+                if (U16) {
+                    u_ok = u_ok && g >= 0;
+                    zc = zc || c == 0;
+                    u_gmax = max(u_gmax, g);
+                }
             }
             abs_sum += m;
+            u_ok = u_ok && zc;
         }
         abs_sum = warp_sum_i64(abs_sum);
         g0_sum = warp_sum_i64(g0_sum);
         c0_sum = warp_sum_i64(c0_sum);
         bad = __any_sync(0xffffffffu, bad) || abs_sum >= GAIN_RANGE_LIMIT || c0_sum >= 0x7fffffffll;
+        if (U16) {
+            u_ok = __all_sync(0xffffffffu, u_ok);
+            u_gmax = (int32_t)__reduce_max_sync(0xffffffffu, (uint32_t)u_gmax);
+        }
         if (lane == 0) {
             red[0] = bad ? 1 : 0;
             red[1] = g0_sum;
             red[2] = c0_sum;
             red[3] = 0;                                   // C* counter
+            // U16: V0 = max g + 1 when sum_i max_k g_ik + V0 fits 16 bits, else 0 (int32 rows)
+            red[4] = (U16 && P.u16 && N > 0 && u_ok && abs_sum + u_gmax + 1 <= 65535) ? u_gmax + 1 : 0;
         }
     }
     const int32_t ntiles = (((B + 32) >> 5) + RPT - 1) / RPT;
@@ -709,6 +819,135 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     // choice-plane stride (tiles per frame): the layout bound for HBM planes, exact for smem
     const int32_t gtiles = (int32_t)(((Bb + 32) >> 5) + RPT - 1) / RPT;
     uint32_t *__restrict__ gch = reinterpret_cast<uint32_t *>(P.workspace + choff);
+
+    // ---- a5 fused: forward backtrack from (frame 0, b = C*); a6 (fused): statistics
+    // (shared by the int32 and the u16 bodies; u16 planes use the pair mapping)
+    auto finish = [&](int32_t G, int32_t Cst, bool feas, bool u16) {
+        uint8_t *exit_s = nullptr;                        // fused + staged options: exits in smem
+        if (FUSE && OSM)
+            exit_s = reinterpret_cast<uint8_t *>(opt_s + P.max_options + P.prof_entries) + ((N + 3) & ~3);
+        if (!feas) {
+            for (int32_t i = tid; i < N; i += nthr) {
+                P.exit_out[ff + i] = 0;
+                if (exit_s) exit_s[i] = 0;
+            }
+        } else if (warp == 0 && !(P.debug & 16)) {
+            // costs of the walk: the staged table, or global memory (option table / profile row)
+            auto cost = [&](int32_t i, int32_t k) -> int32_t {
+                if (OSM) return opt_s[i * K + k].y;
+                int32_t g, c;
+                load_opt(i, k, g, c);
+                return c;
+            };
+            bool done = false;
+            if constexpr (U16) {
+                if (u16) {
+                    backtrack_warp<K, MODE, decltype(cost), true>(N, Cst, sch, gch, ntiles, gtiles, cost,
+                                                                  P.exit_out + ff, exit_s, lane);
+                    done = true;
+                }
+            }
+            if (done) {
+            } else if (MODE == DP_SOLVE_SMEM && OSM && (P.debug & 256)) {
+                backtrack_warp_spec<K, MODE>(N, Cst, sch, gch, ntiles, gtiles, cost, P.exit_out + ff, exit_s, lane);
+            } else {
+                backtrack_warp<K, MODE>(N, Cst, sch, gch, ntiles, gtiles, cost, P.exit_out + ff, exit_s, lane);
+            }
+        }
+        if (FUSE) {                                       // a6: CTA-private histograms
+            if (nwarps > 1) __syncthreads(); else __syncwarp();
+            trace_mark(P, w, 4);
+            for (int32_t i = tid; i < N; i += nthr) {
+                const uint32_t k = exit_s ? exit_s[i] : P.exit_out[ff + i];   // global: visible after the barrier
+                const uint32_t cls = class_of(i);
+                atomicAdd(&hist[k], 1u);
+                if (cls < 10) atomicAdd(&hist[16 + cls * 16 + k], 1u);
+            }
+            if (nwarps > 1) __syncthreads(); else __syncwarp();
+            if (!(P.debug & 8)) flush_window_stats(P, hist, G, Cst, feas, N, tid, nthr);
+        }
+    };
+
+    if constexpr (U16) {
+        if (red[4] != 0) {
+            // ---- NEXT-5: the u16-row body (dp_tile_u16). Options restaged as (g << 16 | 15 - k, c).
+            const uint32_t V0 = (uint32_t)red[4];
+            if (tid == 0 && P.u16_count != nullptr)
+                atomicAdd(reinterpret_cast<unsigned long long *>(P.u16_count), 1ull);
+            for (int32_t o = tid; o < N * K; o += nthr) {
+                const int32_t x = opt_s[o].x;
+                opt_s[o].x = (int32_t)(((uint32_t)(x >> 4) << 16) | (uint32_t)(x & 15));
+            }
+            const int32_t PW = P.pad_words, RW = P.row_words, HP = PW >> 1, HR = RW >> 1;
+            uint32_t *const A0 = reinterpret_cast<uint32_t *>(rowA) - HP;
+            uint32_t *const A1 = reinterpret_cast<uint32_t *>(rowA) + HR;
+            uint32_t *const B0 = reinterpret_cast<uint32_t *>(rowB) - HP;
+            uint32_t *const B1 = reinterpret_cast<uint32_t *>(rowB) + HR;
+            for (int32_t x = tid; x < HP; x += nthr) {    // pads: 0 = -inf (below every real v >= V0)
+                A0[x - HP] = 0;
+                A1[x - HP] = 0;
+                if (nwarps > 1) {
+                    B0[x - HP] = 0;
+                    B1[x - HP] = 0;
+                }
+            }
+            const uint32_t VV = V0 | (V0 << 16);          // S_N = 0 -> v = V0 on every cell b >= 0
+            for (int32_t x = tid; x < nrows * 16; x += nthr) {
+                A0[x] = VV;
+                A1[x] = x == 0 ? (V0 << 16) : VV;         // copy1 word 0 = (cell -1 = pad, cell 0)
+            }
+            if (nwarps > 1 && tid == 0) B1[0] = 0;        // cell -1 of the other buffer's copy1
+            if (nwarps > 1) __syncthreads(); else __syncwarp();
+            const uint32_t *c0 = A0, *c1 = A1;
+            uint32_t *n0 = inplace ? A0 : B0, *n1 = inplace ? A1 : B1;
+            const int32_t t0 = inplace ? ntiles - 1 : warp;
+            const int32_t dt = inplace ? -1 : nwarps;
+            for (int32_t i = N - 1; i >= 0; --i) {
+                uint32_t gp[K];
+                int32_t cc[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const int2 v = opt_s[i * K + k];
+                    gp[k] = (uint32_t)v.x;
+                    cc[k] = v.y;
+                }
+                int32_t cmax = cc[0];
+#pragma unroll
+                for (int k = 1; k < K; ++k) cmax = max(cmax, cc[k]);
+                for (int32_t t = t0; t >= 0 && t < ntiles; t += dt)
+                    dp_tile_u16<K, MODE>(P, t, i, ntiles, gtiles, c0, c1, n0, reinterpret_cast<uint16_t *>(n1), sch,
+                                         gch, gp, cc, cmax, inplace, lane);
+                if (nwarps > 1) __syncthreads(); else __syncwarp();
+                const uint32_t *t_0 = c0, *t_1 = c1;
+                c0 = n0;
+                c1 = n1;
+                n0 = const_cast<uint32_t *>(t_0);
+                n1 = const_cast<uint32_t *>(t_1);
+            }
+            trace_mark(P, w, 2);
+            // a4 on v = S_0 + V0 (every cell >= 0 feasible under the eligibility rule)
+            const uint16_t *v = reinterpret_cast<const uint16_t *>(c0);
+            const int32_t vB = v[B];
+            const bool feas = vB >= (int32_t)V0;
+            const int32_t cnt = (warp == 0 && feas) ? warp_first_at_least(v, B, vB, lane) : 0;
+            const int32_t G = feas ? vB - (int32_t)V0 : (int32_t)red[1];
+            const int32_t Cst = feas ? cnt : (int32_t)red[2];
+            if (tid == 0) {
+                P.best_gain[w] = G;
+                P.best_cost[w] = Cst;
+                P.feasible[w] = feas ? 1 : 0;
+            }
+            trace_mark(P, w, 3);
+            finish(G, Cst, feas, true);
+            // the int32 rows' -inf pads back for the CTA's next window
+            if (nwarps > 1) __syncthreads(); else __syncwarp();
+            for (int32_t x = tid; x < PW; x += nthr) {
+                rowA[x - PW] = NEG_R;
+                if (nwarps > 1) rowB[x - PW] = NEG_R;
+            }
+            return;
+        }
+    }
 
     // !OSM: options live in registers, CH = 32/K frames per warp-wide chunk (lane q*K + k holds
     // option k of the chunk's q-th frame); the next chunk is loaded while the current one is
@@ -816,41 +1055,7 @@ __device__ __forceinline__ void dp_window(const DpParams &P, int64_t w, int32_t 
     }
     trace_mark(P, w, 3);
     if (MODE == DP_PLAN) return;
-
-    // ---- a5 fused: forward backtrack from (frame 0, b = C*)
-    uint8_t *exit_s = nullptr;                            // fused + staged options: exits in smem
-    if (FUSE && OSM)
-        exit_s = reinterpret_cast<uint8_t *>(opt_s + P.max_options + P.prof_entries) + ((N + 3) & ~3);
-    if (!feas) {
-        for (int32_t i = tid; i < N; i += nthr) {
-            P.exit_out[ff + i] = 0;
-            if (exit_s) exit_s[i] = 0;
-        }
-    } else if (warp == 0 && !(P.debug & 16)) {
-        // costs of the walk: the staged table, or global memory (option table / profile row)
-        auto cost = [&](int32_t i, int32_t k) -> int32_t {
-            if (OSM) return opt_s[i * K + k].y;
-            int32_t g, c;
-            load_opt(i, k, g, c);
-            return c;
-        };
-        if (MODE == DP_SOLVE_SMEM && OSM && (P.debug & 256))
-            backtrack_warp_spec<K, MODE>(N, Cst, sch, gch, ntiles, gtiles, cost, P.exit_out + ff, exit_s, lane);
-        else
-            backtrack_warp<K, MODE>(N, Cst, sch, gch, ntiles, gtiles, cost, P.exit_out + ff, exit_s, lane);
-    }
-    if (FUSE) {                                           // a6: CTA-private histograms
-        if (nwarps > 1) __syncthreads(); else __syncwarp();
-        trace_mark(P, w, 4);
-        for (int32_t i = tid; i < N; i += nthr) {
-            const uint32_t k = exit_s ? exit_s[i] : P.exit_out[ff + i];   // global: visible after the barrier
-            const uint32_t cls = class_of(i);
-            atomicAdd(&hist[k], 1u);
-            if (cls < 10) atomicAdd(&hist[16 + cls * 16 + k], 1u);
-        }
-        if (nwarps > 1) __syncthreads(); else __syncwarp();
-        if (!(P.debug & 8)) flush_window_stats(P, hist, G, Cst, feas, N, tid, nthr);
-    }
+    finish(G, Cst, feas, false);
 }
 
 // Out-of-line instance per K for the mixed-K kernel: keeps that kernel a small switch over
@@ -1058,7 +1263,8 @@ __device__ __forceinline__ void dp_window_gen(const DpParams &P, int64_t w, cons
 // smem layout per CTA: [red: 8 x int64][pad][rowA][pad][rowB (G > 1)][options (OSM) | costs]
 // [choice planes (solve smem)]. The pads (pad_words of -inf below each row buffer) are written
 // once and never overwritten.
-template <int KSEL, int MODE, bool OSM, bool FUSE>
+// U16 (NEXT-5, opt-in): fixed-K kernels that plan qualifying windows on u16 rows (dp_u16.cu).
+template <int KSEL, int MODE, bool OSM, bool FUSE, bool U16 = false>
 // Register budget: 64 for fixed-K kernels (4 CTAs x 256 threads or 2 x 512 per SM); the
 // mixed-K kernel inlines every K and gets 128 to avoid spilling its hot loop.
 __global__ void __launch_bounds__(512, (KSEL == 0) ? 1 : 2) dp_cta_kernel(DpParams P)
@@ -1109,8 +1315,8 @@ __global__ void __launch_bounds__(512, (KSEL == 0) ? 1 : 2) dp_cta_kernel(DpPara
         const int rc = row_class((int64_t)P.windows[w].budget_bound + 1);
         if (rc >= TURBO_NUM_CLASSES || (P.cls >= 0 && rc != P.cls)) continue;   // other launch serves it
         if (KSEL != 0) {
-            dp_window<(KSEL > 0 ? KSEL : 2), MODE, OSM, FUSE>(P, w, rowA, rowB, sch, cst, opt_s, red, hist, warp, nwarps,
-                                                             lane);
+            dp_window<(KSEL > 0 ? KSEL : 2), MODE, OSM, FUSE, U16>(P, w, rowA, rowB, sch, cst, opt_s, red, hist,
+                                                                  warp, nwarps, lane);
         } else {
             switch (P.windows[w].num_exits) {
 #define TURBO_K_CASE(KK) \
@@ -1150,5 +1356,6 @@ dp_kernel_t dp_kernel_plan(int kmin, int kmax, bool osm);
 dp_kernel_t dp_kernel_generic(bool osm, bool fuse);
 dp_kernel_t dp_kernel_solve_smem(int kmin, int kmax, bool osm);
 dp_kernel_t dp_kernel_schedule(int kmin, int kmax, int mode, bool osm);
+dp_kernel_t dp_kernel_u16(int kmin, int kmax, bool fuse);
 
 }  // namespace turbo

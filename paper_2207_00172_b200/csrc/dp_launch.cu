@@ -84,10 +84,15 @@ static cudaError_t resolve_dp(const turbo_shape_t *shape, int mode, const DpPara
     // (HBM choice planes are always walked by a separate kernel: DP_SOLVE_GLOBAL never gets here)
     if (mode == DP_SOLVE_GLOBAL) return cudaErrorInvalidValue;
     if (P.generic && mode != DP_PLAN) return cudaErrorInvalidValue;
-    dp_kernel_t kern = P.generic               ? dp_kernel_generic(osm, P.fuse != 0)
-                       : P.fuse                ? dp_kernel_schedule(shape->min_exits, shape->max_exits, mode, osm)
-                       : mode == DP_PLAN         ? dp_kernel_plan(shape->min_exits, shape->max_exits, osm)
-                                                 : dp_kernel_solve_smem(shape->min_exits, shape->max_exits, osm);
+    // NEXT-5 u16 rows (opt-in, P.u16): the fixed-K fused-solve kernels with staged options
+    dp_kernel_t kern = (P.u16 && osm && mode == DP_SOLVE_SMEM && !P.generic)
+                           ? dp_kernel_u16(shape->min_exits, shape->max_exits, P.fuse != 0)
+                           : nullptr;
+    if (kern == nullptr)
+        kern = P.generic               ? dp_kernel_generic(osm, P.fuse != 0)
+               : P.fuse                ? dp_kernel_schedule(shape->min_exits, shape->max_exits, mode, osm)
+               : mode == DP_PLAN         ? dp_kernel_plan(shape->min_exits, shape->max_exits, osm)
+                                         : dp_kernel_solve_smem(shape->min_exits, shape->max_exits, osm);
     static std::mutex amu;
     static std::map<const void *, size_t> static_smem;
     size_t st_bytes = 0;

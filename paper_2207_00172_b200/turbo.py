@@ -67,7 +67,7 @@ EXPORTS = ["turbo_mckp_workspace", "turbo_profile_lookup", "turbo_mckp_plan", "t
            "turbo_mckp_solve", "turbo_mckp_solve_workspace", "turbo_mckp_plane_bytes", "turbo_schedule",
            "turbo_schedule_theta", "turbo_heuristic_plan", "turbo_stats",
            "turbo_bucketize", "turbo_batches", "turbo_batched_plan", "turbo_batched_workspace",
-           "turbo_debug_set_variant", "turbo_debug_trace", "turbo_debug_smem_stream", "turbo_debug_tcheck_selftest",
+           "turbo_debug_set_variant", "turbo_debug_trace", "turbo_debug_u16_counter", "turbo_debug_smem_stream", "turbo_debug_tcheck_selftest",
            "turbo_launch_count",
            "turbo_status_string", "turbo_abi_version"]
 
@@ -102,6 +102,7 @@ def load(path: Optional[str] = None):
     lib.turbo_batched_workspace.argtypes = [vp, vp]
     lib.turbo_debug_set_variant.argtypes = [i32]
     lib.turbo_debug_trace.argtypes = [vp, i64]
+    lib.turbo_debug_u16_counter.argtypes = [vp]
     lib.turbo_debug_smem_stream.argtypes = [i32, i32, i32, vp, vp, vp]
     lib.turbo_debug_tcheck_selftest.argtypes = [vp]
     lib.turbo_launch_count.argtypes = []
@@ -300,6 +301,13 @@ def debug_trace(buf=None):
         _check("turbo_debug_trace", load().turbo_debug_trace(None, 0))
     else:
         _check("turbo_debug_trace", load().turbo_debug_trace(ctypes.c_void_p(buf.data_ptr()), int(buf.numel())))
+
+
+def debug_u16_counter(buf=None):
+    """Count the windows the DP kernels plan on u16 rows (NEXT-5) into `buf` (one-element int64
+    device tensor, zeroed by the caller; turbo.h turbo_debug_u16_counter); None disables."""
+    _check("turbo_debug_u16_counter",
+           load().turbo_debug_u16_counter(None if buf is None else ctypes.c_void_p(buf.data_ptr())))
 
 
 # ----------------------------------------------------------------------------- planner object

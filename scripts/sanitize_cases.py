@@ -2,7 +2,8 @@
 """Small cases through every kernel path, for compute-sanitizer (one tool per run):
 the per-class CTA kernels (fused / plan / smem / HBM variants), the runtime-K kernel, the
 lockstep kernel, the long-window grid kernel on both its paths (halo segments and L2 rows) with
-its walk kernel, turbo_schedule_theta, the batches / latency kernel and both NEXT-4 kernels."""
+its walk kernel, the u16-row kernels (NEXT-5), turbo_schedule_theta, the batches / latency kernel and
+both NEXT-4 kernels."""
 import os
 import sys
 
@@ -34,6 +35,15 @@ def main():
     turbo.run_path(b, fused="all")
     torch.cuda.synchronize()
     turbo.debug_set_variant(0)
+    # NEXT-5 u16 rows (variant 128): in-place and multi-warp rows, shifts beyond the pad, fused and solve
+    wl = synth.make_nonneg_set(seed=5, W=60, K=5, max_frames=30, min_budget=0, max_budget=4000, max_gain=1400,
+                               max_cost=901, no_zero_frac=0.3)
+    for fused in ("all", True):
+        turbo.debug_set_variant(128)
+        b = turbo.batch_from_workload(wl, with_plan_workspace=False)
+        turbo.run_path(b, fused=fused)
+        torch.cuda.synchronize()
+        turbo.debug_set_variant(0)
     # NEXT-3 fused, NEXT-2 latency
     wl = synth.make_config(5, num_windows=24)
     b = turbo.batch_from_workload(wl, with_plan_workspace=False)

@@ -39,4 +39,6 @@ from .workloads import (  # noqa: F401
     supermodular_gain_table,
     batch_latency_table,
     with_budget_edges,
+    make_nonneg_set,
+    make_u16_boundary,
 )

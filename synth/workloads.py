@@ -405,6 +405,52 @@ def make_batched_random(seed: int, W: int, max_frames: int = 8, K: int = 3, C: i
     return wl
 
 
+# ----------------------------------------------------------------------------- NEXT-5 parity sets
+S_NN_GAIN, S_NN_COST, S_NN_ZERO, S_NN_N, S_NN_B, S_NN_PROF, S_NN_NOZ = range(50, 57)
+
+
+def make_nonneg_set(seed: int, W: int, K: int, max_frames: int, min_budget: int, max_budget: int,
+                    max_gain: int, max_cost: int, num_profiles: int = 8, C: int = NUM_CLASSES,
+                    no_zero_frac: float = 0.0, base_cost: int = 5) -> Workload:
+    """Windows of ONE K with gains U{0..max_gain} and costs U{0..max_cost}, where in every class
+    row one exit (drawn per row, not always exit 0) costs 0 -- the shape of the paper's tables
+    (gains >= 0, the no-enhancement exit free) that the u16 rows of NEXT-5 serve. A fraction
+    `no_zero_frac` of the profiles keeps no cost-0 exit (those windows stay on int32 rows).
+    Budgets U{min_budget..max_budget}, N U{0..max_frames}. Inputs only."""
+    gains, costs, shapes = [], [], []
+    for p in range(num_profiles):
+        n = C * K
+        g = rand_int(seed, S_NN_GAIN, p * 4096 + np.arange(n), 0, max_gain).astype(np.int32)
+        c = rand_int(seed, S_NN_COST, p * 4096 + np.arange(n), 0, max_cost).astype(np.int32)
+        if rand_uniform(seed, S_NN_NOZ, p) >= no_zero_frac:
+            z = rand_int(seed, S_NN_ZERO, p * 64 + np.arange(C), 0, K - 1)
+            c.reshape(C, K)[np.arange(C), z] = 0
+        else:
+            c = np.maximum(c, 1).astype(np.int32)
+        gains.append(g)
+        costs.append(c)
+        shapes.append((C, K))
+    wid = np.arange(W)
+    N = rand_int(seed, S_NN_N, wid, 0, max_frames).astype(np.int32)
+    B = rand_int(seed, S_NN_B, wid, min_budget, max_budget).astype(np.int32)
+    prof = rand_int(seed, S_NN_PROF, wid, 0, num_profiles - 1).astype(np.int32)
+    u = rand_uniform(seed, S_CLASS, np.arange(int(N.sum())))
+    cls = np.minimum((u * C).astype(np.int64), C - 1)
+    return _wl(f"nonneg{seed}_K{K}", gains, costs, shapes, N, B, prof, cls, base_cost, {"seed": seed})
+
+
+def make_u16_boundary(y: int, base_cost: int = 5) -> Workload:
+    """One window at the edge of the u16 row rule (NEXT-5): 21 frames, K = 4, costs (0, 1, 2, 3),
+    20 frames with gains (0, 1, 2, 3000) and one with (0, 1, 2, y), budget 63 (every frame can
+    take exit 3), and the same frames under budgets 40, 17 and 0. sum_i max_k g + max g + 1 =
+    63001 + y: y = 2534 is exactly 65535 (u16 rows), y = 2535 one above (int32 rows). Inputs only."""
+    g = np.array([0, 1, 2, 3000, 0, 1, 2, y], dtype=np.int32)
+    c = np.array([0, 1, 2, 3, 0, 1, 2, 3], dtype=np.int32)
+    cls = np.array(([0] * 10 + [1] + [0] * 10) * 4, dtype=np.int64)
+    return _wl(f"u16_boundary_{y}", [g], [c], [(2, 4)], [21] * 4, [63, 40, 17, 0], [0] * 4, cls, base_cost,
+               {"y": y})
+
+
 # ----------------------------------------------------------------------------- a1 edge inputs
 S_EDGE_MODE, S_EDGE_VAL = 40, 41
 
