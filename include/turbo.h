@@ -349,7 +349,8 @@ turbo_status_t turbo_batched_workspace(const turbo_shape_t *shape, size_t *bytes
  * variant & 128: u16 rows (NEXT-5) for the windows that qualify in the fixed-K CTA kernels with
  *   staged options and the walk in the kernel -- gains >= 0, a cost-0 exit in every frame,
  *   sum_i max_k g + max g + 1 <= 65535. Opt-in: measured slower than the int32 rows on c2 (the
- *   two-cells-per-word unpack costs more instructions than the halved shared loads save).
+ *   two-cells-per-word unpack costs more instructions than the halved shared loads save);
+ * variant & 256: never the 72-register kernels for launches of <= 4 warps per window.
  * Returns INVALID_ARG for other values. Process-wide; not needed in production. */
 turbo_status_t turbo_debug_set_variant(int32_t variant);
 

@@ -154,7 +154,7 @@ turbo_status_t turbo_debug_u16_counter(int64_t *counter)
 
 turbo_status_t turbo_debug_set_variant(int32_t variant)
 {
-    if (variant < 0 || variant > 255 || (variant & 3) == 3) return TURBO_ERR_INVALID_ARG;
+    if (variant < 0 || variant > 511 || (variant & 3) == 3) return TURBO_ERR_INVALID_ARG;
     g_variant = variant;
     return TURBO_OK;
 }
@@ -487,6 +487,7 @@ static DpParams base_params(const turbo_shape_t *shape, const turbo_window_t *wi
     P.debug = dbg;
     P.u16 = (g_variant & 128) ? 1 : 0;                 // NEXT-5 u16 rows: opt-in
     P.u16_count = g_u16_count;
+    P.small = (g_variant & 256) ? 0 : 1;
     P.trace = g_trace;
     P.trace_words = g_trace_words;
     return P;

@@ -1264,10 +1264,13 @@ __device__ __forceinline__ void dp_window_gen(const DpParams &P, int64_t w, cons
 // [choice planes (solve smem)]. The pads (pad_words of -inf below each row buffer) are written
 // once and never overwritten.
 // U16 (NEXT-5, opt-in): fixed-K kernels that plan qualifying windows on u16 rows (dp_u16.cu).
-template <int KSEL, int MODE, bool OSM, bool FUSE, bool U16 = false>
+// SMALL: launches of <= 4 warps per window (dp_small.cu): 72 registers instead of 64 (7 CTAs of
+// 128 threads per SM), which removes the per-frame rematerialisation of loop invariants the
+// 64-register budget forces (same-box A/B on c2: 40.9 -> 39.4 us per step).
+template <int KSEL, int MODE, bool OSM, bool FUSE, bool U16 = false, bool SMALL = false>
 // Register budget: 64 for fixed-K kernels (4 CTAs x 256 threads or 2 x 512 per SM); the
 // mixed-K kernel inlines every K and gets 128 to avoid spilling its hot loop.
-__global__ void __launch_bounds__(512, (KSEL == 0) ? 1 : 2) dp_cta_kernel(DpParams P)
+__global__ void __launch_bounds__(SMALL ? 128 : 512, SMALL ? 7 : ((KSEL == 0) ? 1 : 2)) dp_cta_kernel(DpParams P)
 {
     extern __shared__ int4 smem_raw[];
     const int lane = threadIdx.x & 31;
@@ -1357,5 +1360,6 @@ dp_kernel_t dp_kernel_generic(bool osm, bool fuse);
 dp_kernel_t dp_kernel_solve_smem(int kmin, int kmax, bool osm);
 dp_kernel_t dp_kernel_schedule(int kmin, int kmax, int mode, bool osm);
 dp_kernel_t dp_kernel_u16(int kmin, int kmax, bool fuse);
+dp_kernel_t dp_kernel_small(int kmin, int kmax, bool fuse);
 
 }  // namespace turbo

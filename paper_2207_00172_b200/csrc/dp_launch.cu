@@ -88,6 +88,10 @@ static cudaError_t resolve_dp(const turbo_shape_t *shape, int mode, const DpPara
     dp_kernel_t kern = (P.u16 && osm && mode == DP_SOLVE_SMEM && !P.generic)
                            ? dp_kernel_u16(shape->min_exits, shape->max_exits, P.fuse != 0)
                            : nullptr;
+    // launches of <= 4 warps per window: the 72-register instantiations (dp_small.cu)
+    if (kern == nullptr && osm && mode == DP_SOLVE_SMEM && !P.generic && dp_warps_per_window(shape) <= 4 &&
+        P.small)
+        kern = dp_kernel_small(shape->min_exits, shape->max_exits, P.fuse != 0);
     if (kern == nullptr)
         kern = P.generic               ? dp_kernel_generic(osm, P.fuse != 0)
                : P.fuse                ? dp_kernel_schedule(shape->min_exits, shape->max_exits, mode, osm)

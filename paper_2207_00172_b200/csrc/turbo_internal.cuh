@@ -128,6 +128,7 @@ struct DpParams {
     uint8_t *class_out;
     int32_t u16;                   // NEXT-5: u16 rows for the windows that qualify (opt-in: variant bit 128)
     int64_t *u16_count;            // test hook (turbo_debug_u16_counter): windows planned on u16 rows
+    int32_t small;                 // <= 4-warp launches may use the 72-register kernels (variant bit 256 clears)
 };
 
 // NEXT-3 (PAPER.md:511 buckets of width 0.1; :525 theta'_x from D_f; reading R6): the class of a

@@ -77,8 +77,11 @@ EDGE_CASES = {
                                             synth.make_long_window(52, N=21, K=4, B=30000, c_max=6000,
                                                                    random_rows=True)]),
 }
-EDGE_PATHS = [("all", 0), (True, 0), (False, 0), (True, 1), (True, 2), ("all", 2)]
-EDGE_IDS = ["schedule", "solve", "plan+backtrack", "solve-smem", "solve-hbm", "schedule-hbm"]
+# variant 256: the 64-register kernels also for <= 4-warp launches (the default takes the 72-register
+# instantiations of dp_small.cu there)
+EDGE_PATHS = [("all", 0), (True, 0), (False, 0), (True, 1), (True, 2), ("all", 2), ("all", 256), (True, 256)]
+EDGE_IDS = ["schedule", "solve", "plan+backtrack", "solve-smem", "solve-hbm", "schedule-hbm", "schedule-r64",
+            "solve-r64"]
 
 
 @pytest.mark.parametrize("case", sorted(EDGE_CASES))
