@@ -338,6 +338,13 @@ turbo_status_t turbo_batched_plan(const turbo_shape_t *shape /* host */, const t
  * (0: the shape is too large for that program -- such windows are then rejected). Host only. */
 turbo_status_t turbo_batched_workspace(const turbo_shape_t *shape, size_t *bytes /* host, out */);
 
+/* Copy `bytes` from src to dst with the SMs (one kernel on `stream`) instead of a copy engine.
+ * Both pointers must be device-accessible: device memory, or pinned host memory (cudaHostAlloc /
+ * torch pin_memory, mapped through unified addressing). Not a step of the method: the transfer of
+ * a serving loop's per-step inputs and results, a few tens of KB, where a copy-engine transfer's
+ * fixed latency dominates. INVALID_ARG for NULL pointers with bytes > 0. */
+turbo_status_t turbo_memcpy_sm(void *dst, const void *src, size_t bytes, turbo_stream_t stream);
+
 /* Debug / test hook: force a DP kernel variant. variant & 3: 0 = automatic, 1 = fused solve
  * keeps choice planes in shared memory (when they fit the per-CTA maximum), 2 = in HBM;
  * variant & 4: do not stage option tables in shared memory (shuffle broadcast instead);

@@ -68,7 +68,7 @@ EXPORTS = ["turbo_mckp_workspace", "turbo_profile_lookup", "turbo_mckp_plan", "t
            "turbo_schedule_theta", "turbo_heuristic_plan", "turbo_stats",
            "turbo_bucketize", "turbo_batches", "turbo_batched_plan", "turbo_batched_workspace",
            "turbo_debug_set_variant", "turbo_debug_trace", "turbo_debug_u16_counter", "turbo_debug_smem_stream", "turbo_debug_tcheck_selftest",
-           "turbo_launch_count",
+           "turbo_launch_count", "turbo_memcpy_sm",
            "turbo_status_string", "turbo_abi_version"]
 
 _lib = None
@@ -106,6 +106,7 @@ def load(path: Optional[str] = None):
     lib.turbo_debug_smem_stream.argtypes = [i32, i32, i32, vp, vp, vp]
     lib.turbo_debug_tcheck_selftest.argtypes = [vp]
     lib.turbo_launch_count.argtypes = []
+    lib.turbo_memcpy_sm.argtypes = [vp, vp, sz, vp]
     lib.turbo_launch_count.restype = i64
     lib.turbo_status_string.restype = ctypes.c_char_p
     lib.turbo_abi_version.restype = i32
@@ -301,6 +302,15 @@ def debug_trace(buf=None):
         _check("turbo_debug_trace", load().turbo_debug_trace(None, 0))
     else:
         _check("turbo_debug_trace", load().turbo_debug_trace(ctypes.c_void_p(buf.data_ptr()), int(buf.numel())))
+
+
+def memcpy_sm(dst, src, stream=None):
+    """dst <- src (same byte size) copied by the SMs (turbo.h turbo_memcpy_sm): device tensors or
+    pinned host tensors (pin_memory), e.g. a serving step's inputs and results."""
+    n = dst.numel() * dst.element_size()
+    if src.numel() * src.element_size() != n:
+        raise ValueError("memcpy_sm: size mismatch")
+    _check("turbo_memcpy_sm", load().turbo_memcpy_sm(_ptr(dst), _ptr(src), n, _stream(stream)))
 
 
 def debug_u16_counter(buf=None):
