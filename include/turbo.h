@@ -95,8 +95,8 @@ typedef struct {
     int32_t ordered;             /* 1: the kernels serve windows through turbo_window_t.order
                                     (several classes, or uneven work); 0: in index order        */
     int32_t cls_order;           /* launch order of the row-size classes, 4 bits each from the
-                                    lowest nibble (turbo_mckp_workspace: 0x3210, smallest rows
-                                    first); not a permutation -> that default                   */
+                                    lowest nibble (turbo_mckp_workspace: 0x0123, longest rows
+                                    first); not a permutation -> 0x3210                   */
     int64_t reserved3;
     /* per row-size class (TURBO_NUM_CLASSES, see below): windows of one class are planned by one
      * launch shaped for them (warps per window, shared memory, residency) */

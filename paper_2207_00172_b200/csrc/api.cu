@@ -242,10 +242,11 @@ turbo_status_t turbo_mckp_workspace(const turbo_profile_t *profiles_host, int32_
         }
         for (int c = 0; c <= TURBO_NUM_CLASSES; ++c)
             if (wmax[c] > 0 && wmax[c] * 2 > wmin[c] * 3) uneven = true;
-        // class launch order: smallest rows first. (Heaviest-window-first by N (B+1) (K+1) was
-        // measured slower on c5, 2.63 vs 2.53 ms: a class's launch shape, not its work estimate,
-        // decides how long its heaviest window takes -- class-2 windows share an SM four ways.)
-        s.cls_order = 0x3210;
+        // class launch order: longest rows first, so the short-row classes fill the SMs the
+        // longest-row launch leaves idle in its last wave (c5, 16,384 windows, same box: 13.44 vs
+        // 13.52 ms smallest-first; scripts/cls_order.py). (Round 1, 2,048 windows: heaviest-window-
+        // first by N (B+1) (K+1) ACROSS classes was slower, 2.63 vs 2.53 ms.)
+        s.cls_order = 0x0123;
         s.ordered = (n_cls > 1 || uneven) ? 1 : 0;
         if (s.ordered) {
             std::sort(key.begin(), key.end());
