@@ -21,6 +21,8 @@
 //    warp broadcasts it with shuffles.
 #pragma once
 
+#include <type_traits>
+
 #include "turbo_internal.cuh"
 
 namespace turbo {
@@ -1200,49 +1202,68 @@ __device__ __forceinline__ void dp_window_gen(const DpParams &P, int64_t w, cons
     const int32_t t0 = inplace ? ntiles - 1 : warp;
     const int32_t dt = inplace ? -1 : nwarps;
     const int32_t pad = P.pad_words;
+    // rows of 32 cells that hold cells <= B: the last tile computes only its live rows, in groups of
+    // four (rows above B are never read by a cell <= B; their choice bits are never walked). Short
+    // rows are most of a mixed batch's windows (c5: B from 64) and a tile is 256 or 512 cells.
+    const int32_t live_rows = (B + 32) >> 5;
+    const int32_t last_groups = (live_rows - (ntiles - 1) * RPT + 3) >> 2;   // 1 .. RPT / 4
+    // one tile: keys of its first NR rows from `cur`, values to `nxt`, choice word to the plane
+    auto tile = [&](auto nr_tag, int32_t i, int32_t t, int q) {
+        constexpr int NR = decltype(nr_tag)::value;
+        const int32_t b_lo = t * RPT * 32;
+        TCHECK(b_lo + RPT * 32 <= P.row_words && t < gtiles);
+        int32_t key[RPT];
+#pragma unroll
+        for (int r = 0; r < RPT; ++r) key[r] = NEG_R;
+        for (int k = 0; k < K; ++k) {
+            int32_t g, c;
+            if (OSM) {
+                const int2 v = opt_s[i * K + k];
+                g = v.x;
+                c = v.y;
+            } else {
+                g = __shfl_sync(0xffffffffu, a_gp, q * K + k);
+                c = __shfl_sync(0xffffffffu, a_c, q * K + k);
+            }
+            if (c <= b_lo + pad) {
+                TCHECK(b_lo - c >= -pad);
+                const int32_t *__restrict__ s = cur + (b_lo + lane - c);
+#pragma unroll
+                for (int r = 0; r < NR; ++r) key[r] = max_plus(s[r * 32], g, key[r]);
+            } else if (c < b_lo + NR * 32) {
+#pragma unroll
+                for (int r = 0; r < NR; ++r) {
+                    const int32_t idx = b_lo + r * 32 + lane - c;
+                    const int32_t v = idx < 0 ? NEG_R : cur[idx < 0 ? 0 : idx];
+                    key[r] = max_plus(v, g, key[r]);
+                }
+            }
+        }
+        if (inplace) __syncwarp();                          // all reads of this tile done
+        int32_t *__restrict__ dst = nxt + b_lo + lane;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) dst[r * 32] = key[r] & ~15;
+        gch[((int64_t)i * gtiles + t) * 32 + lane] = pack_choices<RPT, CB>(key);
+    };
+    int q = 0;                                              // frame index inside the option chunk
     for (int32_t i = N - 1; i >= 0; --i) {
         const int32_t f = N - 1 - i;
-        const int q = f % CH;
-        if (!OSM && q == 0 && f > 0) {
+        if (!OSM && f > 0 && ++q == CH) {
+            q = 0;
             a_gp = (b_g << 4) | (15 - lk);
             a_c = b_c;
             load_raw(i - CH, b_g, b_c);
         }
         for (int32_t t = t0; t >= 0 && t < ntiles; t += dt) {
-            const int32_t b_lo = t * RPT * 32;
-            TCHECK(b_lo + RPT * 32 <= P.row_words && t < gtiles);
-            int32_t key[RPT];
-#pragma unroll
-            for (int r = 0; r < RPT; ++r) key[r] = NEG_R;
-            for (int k = 0; k < K; ++k) {
-                int32_t g, c;
-                if (OSM) {
-                    const int2 v = opt_s[i * K + k];
-                    g = v.x;
-                    c = v.y;
-                } else {
-                    g = __shfl_sync(0xffffffffu, a_gp, q * K + k);
-                    c = __shfl_sync(0xffffffffu, a_c, q * K + k);
-                }
-                if (c <= b_lo + pad) {
-                    TCHECK(b_lo - c >= -pad);
-                    const int32_t *__restrict__ s = cur + (b_lo + lane - c);
-#pragma unroll
-                    for (int r = 0; r < RPT; ++r) key[r] = max_plus(s[r * 32], g, key[r]);
-                } else if (c < b_lo + RPT * 32) {
-#pragma unroll
-                    for (int r = 0; r < RPT; ++r) {
-                        const int32_t idx = b_lo + r * 32 + lane - c;
-                        const int32_t v = idx < 0 ? NEG_R : cur[idx < 0 ? 0 : idx];
-                        key[r] = max_plus(v, g, key[r]);
-                    }
-                }
+            if (t < ntiles - 1 || last_groups * 4 >= RPT) {
+                tile(std::integral_constant<int, RPT>(), i, t, q);
+            } else if (CB == 4 || last_groups == 1) {       // RPT 8: 4 live rows; RPT 16: 4
+                tile(std::integral_constant<int, 4>(), i, t, q);
+            } else if (last_groups == 2) {
+                tile(std::integral_constant<int, (CB == 2 ? 8 : 4)>(), i, t, q);
+            } else {
+                tile(std::integral_constant<int, (CB == 2 ? 12 : 4)>(), i, t, q);
             }
-            if (inplace) __syncwarp();                      // all reads of this tile done
-            int32_t *__restrict__ dst = nxt + b_lo + lane;
-#pragma unroll
-            for (int r = 0; r < RPT; ++r) dst[r * 32] = key[r] & ~15;
-            gch[((int64_t)i * gtiles + t) * 32 + lane] = pack_choices<RPT, CB>(key);
         }
         if (nwarps > 1) __syncthreads(); else __syncwarp();
         int32_t *tmp = cur;
