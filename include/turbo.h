@@ -357,7 +357,8 @@ turbo_status_t turbo_memcpy_sm(void *dst, const void *src, size_t bytes, turbo_s
  *   staged options and the walk in the kernel -- gains >= 0, a cost-0 exit in every frame,
  *   sum_i max_k g + max g + 1 <= 65535. Opt-in: measured slower than the int32 rows on c2 (the
  *   two-cells-per-word unpack costs more instructions than the halved shared loads save);
- * variant & 256: never the 72-register kernels for launches of <= 4 warps per window.
+ * variant & 256: never the 72-register kernels (fixed-K fused solve and runtime-K) for launches of
+ *   <= 4 warps per window.
  * Returns INVALID_ARG for other values. Process-wide; not needed in production. */
 turbo_status_t turbo_debug_set_variant(int32_t variant);
 

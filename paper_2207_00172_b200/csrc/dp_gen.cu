@@ -9,8 +9,9 @@
 
 namespace turbo {
 
-template <bool OSM, bool FUSE>
-__global__ void __launch_bounds__(512, 2) dp_gen_kernel(DpParams P)
+// SMALL: launches of <= 4 warps per window (row classes 0-1): 72 registers (7 x 128 threads / SM)
+template <bool OSM, bool FUSE, bool SMALL = false>
+__global__ void __launch_bounds__(SMALL ? 128 : 512, SMALL ? 7 : 2) dp_gen_kernel(DpParams P)
 {
     extern __shared__ int4 smem_raw[];
     const int lane = threadIdx.x & 31;
@@ -45,8 +46,12 @@ __global__ void __launch_bounds__(512, 2) dp_gen_kernel(DpParams P)
     }
 }
 
-dp_kernel_t dp_kernel_generic(bool osm, bool fuse)
+dp_kernel_t dp_kernel_generic(bool osm, bool fuse, bool small)
 {
+    if (small) {             // same-box A/B, c5: 13.28 -> 13.20 ms
+        if (fuse) return osm ? dp_gen_kernel<true, true, true> : dp_gen_kernel<false, true, true>;
+        return osm ? dp_gen_kernel<true, false, true> : dp_gen_kernel<false, false, true>;
+    }
     if (fuse) return osm ? dp_gen_kernel<true, true> : dp_gen_kernel<false, true>;
     return osm ? dp_gen_kernel<true, false> : dp_gen_kernel<false, false>;
 }

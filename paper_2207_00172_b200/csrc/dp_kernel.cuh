@@ -1377,7 +1377,7 @@ dp_kernel_t pick_dp_kernel(int kmin, int kmax)
 }
 
 dp_kernel_t dp_kernel_plan(int kmin, int kmax, bool osm);
-dp_kernel_t dp_kernel_generic(bool osm, bool fuse);
+dp_kernel_t dp_kernel_generic(bool osm, bool fuse, bool small);
 dp_kernel_t dp_kernel_solve_smem(int kmin, int kmax, bool osm);
 dp_kernel_t dp_kernel_schedule(int kmin, int kmax, int mode, bool osm);
 dp_kernel_t dp_kernel_u16(int kmin, int kmax, bool fuse);

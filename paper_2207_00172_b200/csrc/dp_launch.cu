@@ -93,7 +93,7 @@ static cudaError_t resolve_dp(const turbo_shape_t *shape, int mode, const DpPara
         P.small)
         kern = dp_kernel_small(shape->min_exits, shape->max_exits, P.fuse != 0);
     if (kern == nullptr)
-        kern = P.generic               ? dp_kernel_generic(osm, P.fuse != 0)
+        kern = P.generic               ? dp_kernel_generic(osm, P.fuse != 0, dp_warps_per_window(shape) <= 4 && P.small)
                : P.fuse                ? dp_kernel_schedule(shape->min_exits, shape->max_exits, mode, osm)
                : mode == DP_PLAN         ? dp_kernel_plan(shape->min_exits, shape->max_exits, osm)
                                          : dp_kernel_solve_smem(shape->min_exits, shape->max_exits, osm);
@@ -199,7 +199,7 @@ cudaError_t launch_dp(const turbo_shape_t *shape, int mode, const DpParams &P0, 
 }  // namespace turbo
 
 namespace turbo {
-dp_kernel_t dp_kernel_generic(bool osm, bool fuse);
+dp_kernel_t dp_kernel_generic(bool osm, bool fuse, bool small);
 dp_kernel_t dp_kernel_sched_smem_osm(int kmin, int kmax);
 dp_kernel_t dp_kernel_sched_smem_reg(int kmin, int kmax);
 dp_kernel_t dp_kernel_sched_global_osm(int kmin, int kmax);

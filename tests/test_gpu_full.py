@@ -168,9 +168,10 @@ def test_lockstep_kernel_bad_class_and_range():
 
 
 # The runtime-K kernel (dp_gen.cu) serves the mixed-K plan-mode launches of row classes 0-2 by
-# default; variant 16 extends it to the longest-row class, variant 32 turns it off (fifteen
-# K-specific bodies). Every combination must give the same bits as the oracle.
-@pytest.mark.parametrize("variant", [0, 16, 32])
+# default (72-register instantiation for <= 4 warps per window; variant 256: the 64-register one);
+# variant 16 extends it to the longest-row class, variant 32 turns it off (fifteen K-specific
+# bodies). Every combination must give the same bits as the oracle.
+@pytest.mark.parametrize("variant", [0, 16, 32, 256])
 @pytest.mark.parametrize("fused", ["all", True, False], ids=["schedule", "solve", "plan+backtrack"])
 def test_runtime_k_body(variant, fused):
     tie = synth.make_tie_heavy(seed=909, W=600, max_frames=60, max_exits=16, max_budget=6000, max_cost=40,
