@@ -124,6 +124,12 @@ typedef struct {
  * frame -- same results, slower; no cost is rejected for its size (reading R17). */
 #define TURBO_BIG_CELLS 24576
 #define TURBO_BIG_MAX_COST 4096
+/* Long rows up to this many cells are planned by a thread-block CLUSTER per window instead (up to
+ * 8 CTAs on neighbouring SMs, each owning a power-of-two segment of the row in shared memory, the
+ * cells below a segment read from the lower CTAs' shared memory through distributed shared
+ * memory, one cluster barrier per frame, any option cost): many such windows run at once. Longer
+ * rows (e.g. 2^20 cells) keep the grid kernel. Same results either way. */
+#define TURBO_CLUSTER_CELLS 131072
 
 /* Number of int64 words of the status vector written by lookup / plan. */
 #define TURBO_STATUS_WORDS 2
@@ -226,8 +232,9 @@ turbo_status_t turbo_mckp_plane_bytes(const turbo_shape_t *shape, const turbo_wi
  * turbo_mckp_solve, a6 ACCUMULATED into stats (int64[181], caller zeroes it).
  * Outputs are bit-identical to lookup -> solve -> stats. Workspace as turbo_mckp_solve
  * (turbo_mckp_solve_workspace() bytes). Windows of every size are served: rows up to
- * TURBO_BIG_CELLS cells by one launch per row-size class, longer rows by the long-window grid
- * kernel with a1, a2 and a6 fused into it as well. Returns TURBO_ERR_UNSUPPORTED (before any
+ * TURBO_BIG_CELLS cells by one launch per row-size class, longer rows by the cluster kernel
+ * (up to TURBO_CLUSTER_CELLS) or the long-window grid kernel, with a1, a2 and a6 fused into them
+ * as well. Returns TURBO_ERR_UNSUPPORTED (before any
  * launch) only when a launch cannot fit the device (a long row too large for the grid's shared
  * memory, about 1.8M cells on 148 SMs). */
 turbo_status_t turbo_schedule(const turbo_shape_t *shape /* host */, const turbo_profile_t *profiles,
@@ -358,7 +365,8 @@ turbo_status_t turbo_memcpy_sm(void *dst, const void *src, size_t bytes, turbo_s
  *   sum_i max_k g + max g + 1 <= 65535. Opt-in: measured slower than the int32 rows on c2 (the
  *   two-cells-per-word unpack costs more instructions than the halved shared loads save);
  * variant & 256: never the 72-register kernels (fixed-K fused solve and runtime-K) for launches of
- *   <= 4 warps per window.
+ *   <= 4 warps per window;
+ * variant & 512: long rows all on the grid kernel (no cluster kernel).
  * Returns INVALID_ARG for other values. Process-wide; not needed in production. */
 turbo_status_t turbo_debug_set_variant(int32_t variant);
 

@@ -154,7 +154,7 @@ turbo_status_t turbo_debug_u16_counter(int64_t *counter)
 
 turbo_status_t turbo_debug_set_variant(int32_t variant)
 {
-    if (variant < 0 || variant > 511 || (variant & 3) == 3) return TURBO_ERR_INVALID_ARG;
+    if (variant < 0 || variant > 1023 || (variant & 3) == 3) return TURBO_ERR_INVALID_ARG;
     g_variant = variant;
     return TURBO_OK;
 }
@@ -341,7 +341,7 @@ static turbo_status_t run_dp(const turbo_shape_t *shape, int kind, const DpParam
     // of the call can run
     const int grid_mode = kind == RUN_PLAN ? DP_PLAN : DP_SOLVE_GLOBAL;
     if (shape->num_big > 0) {
-        const cudaError_t ge = check_dp_grid(shape, grid_mode, d.num_sms, d.smem_per_cta_optin);
+        const cudaError_t ge = check_dp_grid(shape, grid_mode, d.num_sms, d.smem_per_cta_optin, base.cluster_cap);
         if (ge != cudaSuccess) {
             cudaGetLastError();
             return ge == cudaErrorInvalidConfiguration || ge == cudaErrorCooperativeLaunchTooLarge
@@ -489,6 +489,7 @@ static DpParams base_params(const turbo_shape_t *shape, const turbo_window_t *wi
     P.u16 = (g_variant & 128) ? 1 : 0;                 // NEXT-5 u16 rows: opt-in
     P.u16_count = g_u16_count;
     P.small = (g_variant & 256) ? 0 : 1;
+    P.cluster_cap = (g_variant & 512) ? 0 : TURBO_CLUSTER_CELLS;   // variant 512: the grid kernel only
     P.trace = g_trace;
     P.trace_words = g_trace_words;
     return P;

@@ -797,7 +797,8 @@ __global__ void __launch_bounds__(GRID_THREADS, GRID_CTAS_PER_SM) dp_grid_kernel
         grid.sync();                   // ring cleared; every CTA has read the header
     }
     for (int64_t w = 0; w < P.num_windows; ++w) {
-        if ((int64_t)P.windows[w].budget_bound + 1 <= TURBO_BIG_CELLS) continue;
+        const int64_t cells = (int64_t)P.windows[w].budget_bound + 1;
+        if (cells <= TURBO_BIG_CELLS || cells <= (int64_t)P.cluster_cap) continue;   // (cluster kernel's)
         if (KSEL != 0) {
             grid_window<(KSEL > 0 ? KSEL : 2)>(P, grid, w, bufA, bufB, red, X, step_base, stage_in, stage_out, mbar,
                                                mbar_uses);
@@ -957,9 +958,26 @@ static cudaError_t grid_geometry(const turbo_shape_t *shape, int num_sms, int sm
     return cudaErrorCooperativeLaunchTooLarge;
 }
 
-cudaError_t check_dp_grid(const turbo_shape_t *shape, int mode, int num_sms, int smem_per_cta_max)
+// Which long-window kernels a call launches: the cluster kernel when the long rows start within
+// its cap, the grid kernel when some long row exceeds it (or the cluster path is off).
+static void long_paths(const turbo_shape_t *shape, int32_t cluster_cap, bool *cluster, bool *grid)
+{
+    *cluster = cluster_cap > 0 && shape->num_big > 0;
+    *grid = shape->num_big > 0 && (int64_t)shape->max_budget + 1 > (int64_t)(cluster_cap > 0 ? cluster_cap : 0);
+}
+
+cudaError_t check_dp_grid(const turbo_shape_t *shape, int mode, int num_sms, int smem_per_cta_max,
+                          int32_t cluster_cap)
 {
     (void)mode;
+    bool use_cluster, use_grid;
+    long_paths(shape, cluster_cap, &use_cluster, &use_grid);
+    if (use_cluster) {
+        ClusterLaunch L;
+        const cudaError_t e = cluster_geometry(shape, smem_per_cta_max, &L);
+        if (e != cudaSuccess) return e;
+    }
+    if (!use_grid) return cudaSuccess;
     dp_grid_kernel_t kern;
     int NP;
     int32_t seg;
@@ -967,10 +985,31 @@ cudaError_t check_dp_grid(const turbo_shape_t *shape, int mode, int num_sms, int
     return grid_geometry(shape, num_sms, smem_per_cta_max, &kern, &NP, &seg, &smem);
 }
 
+static cudaError_t launch_grid_kernel(const turbo_shape_t *shape, DpParams P, int num_sms, int smem_per_cta_max,
+                                      cudaStream_t stream);
+
 cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams &P0, int num_sms,
                            int smem_per_cta_max, cudaStream_t stream)
 {
     DpParams P = P0;
+    P.ordered = shape->ordered;
+    bool use_cluster, use_grid;
+    long_paths(shape, P.cluster_cap, &use_cluster, &use_grid);
+    cudaError_t e = cudaSuccess;
+    if (use_cluster && (e = launch_dp_cluster(shape, P, smem_per_cta_max, stream)) != cudaSuccess) return e;
+    if (use_grid && (e = launch_grid_kernel(shape, P, num_sms, smem_per_cta_max, stream)) != cudaSuccess) return e;
+    if (mode == DP_PLAN) return cudaSuccess;
+    // a5 (+ a6): one 512-thread CTA per long window
+    note_launch();
+    long_walk_kernel_t wk = pick_walk(shape->min_exits, shape->max_exits);
+    wk<<<(unsigned)std::min<int64_t>(shape->num_big, 65535), 512, 0, stream>>>(P, shape->num_big);
+    return cudaGetLastError();
+}
+
+// the cooperative grid kernel for the long rows beyond the cluster kernel's cap
+static cudaError_t launch_grid_kernel(const turbo_shape_t *shape, DpParams P, int num_sms, int smem_per_cta_max,
+                                      cudaStream_t stream)
+{
     dp_grid_kernel_t kern;
     int NP;
     int32_t seg;
@@ -988,13 +1027,7 @@ cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams 
     P.grid_max_budget = shape->max_budget;
     void *args[] = {(void *)&P, (void *)&seg, (void *)&span};
     note_launch();
-    e = cudaLaunchCooperativeKernel((const void *)kern, dim3(NP), dim3(GRID_THREADS), args, smem, stream);
-    if (e != cudaSuccess || mode == DP_PLAN) return e;
-    // a5 (+ a6): one 512-thread CTA per long window
-    note_launch();
-    long_walk_kernel_t wk = pick_walk(shape->min_exits, shape->max_exits);
-    wk<<<(unsigned)std::min<int64_t>(shape->num_big, 65535), 512, 0, stream>>>(P, shape->num_big);
-    return cudaGetLastError();
+    return cudaLaunchCooperativeKernel((const void *)kern, dim3(NP), dim3(GRID_THREADS), args, smem, stream);
 }
 
 }  // namespace turbo

@@ -129,6 +129,7 @@ struct DpParams {
     int32_t u16;                   // NEXT-5: u16 rows for the windows that qualify (opt-in: variant bit 128)
     int64_t *u16_count;            // test hook (turbo_debug_u16_counter): windows planned on u16 rows
     int32_t small;                 // <= 4-warp launches may use the 72-register kernels (variant bit 256 clears)
+    int32_t cluster_cap;           // long rows up to this many cells take the cluster kernel (0: none)
 };
 
 // NEXT-3 (PAPER.md:511 buckets of width 0.1; :525 theta'_x from D_f; reading R6): the class of a
@@ -199,7 +200,7 @@ int dp_warps_per_window(const turbo_shape_t *shape);
 // host-only validation (no launch): the class kernel fits its shared memory / the long-window
 // kernel fits shared memory and the cooperative grid fits the device
 cudaError_t check_dp(const turbo_shape_t *shape, int mode, const DpParams &P, int smem_per_cta_max);
-cudaError_t check_dp_grid(const turbo_shape_t *shape, int mode, int num_sms, int smem_per_cta_max);
+cudaError_t check_dp_grid(const turbo_shape_t *shape, int mode, int num_sms, int smem_per_cta_max, int32_t cluster_cap);
 
 // long-window (grid) kernel: scratch = flags (pub/con per CTA + misc) + halo ring
 constexpr int GRID_MAX_CTAS = 512;                 // two CTAs per SM on 148 SMs
@@ -238,6 +239,17 @@ cudaError_t launch_pack(const turbo_shape_t *s, const DpParams &P, int num_sms, 
                         cudaStream_t stream);
 cudaError_t launch_dp_grid(const turbo_shape_t *shape, int mode, const DpParams &P, int num_sms,
                            int smem_per_cta_max, cudaStream_t stream);
+// cluster kernel for long rows up to TURBO_CLUSTER_CELLS cells (dp_cluster.cu)
+struct ClusterLaunch {
+    const void *kern;
+    int cs;                 // CTAs per cluster
+    int32_t seg, lg_seg;    // cells per CTA segment (a power of two) and its log2
+    size_t smem;
+    int max_clusters;       // resident clusters on the device
+};
+cudaError_t cluster_geometry(const turbo_shape_t *shape, int smem_per_cta_max, ClusterLaunch *out);
+cudaError_t launch_dp_cluster(const turbo_shape_t *shape, const DpParams &P, int smem_per_cta_max,
+                              cudaStream_t stream);
 size_t dp_smem_bytes(const DpParams &P, int nwarps);
 // cls >= 0: only the windows of that row-size class (the others were walked elsewhere)
 // Window selection of a per-class launch: the class's range of the serving order (ordered), or

@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Small cases through every kernel path, for compute-sanitizer (one tool per run):
 the per-class CTA kernels (fused / plan / smem / HBM variants), the runtime-K kernel, the
-lockstep kernel, the long-window grid kernel on both its paths (halo segments and L2 rows) with
+lockstep kernel, the long-row cluster kernel, the long-window grid kernel on both its paths (halo segments and L2 rows) with
 its walk kernel, the u16-row kernels (NEXT-5), turbo_schedule_theta, the batches / latency kernel and
 both NEXT-4 kernels."""
 import os
@@ -23,7 +23,8 @@ def main():
              synth.make_tie_heavy(seed=9, W=64, max_frames=12, max_exits=9, max_budget=700),
              synth.make_config(5, num_windows=24), long2]
     for wl in cases:
-        for fused, variant in ((True, 0), (True, 1), (True, 2), (False, 0), (True, 4), ("all", 0), ("all", 32)):
+        for fused, variant in ((True, 0), (True, 1), (True, 2), (False, 0), (True, 4), ("all", 0), ("all", 32),
+                               (True, 512), ("all", 512)):
             turbo.debug_set_variant(variant)
             b = turbo.batch_from_workload(wl, with_plan_workspace=True)
             turbo.run_path(b, fused=fused)

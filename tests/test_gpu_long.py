@@ -1,6 +1,7 @@
-"""Long windows (rows > TURBO_BIG_CELLS cells) served by the cooperative grid kernel (K4):
-bit-exact parity with the oracle, mixed batches (routing between the CTA and grid kernels)
-and config c4 at full size (3000 frames, B = 2^20)."""
+"""Long windows (rows > TURBO_BIG_CELLS cells): the cluster kernel (rows up to TURBO_CLUSTER_CELLS,
+one thread-block cluster per window, dp_cluster.cu) and the cooperative grid kernel (longer rows,
+and every long row with variant 512), bit-exact against the oracle; mixed batches (routing
+between the CTA, cluster and grid kernels) and config c4 at full size (3000 frames, B = 2^20)."""
 import numpy as np
 import pytest
 
@@ -20,21 +21,29 @@ def _lib():
     turbo.load()
 
 
+# 0: long rows up to TURBO_CLUSTER_CELLS on the cluster kernel; 512: every long row on the grid kernel
+LONG = [0, 512]
+LONG_IDS = ["cluster", "grid"]
+
+
+@pytest.mark.parametrize("variant", LONG, ids=LONG_IDS)
 @pytest.mark.parametrize("fused", [True, False, "all"], ids=["solve", "plan+backtrack", "schedule"])
-def test_long_window_paper_profile(fused):
+def test_long_window_paper_profile(fused, variant):
     wl = synth.make_long_window(3, N=120, K=6, B=40000)
-    compare(wl, gpu_run(wl, fused), oracle_run(wl), check_options=fused != "all")
+    compare(wl, gpu_run(wl, fused, variant), oracle_run(wl), check_options=fused != "all")
 
 
+@pytest.mark.parametrize("variant", LONG, ids=LONG_IDS)
 @pytest.mark.parametrize("K", [2, 3, 4, 5, 6, 7, 8, 11, 16])
-def test_long_window_random_rows(K):
+def test_long_window_random_rows(K, variant):
     """Random (non-monotone, negative) gains, costs up to 700, ragged top tile; N not a multiple
     of the backtrack's frames per round (tail rounds)."""
     wl = synth.make_long_window(10 + K, N=90 + K % 5, K=K, B=30001 + 37 * K, c_max=700, random_rows=True)
-    compare(wl, gpu_run(wl, True), oracle_run(wl))
+    compare(wl, gpu_run(wl, True, variant), oracle_run(wl))
 
 
-def test_mixed_batch_routes_small_and_long_windows():
+@pytest.mark.parametrize("variant", LONG, ids=LONG_IDS)
+def test_mixed_batch_routes_small_and_long_windows(variant):
     parts = [synth.make_config(2, num_windows=40), synth.make_long_window(5, N=64, K=5, B=50000),
              synth.make_config(1), synth.make_long_window(6, N=40, K=5, B=26000, c_max=3000)]
     for p in parts:
@@ -42,20 +51,21 @@ def test_mixed_batch_routes_small_and_long_windows():
         p.capacity = (p.budget.astype(np.int64) + p.num_frames.astype(np.int64) * 84).astype(np.int32)
     wl = synth.concat_workloads(parts)
     for fused in (True, False):
-        compare(wl, gpu_run(wl, fused), oracle_run(wl))
-    # turbo_schedule: the long windows go to the grid kernel with a1/a2/a6 fused into it
-    compare(wl, gpu_run(wl, "all"), oracle_run(wl), check_options=False)
+        compare(wl, gpu_run(wl, fused, variant), oracle_run(wl))
+    # turbo_schedule: the long windows go to the cluster / grid kernel with a1/a2/a6 fused into it
+    compare(wl, gpu_run(wl, "all", variant), oracle_run(wl), check_options=False)
 
 
+@pytest.mark.parametrize("variant", LONG, ids=LONG_IDS)
 @pytest.mark.parametrize("fused", [True, False, "all"], ids=["solve", "plan+backtrack", "schedule"])
-def test_long_windows_a1_edges(fused):
+def test_long_windows_a1_edges(fused, variant):
     """a1 on long windows: clamped (budget 0), under-bound and exact-fit capacities."""
     parts = [synth.make_long_window(40 + s, N=20 + 7 * s, K=4 + s, B=30000 + 999 * s, c_max=600, random_rows=True)
              for s in range(6)]
     wl = synth.with_budget_edges(synth.concat_workloads(parts), seed=3)
     want = oracle_run(wl)
     assert (want["budget"] < wl.budget).any()
-    compare(wl, gpu_run(wl, fused), want, check_options=fused != "all")
+    compare(wl, gpu_run(wl, fused, variant), want, check_options=fused != "all")
 
 
 @pytest.mark.parametrize("fused", [True, "all"], ids=["lookup+solve+stats", "schedule"])
@@ -88,8 +98,9 @@ def test_graph_replay_with_changed_inputs(fused):
         compare(cur, got, oracle_run(cur), check_options=fused != "all")
 
 
+@pytest.mark.parametrize("variant", LONG, ids=LONG_IDS)
 @pytest.mark.parametrize("fused", [True, False, "all"], ids=["solve", "plan+backtrack", "schedule"])
-def test_long_window_costs_beyond_the_halo(fused):
+def test_long_window_costs_beyond_the_halo(fused, variant):
     """Option costs above the halo capacity (TURBO_BIG_MAX_COST cells) take the L2-row path
     (rows in global memory, a grid barrier per frame) -- planned exactly, no longer rejected
     (reading R17). The batch mixes such windows with halo-path windows, K fixed and mixed."""
@@ -99,7 +110,27 @@ def test_long_window_costs_beyond_the_halo(fused):
              synth.make_long_window(10, N=17, K=3, B=27000, c_max=26000, random_rows=True)]
     wl = synth.concat_workloads(parts)
     want = oracle_run(wl)
-    got = gpu_run(wl, fused)
+    got = gpu_run(wl, fused, variant)
+    assert int(got["status"][1]) == -1
+    compare(wl, got, want, check_options=fused != "all")
+
+
+@pytest.mark.parametrize("fused", [True, False, "all"], ids=["solve", "plan+backtrack", "schedule"])
+def test_cluster_kernel_edges(fused):
+    """The cluster kernel at its edges, in ONE batch with grid-kernel rows: rows of exactly
+    TURBO_CLUSTER_CELLS cells (8 CTAs of 16,384 cells) and one cell more (grid kernel), the smallest
+    long row (24,577 cells), costs reaching several segments down and below cell 0, every segment
+    size (4,096 / 8,192 / 16,384 cells), tie-heavy rows, and more long windows than clusters."""
+    parts = [synth.make_long_window(81, N=9, K=5, B=131071, c_max=40000, random_rows=True),
+             synth.make_long_window(82, N=7, K=4, B=131072, c_max=3000, random_rows=True),
+             synth.make_long_window(83, N=33, K=6, B=24576, c_max=24000, random_rows=True),
+             synth.make_long_window(84, N=21, K=3, B=65535, c_max=65000, random_rows=True),
+             synth.make_long_window(85, N=12, K=8, B=32767, c_max=9000, random_rows=True)]
+    parts += [synth.make_long_window(90 + s, N=5 + s % 7, K=2 + s % 15, B=24577 + 2311 * s, c_max=50 + 97 * s,
+                                     random_rows=s % 2 == 1) for s in range(40)]
+    wl = synth.concat_workloads(parts)
+    want = oracle_run(wl)
+    got = gpu_run(wl, fused, 0)
     assert int(got["status"][1]) == -1
     compare(wl, got, want, check_options=fused != "all")
 
