@@ -28,6 +28,11 @@ namespace cg = cooperative_groups;
 namespace turbo {
 
 constexpr int CL_THREADS = 512;
+// fixed-K instantiations: two CTAs per SM (64 registers; a few spilled words) -- same box, 64 windows
+// x 300 frames x 60,000 cells: 4.62 -> 3.03 ms; 148 x 30,000: 8.53 -> 6.47 ms (384 x 2 and 256 x 3
+// won on the first and lost on the second: 16 tiles per segment over 12 / 8 warps). The mixed-K
+// instantiation keeps 128 registers, one CTA per SM.
+constexpr int CL_MINB_FIXED = 2;
 constexpr int CL_MAX = 8;                  // portable cluster size
 constexpr int CL_NX = 5;                   // per-rank exchange words: bad, g0, c0, asum, cmax
 constexpr int CL_XCH = CL_MAX * CL_NX + 8; // exchange words (rank 0's copy is the cluster's)
@@ -289,7 +294,7 @@ __device__ __noinline__ void cluster_window_call(const DpParams &P, cg::cluster_
 // Cluster c serves the long windows r = c, c + clusters, ... (the serving order lists the long
 // windows last, heaviest first); rows beyond `cap` cells are the grid kernel's.
 template <int KSEL>
-__global__ void __launch_bounds__(CL_THREADS, 1) dp_cluster_kernel(DpParams P, int32_t seg, int32_t lg_seg,
+__global__ void __launch_bounds__(CL_THREADS, (KSEL == 0) ? 1 : CL_MINB_FIXED) dp_cluster_kernel(DpParams P, int32_t seg, int32_t lg_seg,
                                                                    int32_t cap, int32_t num_big)
 {
     cg::cluster_group cluster = cg::this_cluster();
@@ -394,9 +399,10 @@ cudaError_t launch_dp_cluster(const turbo_shape_t *shape, const DpParams &P, int
     ClusterLaunch L;
     cudaError_t e = cluster_geometry(shape, smem_per_cta_max, &L);
     if (e != cudaSuccess) return e;
-    // one cluster per long window, at most a few waves of the resident clusters (each cluster
-    // loops over its share of the windows)
-    const int64_t nclus = std::max<int64_t>(1, std::min<int64_t>(shape->num_big, (int64_t)L.max_clusters * 4));
+    // one cluster per long window (the block scheduler starts a cluster as soon as CS SMs free up;
+    // capping the grid at a few waves of resident clusters made some clusters plan two windows
+    // while the others idled: 64 windows on 60 clusters took twice the one-window time)
+    const int64_t nclus = std::max<int64_t>(1, std::min<int64_t>(shape->num_big, (int64_t)(65535 / L.cs)));
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
