@@ -39,6 +39,10 @@ WORKLOADS = {
     "c4": dict(config=4, per_gpu=1, desc="single long window: 3000 frames, K=6, B=2^20 (grid-spanning row; replicas)"),
     "c5": dict(config=5, per_gpu=16384, desc="mixed sweep: K 2-16, B 64-16384, N 30-300, skewed classes; "
                                            "16384 windows (the whole config) per GPU"),
+    # large budgets (not a BASELINE config): a batch of long windows, each planned by one
+    # thread-block cluster (dp_cluster.cu) -- c4-shaped frames and exits at 60,001 cells
+    "lw": dict(config="lw", per_gpu=64, desc="64 long windows x 300 frames, K=6, B=60000 per GPU (one thread-block "
+                                             "cluster per window)"),
     # NEXT-4 (batched latency): the c2 window shape with batch latency tables
     "b2": dict(config="b2", per_gpu=1024, desc="NEXT-4 batched-cost GAP: 1024 windows x 30 frames, K=5, B=1000, "
                                                "I_k(n) = ceil(c_k (2+3n)/5) per GPU"),
@@ -77,6 +81,10 @@ def make_workload(name: str, rank: int, world: int = 1, scaling: str = "weak"):
     if name.startswith("b"):
         return synth.make_batched_config(int(name[1:]), num_windows=spec["per_gpu"],
                                          window_offset=rank * spec["per_gpu"])
+    if name == "lw":                   # replicas of the shape; each rank its own seeded windows
+        n = spec["per_gpu"]
+        return synth.concat_workloads([synth.make_long_window(500 + rank * n + s, N=300, K=6, B=60000)
+                                       for s in range(n)])
     if scaling == "strong":
         from paper_2207_00172_b200.shard import shard_ranges, work_per_window
         whole = synth.CONFIGS[spec["config"]]["W"] if spec["config"] in synth.CONFIGS else 16384

@@ -15,7 +15,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "gpurun_out", "round")
 DST = os.path.join(ROOT, "profiles")
 TRAFFIC = {"full_schedule_c2": "c2", "full_schedule_c3": "c3", "full_grid_c4": "c4",
-           "full_schedule_c5_cls3": "c5", "full_batched_b2": "b2"}
+           "full_schedule_c5_cls3": "c5", "full_batched_b2": "b2", "full_cluster_lw": "lw"}
 
 
 def main():

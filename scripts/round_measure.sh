@@ -7,7 +7,7 @@ cd "${GRAFT_REPO_ROOT:-/root/repo}"
 mkdir -p gpurun_out/round
 R=gpurun_out/round
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $R/gpu.txt 2>&1
-for w in c2 c3 c5 c4 c1; do
+for w in c2 c3 c5 c4 c1 lw; do
   python bench.py --workload $w --steps 20 --warmup 5 --cpu-seconds 8 > $R/bench_$w.json 2> $R/bench_$w.err
 done
 python bench.py --workload b2 --steps 20 --warmup 5 --cpu-seconds 5 > $R/bench_b2.json 2> $R/bench_b2.err
@@ -28,6 +28,7 @@ prof full_grid_c4 c4 'dp_grid_kernel' 1
 prof full_schedule_c5_cls3 c5 'dp_cta_kernel' 3
 prof full_gen_c5_cls2 c5 'dp_gen_kernel' 5
 prof full_batched_b2 b2 'batched_kernel' 2
+prof full_cluster_lw lw 'dp_cluster_kernel' 1
 # summaries on the box (only gpurun_out/ travels back, <= 64 MiB): JSON + CSV, then drop the reports
 python scripts/collect_round.py ${TAG:-r02} $R/collected > $R/collect.log 2>&1
 rm -f $R/*.ncu-rep
