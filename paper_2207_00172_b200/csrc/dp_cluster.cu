@@ -20,6 +20,9 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "dp_kernel.cuh"
 
@@ -368,8 +371,6 @@ cudaError_t cluster_geometry(const turbo_shape_t *shape, int smem_per_cta_max, C
     if (e != cudaSuccess) return e;
     const size_t smem = (size_t)8 * (24 + CL_XCH + 3 * CL_MAX) + (size_t)12 * seg;
     if (smem + fa.sharedSizeBytes > (size_t)smem_per_cta_max) return cudaErrorInvalidConfiguration;
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -381,9 +382,26 @@ cudaError_t cluster_geometry(const turbo_shape_t *shape, int smem_per_cta_max, C
     cfg.dynamicSmemBytes = smem;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    // resident clusters: a host-side query, cached per (device, kernel, cluster size, smem)
+    static std::mutex mu;
+    static std::map<std::tuple<int, const void *, int, size_t>, int> cache;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const auto key = std::make_tuple(dev, (const void *)kern, CS, smem);
     int nclusters = 0;
-    e = cudaOccupancyMaxActiveClusters(&nclusters, (const void *)kern, &cfg);
-    if (e != cudaSuccess) return e;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) nclusters = it->second;
+    }
+    if (nclusters == 0) {               // first use of this shape: the smem attribute, then the query
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveClusters(&nclusters, (const void *)kern, &cfg);
+        if (e != cudaSuccess) return e;
+        std::lock_guard<std::mutex> lk(mu);
+        cache[key] = nclusters;
+    }
     if (nclusters < 1) return cudaErrorInvalidConfiguration;
     out->kern = (const void *)kern;
     out->cs = CS;
