@@ -657,12 +657,12 @@ def run_turbo(args):
     per_step = sorted(a.elapsed_time(bb) for a, bb in evs)                          # ms, this rank
     per_dp = sorted(a.elapsed_time(bb) for a, bb in evd)
     t_lk = sum(a.elapsed_time(bb) for a, bb in evl) / args.steps / 1e3
-    turbo.reset_outputs(b)                               # (the lookup graph left status untouched)
-
-    # correctness of the timed run (cheap, rank-local): no status errors
+    # correctness of the timed run (cheap, rank-local): no status errors (checked BEFORE the reset;
+    # the lookup graph leaves status untouched on valid inputs)
     st = b.status.cpu().numpy()
     if st[0] != -1 or st[1] != -1:
         raise RuntimeError(f"status words set during bench: {st}")
+    turbo.reset_outputs(b)
 
     # ---- e2e through the C ABI with HOST buffers (pinned), H2D inputs + D2H results inside
     F = int(b.shape.total_frames)
@@ -812,7 +812,8 @@ def run_turbo(args):
                    "l2": "flushed between timed steps (256 MiB write outside the step events)",
                    "parallelism": f"{args.scaling} dp{N} (windows sharded, NCCL allreduce of stats)",
                    "nccl_ranks": (dist.get_world_size() if dist is not None else 1),
-                   "windows_total": W_total},
+                   "windows_total": W_total,
+                   "stats_reset": "every step, one device copy in front of the kernel (inside the step graph)"},
         "windows_per_s": W_total / t_step,
         "dp_ms": t_dp * 1e3,
         "step_ms_stats": {"median": statistics.median(per_step), "min": per_step[0], "max": per_step[-1],
