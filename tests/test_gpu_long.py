@@ -125,7 +125,9 @@ def test_cluster_kernel_edges(fused):
              synth.make_long_window(82, N=7, K=4, B=131072, c_max=3000, random_rows=True),
              synth.make_long_window(83, N=33, K=6, B=24576, c_max=24000, random_rows=True),
              synth.make_long_window(84, N=21, K=3, B=65535, c_max=65000, random_rows=True),
-             synth.make_long_window(85, N=12, K=8, B=32767, c_max=9000, random_rows=True)]
+             synth.make_long_window(85, N=12, K=8, B=32767, c_max=9000, random_rows=True),
+             synth.make_long_window(86, N=0, K=5, B=40000, c_max=100),            # no frames
+             synth.make_long_window(87, N=1, K=5, B=70000, c_max=69000, random_rows=True)]
     parts += [synth.make_long_window(90 + s, N=5 + s % 7, K=2 + s % 15, B=24577 + 2311 * s, c_max=50 + 97 * s,
                                      random_rows=s % 2 == 1) for s in range(40)]
     wl = synth.concat_workloads(parts)
