@@ -125,10 +125,11 @@ typedef struct {
 #define TURBO_BIG_CELLS 24576
 #define TURBO_BIG_MAX_COST 4096
 /* Long rows up to this many cells are planned by a thread-block CLUSTER per window instead (up to
- * 8 CTAs on neighbouring SMs, each owning a power-of-two segment of the row in shared memory, the
- * cells below a segment read from the lower CTAs' shared memory through distributed shared
- * memory, one cluster barrier per frame, any option cost): many such windows run at once. Longer
- * rows (e.g. 2^20 cells) keep the grid kernel. Same results either way. */
+ * 16 CTAs, each owning a power-of-two segment of the row in shared memory; the top cells of a
+ * segment are pushed into the next CTA's halo through distributed shared memory, costs beyond the
+ * halo read the lower segments directly; one split cluster barrier per frame; any option cost):
+ * many such windows run at once. Longer rows (e.g. 2^20 cells) keep the grid kernel. Same results
+ * either way. */
 #define TURBO_CLUSTER_CELLS 131072
 
 /* Number of int64 words of the status vector written by lookup / plan. */

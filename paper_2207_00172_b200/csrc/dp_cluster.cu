@@ -4,7 +4,7 @@
 // Same recurrence as dp_kernel.cuh (PAPER.md:519-525 with f = sum; readings R1, R7):
 //     S_i[b] = max_{k : c_ik <= b} ( g_ik + S_{i+1}[b - c_ik] ),  frames N-1 .. 0.
 // Rows longer than one CTA's shared memory (budget_bound + 1 > TURBO_BIG_CELLS) up to
-// TURBO_CLUSTER_CELLS cells: CTA r of a cluster of CS (<= 8, portable) owns the segment
+// TURBO_CLUSTER_CELLS cells: CTA r of a cluster of CS (<= 16) owns the segment
 // [r seg, (r + 1) seg) of the row in its shared memory for the whole window.
 // A cell reads cells at or below itself: tiles whose reads stay inside the own segment use plain
 // shared loads; the bottom tiles read the cells below the segment straight from the lower CTAs'
@@ -30,14 +30,15 @@ namespace cg = cooperative_groups;
 
 namespace turbo {
 
-constexpr int CL_THREADS = 512;
-// fixed-K instantiations: two CTAs per SM (64 registers; a few spilled words) -- same box, 64 windows
-// x 300 frames x 60,000 cells: 4.62 -> 3.03 ms; 148 x 30,000: 8.53 -> 6.47 ms (384 x 2 and 256 x 3
-// won on the first and lost on the second: 16 tiles per segment over 12 / 8 warps). The mixed-K
-// instantiation keeps 128 registers, one CTA per SM.
-constexpr int CL_MINB_FIXED = 2;
-constexpr int CL_MAX = 8;                  // portable cluster size
+// 256 threads, fixed-K instantiations up to three CTAs per SM (85 registers, no spills) -- same box,
+// 64 windows x 300 frames x 60,001 cells / 148 x 30,001 cells: 512 x 1 (128 registers) 4.62 / 8.53 ms,
+// 512 x 2 (64 registers, spills) 3.03 / 6.47 ms, with the pushed halo 512 x 2 3.17 / 5.22, 384 x 2
+// 2.52 / 4.75, 256 x 3 2.52 / 3.81 ms. The mixed-K instantiation: one CTA per SM.
+constexpr int CL_THREADS = 256;
+constexpr int CL_MINB_FIXED = 3;
+constexpr int CL_MAX = 16;                 // largest cluster (8 portable, 16 with the opt-in)
 constexpr int CL_NX = 5;                   // per-rank exchange words: bad, g0, c0, asum, cmax
+constexpr int CL_HALO = 1024;              // cells below each segment buffer: the pushed halo
 constexpr int CL_XCH = CL_MAX * CL_NX + 8; // exchange words (rank 0's copy is the cluster's)
 
 __device__ __forceinline__ void cl_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
@@ -179,6 +180,15 @@ __device__ __forceinline__ void cluster_window(const DpParams &P, cg::cluster_gr
     const int32_t nt = max(0, min(seg / TC, live_tiles - t0));
     TCHECK(seg % TC == 0 && (int64_t)CS * seg >= (int64_t)live_tiles * TC);
     for (int32_t x = tid; x < nt * TC; x += nthr) buf[0][x] = 0;         // S_N = 0 (buffer 0)
+    // halos (CL_HALO cells below each buffer): rank 0's are -inf (cells below 0) for good; the
+    // others hold the lower segment's top cells, pushed by its CTA as it computes them (S_N: 0)
+    for (int32_t x = tid; x < CL_HALO; x += nthr) {
+        buf[0][x - CL_HALO] = rank == 0 ? NEG_R : 0;
+        if (rank == 0) {
+            buf[1][x - CL_HALO] = NEG_R;
+            buf[2][x - CL_HALO] = NEG_R;
+        }
+    }
     int32_t my_g = 0, my_c = 0;                    // lane k < K: option k of the next frame (raw)
     if (N > 0 && lane < K) {
         my_g = opt_g(N - 1, lane);
@@ -189,6 +199,11 @@ __device__ __forceinline__ void cluster_window(const DpParams &P, cg::cluster_gr
 
     const int32_t smask = seg - 1;
     const int32_t seg_hi = seg_lo + seg;
+    // cells of the lower segment held locally: rank 0 its -inf pad, the others the pushed halo
+    // (the top h_eff cells of the lower segment, h_eff = the window's largest cost, at most CL_HALO)
+    const int32_t h_eff = min(CL_HALO, (cmax_w + 31) & ~31);
+    const int32_t lo_local = seg_lo - (rank == 0 ? CL_HALO : h_eff);
+    const bool push = rank + 1 < CS && h_eff > 0;
     int m = 0;                                     // buffer holding S_{i+1}; S_i goes to (m + 1) % 3
     int32_t key[RPT];
     for (int32_t f = 0; f < N; ++f) {
@@ -211,11 +226,13 @@ __device__ __forceinline__ void cluster_window(const DpParams &P, cg::cluster_gr
 #pragma unroll
         for (int k = 1; k < K; ++k) cmax = max(cmax, cc[k]);
         // a tile is SAFE when its reads stay in the own segment and no higher segment reads its
-        // cells (the top c_max cells): it may run before the barrier of the previous frame
+        // cells directly (the upper neighbour reads its pushed halo copy, unless the window has
+        // costs beyond the halo): it may run before the barrier of the previous frame
+        int32_t *nbh = push ? base[mw][rank + 1] : nullptr;     // upper neighbour's buffer (DSMEM)
         auto tile = [&](int32_t t) {
             const int32_t b_lo = t * TC;           // global cell of the tile's first row
             const int32_t lb = b_lo - seg_lo;      // its local index
-            if (b_lo - cmax >= seg_lo) {           // every read inside the own segment
+            if (b_lo - cmax >= lo_local) {         // every read in the own segment or its halo
                 tile_keys_fast<K, RPT>(cur + lane, lb, gp, cc, key);
             } else {
 #pragma unroll
@@ -225,7 +242,11 @@ __device__ __forceinline__ void cluster_window(const DpParams &P, cg::cluster_gr
                     const int32_t c = cc[k];
                     const int32_t x0 = b_lo - c;   // the option's first read
                     const int32_t q0 = x0 >> lg_seg, q1 = (x0 + TC - 1) >> lg_seg;
-                    if (x0 >= 0 && q0 == q1) {     // one segment (own or lower): one base pointer
+                    if (x0 >= lo_local) {          // own segment or halo
+                        const int32_t *__restrict__ s = cur + (x0 - seg_lo) + lane;
+#pragma unroll
+                        for (int r = 0; r < RPT; ++r) key[r] = max_plus(s[r * 32], gp[k], key[r]);
+                    } else if (x0 >= 0 && q0 == q1) {   // one lower segment: one base pointer
                         const int32_t *__restrict__ s = (q0 == rank ? cur : cb[q0]) + (x0 & smask) + lane;
 #pragma unroll
                         for (int r = 0; r < RPT; ++r) key[r] = max_plus(s[r * 32], gp[k], key[r]);
@@ -245,8 +266,19 @@ __device__ __forceinline__ void cluster_window(const DpParams &P, cg::cluster_gr
             for (int r = 0; r < RPT; ++r) dst[r * 32] = key[r] & ~15;
             TCHECK(t < gtiles);
             gch[((int64_t)i * gtiles + t) * 32 + lane] = pack_choices<RPT, CB>(key);
+            if (push && b_lo + TC > seg_hi - h_eff) {    // top cells -> the upper neighbour's halo
+                for (int r = 0; r < RPT; ++r) {          // (read back: key[] is dead by now)
+                    const int32_t x = b_lo + r * 32 + lane;
+                    if (x >= seg_hi - h_eff) nbh[x - seg_hi] = dst[r * 32];
+                }
+            }
         };
-        auto safe = [&](int32_t t) { return t * TC - cmax >= seg_lo && t * TC + TC <= seg_hi - cmax_w; };
+        // (the pushed halo of this frame is only complete after the barrier: a tile reading it is
+        // not safe; rank 0's halo is the constant -inf pad)
+        const int32_t safe_lo = rank == 0 ? lo_local : seg_lo;
+        auto safe = [&](int32_t t) {
+            return t * TC - cmax >= safe_lo && (cmax_w <= h_eff || t * TC + TC <= seg_hi - cmax_w);
+        };
         __syncthreads();                           // the own S_{i+1} (previous frame) complete
         for (int32_t tl = warp; tl < nt; tl += nwarps)
             if (safe(t0 + tl)) tile(t0 + tl);
@@ -305,10 +337,10 @@ __global__ void __launch_bounds__(CL_THREADS, (KSEL == 0) ? 1 : CL_MINB_FIXED) d
     long long *red = reinterpret_cast<long long *>(smem_raw);            // 16 scratch + 8 results
     long long *xch = red + 24;                                           // CL_XCH words
     int32_t *(*base)[CL_MAX] = reinterpret_cast<int32_t *(*)[CL_MAX]>(xch + CL_XCH);   // [3][CL_MAX]
-    int32_t *buf[3];
-    buf[0] = reinterpret_cast<int32_t *>(base + 3);
-    buf[1] = buf[0] + seg;
-    buf[2] = buf[1] + seg;
+    int32_t *buf[3];                               // [CL_HALO halo][seg cells] each
+    buf[0] = reinterpret_cast<int32_t *>(base + 3) + CL_HALO;
+    buf[1] = buf[0] + CL_HALO + seg;
+    buf[2] = buf[1] + CL_HALO + seg;
     const int CS = (int)cluster.num_blocks();
     if (threadIdx.x < (unsigned)CS)
         for (int mm = 0; mm < 3; ++mm) base[mm][threadIdx.x] = cluster.map_shared_rank(buf[mm], (int)threadIdx.x);
@@ -353,23 +385,16 @@ static dp_cluster_kernel_t pick_cluster(int kmin, int kmax)
     return dp_cluster_kernel<0>;
 }
 
-// Geometry of the cluster launch for the long windows of `shape` up to TURBO_CLUSTER_CELLS cells:
-// segment seg (a power of two >= 4096 cells, so CS = ceil(cells / seg) <= 8), shared memory, and
-// the host-only checks (shared memory incl. the static part, at least one resident cluster).
-cudaError_t cluster_geometry(const turbo_shape_t *shape, int smem_per_cta_max, ClusterLaunch *out)
+// One candidate launch shape: segment seg (2^lg cells) and CS CTAs per cluster; sets the kernel's
+// shared-memory (and, CS > 8, non-portable cluster size) attributes and asks for the resident
+// clusters (cached per shape). cudaErrorInvalidConfiguration when no such cluster fits.
+static cudaError_t try_geometry(dp_cluster_kernel_t kern, int32_t seg, int32_t lg, int CS, int smem_per_cta_max,
+                                ClusterLaunch *out)
 {
-    const int64_t cells = std::min<int64_t>((int64_t)shape->max_budget + 1, TURBO_CLUSTER_CELLS);
-    int32_t seg = 4096, lg = 12;
-    while ((int64_t)seg * CL_MAX < cells) {
-        seg *= 2;
-        ++lg;
-    }
-    const int CS = (int)((cells + seg - 1) / seg);
-    dp_cluster_kernel_t kern = pick_cluster(shape->min_exits, shape->max_exits);
     cudaFuncAttributes fa;
     cudaError_t e = cudaFuncGetAttributes(&fa, kern);
     if (e != cudaSuccess) return e;
-    const size_t smem = (size_t)8 * (24 + CL_XCH + 3 * CL_MAX) + (size_t)12 * seg;
+    const size_t smem = (size_t)8 * (24 + CL_XCH + 3 * CL_MAX) + (size_t)12 * (seg + CL_HALO);
     if (smem + fa.sharedSizeBytes > (size_t)smem_per_cta_max) return cudaErrorInvalidConfiguration;
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
@@ -388,17 +413,20 @@ cudaError_t cluster_geometry(const turbo_shape_t *shape, int smem_per_cta_max, C
     int dev = 0;
     cudaGetDevice(&dev);
     const auto key = std::make_tuple(dev, (const void *)kern, CS, smem);
-    int nclusters = 0;
+    int nclusters = -1;
     {
         std::lock_guard<std::mutex> lk(mu);
         auto it = cache.find(key);
         if (it != cache.end()) nclusters = it->second;
     }
-    if (nclusters == 0) {               // first use of this shape: the smem attribute, then the query
+    if (nclusters < 0) {                // first use of this shape: the attributes, then the query
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveClusters(&nclusters, (const void *)kern, &cfg);
-        if (e != cudaSuccess) return e;
+        if (e == cudaSuccess && CS > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e == cudaSuccess) e = cudaOccupancyMaxActiveClusters(&nclusters, (const void *)kern, &cfg);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            nclusters = 0;
+        }
         std::lock_guard<std::mutex> lk(mu);
         cache[key] = nclusters;
     }
@@ -410,6 +438,28 @@ cudaError_t cluster_geometry(const turbo_shape_t *shape, int smem_per_cta_max, C
     out->smem = smem;
     out->max_clusters = nclusters;
     return cudaSuccess;
+}
+
+// Geometry of the cluster launch for the long windows of `shape` up to TURBO_CLUSTER_CELLS cells:
+// rows up to 65,536 cells: a power-of-two segment >= 4,096 cells, CS = ceil(cells / seg) <= 8
+// (portable); longer rows: 8,192-cell segments, 9..16 CTAs (non-portable cluster size, two CTAs
+// per SM), else 16,384-cell segments, <= 8 CTAs (one CTA per SM: 16 x 120,001-cell windows 3.35 vs
+// 2.5 ms). Shared memory incl. the static part and at least one resident cluster are checked here
+// (host only), before any launch.
+cudaError_t cluster_geometry(const turbo_shape_t *shape, int smem_per_cta_max, ClusterLaunch *out)
+{
+    const int64_t cells = std::min<int64_t>((int64_t)shape->max_budget + 1, TURBO_CLUSTER_CELLS);
+    dp_cluster_kernel_t kern = pick_cluster(shape->min_exits, shape->max_exits);
+    if (cells > 8 * 8192) {
+        const int CS = (int)((cells + 8191) / 8192);
+        if (try_geometry(kern, 8192, 13, CS, smem_per_cta_max, out) == cudaSuccess) return cudaSuccess;
+    }
+    int32_t seg = 4096, lg = 12;
+    while ((int64_t)seg * 8 < cells) {
+        seg *= 2;
+        ++lg;
+    }
+    return try_geometry(kern, seg, lg, (int)((cells + seg - 1) / seg), smem_per_cta_max, out);
 }
 
 cudaError_t launch_dp_cluster(const turbo_shape_t *shape, const DpParams &P, int smem_per_cta_max, cudaStream_t stream)
