@@ -26,7 +26,7 @@ prof full_schedule_c2 c2 'dp_cta_kernel' 2
 prof full_schedule_c3 c3 'dp_cta_kernel' 2
 prof full_grid_c4 c4 'dp_grid_kernel' 1
 prof full_schedule_c5_cls3 c5 'dp_cta_kernel' 3
-prof full_gen_c5_cls2 c5 'dp_gen_kernel' 5
+prof full_gen_c5_cls2 c5 'dp_gen_kernel' 3
 prof full_batched_b2 b2 'batched_kernel' 2
 prof full_cluster_lw lw 'dp_cluster_kernel' 1
 # summaries on the box (only gpurun_out/ travels back, <= 64 MiB): JSON + CSV, then drop the reports
