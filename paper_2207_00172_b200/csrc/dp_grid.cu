@@ -239,9 +239,33 @@ __device__ __forceinline__ void backtrack_cta_spec(int32_t N, int32_t b, const u
         for (int k = 0; k < K; ++k) lcv[k] = last ? cost(i0 + d, k) : 0;
     };
     int32_t pcA[D], lcA[K], pcB[D], lcB[K];
+    // the window's largest option cost bounds where the next round's cells can lie
+    __shared__ int32_t cmx_s;
+    if (tid == 0) cmx_s = 0;
+    __syncthreads();
+    {
+        int32_t m = 0;
+        for (int32_t x = tid; x < N * K; x += blockDim.x) m = max(m, cost(x / K, x % K));
+        m = (int32_t)__reduce_max_sync(0xffffffffu, (uint32_t)m);
+        if (lane == 0) atomicMax(&cmx_s, m);
+    }
+    __syncthreads();
+    const int32_t cmx = cmx_s;
     auto round = [&](int32_t i, int par, const int32_t (&pcv)[D], const int32_t (&lcv)[K], int32_t (&pcn)[D],
                      int32_t (&lcn)[K]) -> bool {
         const int32_t dm = min(D, N - i);
+        // the next round's frames: one bulk L2 prefetch (cp.async.bulk.prefetch.L2) per frame of the
+        // tiles its cell can lie in, so the next round's choice reads hit L2 instead of HBM (same
+        // box: c4 6.64 -> 6.43 ms; two rounds ahead the same, three slower; per-line prefetches by
+        // every thread were slower, DESIGN.md dead ends)
+        if (tid < D && i + D + tid < N) {
+            const int32_t fi = i + D + tid;
+            const int32_t lo = max(0, b - (D + tid) * cmx);
+            const int32_t tlo = lo / (32 * RPT), thi = max(b, 0) / (32 * RPT);
+            const uint32_t *a = gch + ((int64_t)fi * gtiles + tlo) * 32;
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"((uint32_t)(thi - tlo + 1) * 128u)
+                         : "memory");
+        }
         if (i + D < N) load_costs(i + D, pcn, lcn);
         int32_t kv[D];
         int32_t bj = b, bd = b;
